@@ -1,0 +1,321 @@
+// C-ABI plumbing: contexts, the immutable device ItemCache (mol.py:216-291) and gating weights.
+#include <mutex>
+
+#include "common.cuh"
+
+namespace molr {
+
+static thread_local std::string g_last_error;
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  cudaError_t e = cudaPointerGetAttributes(&a, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+int finish_outputs(cudaStream_t s, std::initializer_list<Out*> outs) {
+  bool any_host = false;
+  for (Out* o : outs) {
+    if (!o) continue;
+    MOLR_TRY(o->finish(s));
+    any_host |= o->host();
+  }
+  if (any_host) MOLR_CUDA(cudaStreamSynchronize(s));
+  return MOLR_OK;
+}
+
+// ---- storage conversion kernels ---------------------------------------------------------------
+// bf16 storage of f32 values that must be exactly representable; bad |= any rounding.
+__global__ void to_bf16_kernel(const float* __restrict__ x, int64_t n, __nv_bfloat16* __restrict__ hi,
+                               int* __restrict__ bad) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int local_bad = 0;
+  for (; i < n; i += stride) {
+    float v = x[i];
+    __nv_bfloat16 h = __float2bfloat16_rn(v);
+    local_bad |= (__bfloat162float(h) != v);
+    hi[i] = h;
+  }
+  if (local_bad) atomicOr(bad, 1);
+}
+
+}  // namespace molr
+
+using namespace molr;
+
+extern "C" {
+
+const char* molr_last_error(void) { return g_last_error.c_str(); }
+const char* molr_version(void) { return "molr_b200 0.1 (sm_100a)"; }
+
+int molr_ctx_create(int device, molr_ctx** out) {
+  if (!out) MOLR_FAIL(MOLR_ERR_INVALID, "out is null");
+  MOLR_CUDA(cudaSetDevice(device));
+  auto* c = new molr_ctx();
+  c->device = device;
+  cudaDeviceProp prop;
+  MOLR_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10) {
+    delete c;
+    MOLR_FAIL(MOLR_ERR_CUDA, "device %d is sm_%d%d; libmolr_b200 is built for sm_100a only", device,
+              prop.major, prop.minor);
+  }
+  c->num_sms = prop.multiProcessorCount;
+  MOLR_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  // keep freed scratch cached in the pool (stream-ordered allocator)
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  *out = c;
+  return MOLR_OK;
+}
+
+int molr_ctx_destroy(molr_ctx* ctx) {
+  if (!ctx) return MOLR_OK;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return MOLR_OK;
+}
+
+int molr_ctx_sync(molr_ctx* ctx, void* stream) {
+  MOLR_CUDA(cudaStreamSynchronize(pick_stream(ctx, stream)));
+  return MOLR_OK;
+}
+
+int64_t molr_ctx_launch_count(molr_ctx* ctx) { return ctx ? ctx->launches.load() : 0; }
+
+// ---- cache ----------------------------------------------------------------------------------
+int molr_cache_alloc(molr_ctx* ctx, int64_t X, int k_x, int d, int G, int d1, int storage,
+                     molr_cache** out) {
+  if (!ctx || !out) MOLR_FAIL(MOLR_ERR_INVALID, "null argument");
+  if (X < 0 || X >= (int64_t(1) << 31)) MOLR_FAIL(MOLR_ERR_OUT_OF_RANGE, "n_items %lld", (long long)X);
+  if (k_x < 1 || d < 1 || G < 1) MOLR_FAIL(MOLR_ERR_DIMENSION, "bad cache dims");
+  if ((storage & (MOLR_STORE_S1_F32 | MOLR_STORE_S1_INT8)) && d1 < 1)
+    MOLR_FAIL(MOLR_ERR_DIMENSION, "stage-1 dim");
+  if ((storage & MOLR_STORE_S1_INT8) && d1 > 131070)
+    MOLR_FAIL(MOLR_ERR_LENGTH_OVERFLOW, "row length %d exceeds int32-safe bound 131070", d1);
+  MOLR_CUDA(cudaSetDevice(ctx->device));
+  auto* c = new molr_cache();
+  c->ctx = ctx;
+  c->X = X;
+  c->k_x = k_x;
+  c->d = d;
+  c->G = G;
+  c->d1 = d1;
+  c->storage = storage;
+  auto grab = [&](void** p, size_t bytes) -> int {
+    if (bytes == 0) bytes = 16;
+    cudaError_t e = cudaMalloc(p, bytes);
+    if (e != cudaSuccess) {
+      set_error(std::string("cudaMalloc cache: ") + cudaGetErrorString(e));
+      return MOLR_ERR_CUDA;
+    }
+    c->bytes += bytes;
+    return MOLR_OK;
+  };
+  size_t ne = size_t(X) * k_x * d;
+  int st = (storage & MOLR_STORE_EMBS_F32) ? grab((void**)&c->embs_f32, ne * 4) : grab((void**)&c->embs_bf16, ne * 2);
+  if (!st && (storage & MOLR_STORE_GP_F32)) st = grab((void**)&c->gp_f32, size_t(X) * G * 4);
+  if (!st && !(storage & MOLR_STORE_GP_F32)) st = grab((void**)&c->gp_bf16, size_t(X) * G * 2);
+  if (!st && (storage & MOLR_STORE_S1_F32)) st = grab((void**)&c->s1_f32, size_t(X) * d1 * 4);
+  if (!st && (storage & MOLR_STORE_S1_INT8)) st = grab((void**)&c->s1_codes, size_t(X) * d1);
+  if (!st && (storage & MOLR_STORE_S1_INT8)) st = grab((void**)&c->s1_scales, size_t(X) * 4);
+  if (st) {
+    molr_cache_destroy(c);
+    return st;
+  }
+  *out = c;
+  return MOLR_OK;
+}
+
+int molr_cache_fill(molr_cache* c, int64_t row0, int64_t n, const float* embs, const float* gp,
+                    const float* s1, const int8_t* codes, const float* scales, void* stream) {
+  if (!c) MOLR_FAIL(MOLR_ERR_INVALID, "null cache");
+  if (row0 < 0 || n < 0 || row0 + n > c->X) MOLR_FAIL(MOLR_ERR_OUT_OF_RANGE, "fill rows out of range");
+  if (n == 0) return MOLR_OK;
+  molr_ctx* ctx = c->ctx;
+  MOLR_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t s = pick_stream(ctx, stream);
+  Scratch bad;
+  MOLR_TRY(bad.alloc(4, s));
+  MOLR_CUDA(cudaMemsetAsync(bad.p, 0, 4, s));
+  const int64_t per_row = int64_t(c->k_x) * c->d;
+  // chunk so staging of host f32 stays bounded (<= 256 MB per chunk)
+  int64_t chunk = std::max<int64_t>(1, (int64_t(64) << 20) / std::max<int64_t>(per_row, c->G));
+  for (int64_t r = 0; r < n; r += chunk) {
+    int64_t m = std::min(chunk, n - r);
+    if (embs) {
+      size_t off = size_t(row0 + r) * per_row;
+      if (c->embs_f32) {
+        MOLR_CUDA(cudaMemcpyAsync(c->embs_f32 + off, embs + r * per_row, size_t(m * per_row) * 4, cudaMemcpyDefault, s));
+      } else {
+        In e;
+        MOLR_TRY(e.stage(embs + r * per_row, size_t(m * per_row) * 4, s));
+        to_bf16_kernel<<<ctx->num_sms * 8, 256, 0, s>>>(e.as<float>(), m * per_row, c->embs_bf16 + off, bad.as<int>());
+        MOLR_LAUNCHED(ctx);
+      }
+    }
+    if (gp) {
+      size_t off = size_t(row0 + r) * c->G;
+      if (c->gp_f32) {
+        MOLR_CUDA(cudaMemcpyAsync(c->gp_f32 + off, gp + r * c->G, size_t(m) * c->G * 4, cudaMemcpyDefault, s));
+      } else {
+        In e;
+        MOLR_TRY(e.stage(gp + r * c->G, size_t(m) * c->G * 4, s));
+        to_bf16_kernel<<<ctx->num_sms * 8, 256, 0, s>>>(e.as<float>(), m * c->G, c->gp_bf16 + off, bad.as<int>());
+        MOLR_LAUNCHED(ctx);
+      }
+    }
+    if (s1 && c->s1_f32)
+      MOLR_CUDA(cudaMemcpyAsync(c->s1_f32 + size_t(row0 + r) * c->d1, s1 + r * c->d1,
+                                size_t(m) * c->d1 * 4, cudaMemcpyDefault, s));
+    if (codes && c->s1_codes)
+      MOLR_CUDA(cudaMemcpyAsync(c->s1_codes + size_t(row0 + r) * c->d1, codes + r * c->d1,
+                                size_t(m) * c->d1, cudaMemcpyDefault, s));
+    if (scales && c->s1_scales)
+      MOLR_CUDA(cudaMemcpyAsync(c->s1_scales + row0 + r, scales + r, size_t(m) * 4, cudaMemcpyDefault, s));
+  }
+  int hbad = 0;
+  MOLR_CUDA(cudaMemcpyAsync(&hbad, bad.p, 4, cudaMemcpyDeviceToHost, s));
+  MOLR_CUDA(cudaStreamSynchronize(s));
+  if (hbad) MOLR_FAIL(MOLR_ERR_INVALID, "values not representable in the cache's bf16 storage");
+  return MOLR_OK;
+}
+
+// Storage probe: which fields are exactly bf16-representable.
+namespace molr {
+__global__ void bf16_exact_kernel(const float* __restrict__ x, int64_t n, int* __restrict__ bad) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int b = 0;
+  for (; i < n; i += stride) b |= (__float_as_uint(x[i]) & 0xffffu) != 0u;
+  if (__syncthreads_or(b) && threadIdx.x == 0) atomicOr(bad, 1);
+}
+static int probe_bf16(molr_ctx* ctx, const float* x, int64_t n, cudaStream_t s, bool* exact) {
+  Scratch bad;
+  MOLR_TRY(bad.alloc(4, s));
+  MOLR_CUDA(cudaMemsetAsync(bad.p, 0, 4, s));
+  int64_t chunk = int64_t(64) << 20;
+  for (int64_t r = 0; r < n; r += chunk) {
+    int64_t m = std::min(chunk, n - r);
+    In e;
+    MOLR_TRY(e.stage(x + r, size_t(m) * 4, s));
+    bf16_exact_kernel<<<ctx->num_sms * 8, 256, 0, s>>>(e.as<float>(), m, bad.as<int>());
+    MOLR_LAUNCHED(ctx);
+  }
+  int h = 0;
+  MOLR_CUDA(cudaMemcpyAsync(&h, bad.p, 4, cudaMemcpyDeviceToHost, s));
+  MOLR_CUDA(cudaStreamSynchronize(s));
+  *exact = (h == 0);
+  return MOLR_OK;
+}
+}  // namespace molr
+
+int molr_cache_create(molr_ctx* ctx, int64_t X, int k_x, int d, int G, const float* embs,
+                      const float* gp, int d1, const float* s1, const int8_t* codes,
+                      const float* scales, molr_cache** out) {
+  if (!ctx || !out || !embs || !gp) MOLR_FAIL(MOLR_ERR_INVALID, "null argument");
+  MOLR_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t s = ctx->stream;
+  bool e_exact = false, g_exact = false;
+  MOLR_TRY(probe_bf16(ctx, embs, X * k_x * d, s, &e_exact));
+  MOLR_TRY(probe_bf16(ctx, gp, X * G, s, &g_exact));
+  int storage = (e_exact ? 0 : MOLR_STORE_EMBS_F32) | (g_exact ? 0 : MOLR_STORE_GP_F32) |
+                (s1 ? MOLR_STORE_S1_F32 : 0) | ((codes && scales) ? MOLR_STORE_S1_INT8 : 0);
+  molr_cache* c = nullptr;
+  MOLR_TRY(molr_cache_alloc(ctx, X, k_x, d, G, d1, storage, &c));
+  int st = molr_cache_fill(c, 0, X, embs, gp, s1, codes, scales, nullptr);
+  if (st) {
+    molr_cache_destroy(c);
+    return st;
+  }
+  *out = c;
+  return MOLR_OK;
+}
+
+int molr_cache_destroy(molr_cache* c) {
+  if (!c) return MOLR_OK;
+  cudaSetDevice(c->ctx->device);
+  cudaFree(c->embs_bf16);
+  cudaFree(c->embs_f32);
+  cudaFree(c->gp_bf16);
+  cudaFree(c->gp_f32);
+  cudaFree(c->s1_f32);
+  cudaFree(c->s1_codes);
+  cudaFree(c->s1_scales);
+  delete c;
+  return MOLR_OK;
+}
+
+int molr_cache_info(const molr_cache* c, int64_t* X, int* storage, int64_t* bytes) {
+  if (!c) MOLR_FAIL(MOLR_ERR_INVALID, "null cache");
+  if (X) *X = c->X;
+  if (storage) *storage = c->storage;
+  if (bytes) *bytes = c->bytes;
+  return MOLR_OK;
+}
+
+// ---- gating ---------------------------------------------------------------------------------
+int molr_gating_tc_prepare(molr_gating* g);  // mol_tc.cu
+
+int molr_gating_create(molr_ctx* ctx, int G, int H, const float* w1, const float* b1, const float* w2,
+                       int d_u, int H_u, const float* uw1, const float* ub1, const float* uw2,
+                       molr_gating** out) {
+  if (!ctx || !out || !w1 || !b1 || !w2) MOLR_FAIL(MOLR_ERR_INVALID, "null argument");
+  if (G < 1 || H < 1) MOLR_FAIL(MOLR_ERR_DIMENSION, "bad gating dims");
+  MOLR_CUDA(cudaSetDevice(ctx->device));
+  auto* g = new molr_gating();
+  g->ctx = ctx;
+  g->G = G;
+  g->H = H;
+  g->d_u = d_u;
+  g->H_u = H_u;
+  auto up = [&](float** dst, const float* src, size_t n) -> int {
+    if (!src) return MOLR_OK;
+    MOLR_CUDA(cudaMalloc(dst, n * 4));
+    MOLR_CUDA(cudaMemcpy(*dst, src, n * 4, cudaMemcpyDefault));
+    return MOLR_OK;
+  };
+  int st = up(&g->w1, w1, size_t(G) * H);
+  if (!st) st = up(&g->b1, b1, H);
+  if (!st) st = up(&g->w2, w2, size_t(H) * G);
+  if (!st && uw1 && d_u > 0 && H_u > 0) {
+    st = up(&g->uw1, uw1, size_t(d_u) * H_u);
+    if (!st) st = up(&g->ub1, ub1, H_u);
+    if (!st) st = up(&g->uw2, uw2, size_t(H_u) * G);
+  }
+  if (!st) st = molr_gating_tc_prepare(g);
+  if (st) {
+    molr_gating_destroy(g);
+    return st;
+  }
+  *out = g;
+  return MOLR_OK;
+}
+
+int molr_gating_destroy(molr_gating* g) {
+  if (!g) return MOLR_OK;
+  cudaSetDevice(g->ctx->device);
+  cudaFree(g->w1);
+  cudaFree(g->b1);
+  cudaFree(g->w2);
+  cudaFree(g->uw1);
+  cudaFree(g->ub1);
+  cudaFree(g->uw2);
+  cudaFree(g->w1t_bf16);
+  cudaFree(g->w2t_bf16);
+  delete g;
+  return MOLR_OK;
+}
+
+}  // extern "C"

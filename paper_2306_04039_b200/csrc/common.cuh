@@ -1,0 +1,237 @@
+// Shared host/device plumbing for libmolr_b200: status handling, UVA staging of host buffers,
+// stream-ordered scratch, orderable keys, bf16 helpers.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/molr_b200.h"
+
+namespace molr {
+
+// ------------------------------------------------------------------------------------------
+// status
+// ------------------------------------------------------------------------------------------
+void set_error(const std::string& msg);
+
+struct Status {
+  int code = MOLR_OK;
+  bool ok() const { return code == MOLR_OK; }
+};
+
+#define MOLR_FAIL(code_, ...)                                   \
+  do {                                                         \
+    char _b[512];                                              \
+    snprintf(_b, sizeof(_b), __VA_ARGS__);                     \
+    ::molr::set_error(_b);                                     \
+    return (code_);                                            \
+  } while (0)
+
+#define MOLR_CUDA(expr)                                                                   \
+  do {                                                                                   \
+    cudaError_t _e = (expr);                                                             \
+    if (_e != cudaSuccess) {                                                             \
+      MOLR_FAIL(MOLR_ERR_CUDA, "%s:%d %s: %s", __FILE__, __LINE__, #expr,                 \
+                cudaGetErrorString(_e));                                                 \
+    }                                                                                    \
+  } while (0)
+
+#define MOLR_TRY(expr)            \
+  do {                            \
+    int _s = (expr);              \
+    if (_s != MOLR_OK) return _s; \
+  } while (0)
+
+#define MOLR_LAUNCHED(ctx)                                                               \
+  do {                                                                                   \
+    (ctx)->launches.fetch_add(1, std::memory_order_relaxed);                              \
+    cudaError_t _e = cudaGetLastError();                                                 \
+    if (_e != cudaSuccess)                                                               \
+      MOLR_FAIL(MOLR_ERR_CUDA, "%s:%d launch: %s", __FILE__, __LINE__,                    \
+                cudaGetErrorString(_e));                                                 \
+  } while (0)
+
+}  // namespace molr
+
+// ------------------------------------------------------------------------------------------
+// handles
+// ------------------------------------------------------------------------------------------
+struct molr_ctx {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  std::atomic<int64_t> launches{0};
+};
+
+struct molr_cache {
+  molr_ctx* ctx = nullptr;
+  int64_t X = 0;
+  int k_x = 0, d = 0, G = 0, d1 = 0;
+  int storage = 0;                     // molr_storage bits
+  __nv_bfloat16* embs_bf16 = nullptr;  // (X, k_x, d) when bf16-exact
+  float* embs_f32 = nullptr;           // (X, k_x, d) otherwise
+  __nv_bfloat16* gp_bf16 = nullptr;    // (X, G) when bf16-exact
+  float* gp_f32 = nullptr;             // (X, G) otherwise
+  float* s1_f32 = nullptr;             // (X, d1)
+  int8_t* s1_codes = nullptr;          // (X, d1)
+  float* s1_scales = nullptr;          // (X,)
+  int64_t bytes = 0;
+};
+
+struct molr_gating {
+  molr_ctx* ctx = nullptr;
+  int G = 0, H = 0, d_u = 0, H_u = 0;
+  float* w1 = nullptr;  // (G, H)
+  float* b1 = nullptr;  // (H,)
+  float* w2 = nullptr;  // (H, G)
+  float* uw1 = nullptr; // (d_u, H_u)
+  float* ub1 = nullptr;
+  float* uw2 = nullptr; // (H_u, G)
+  // tensor-core operand images (bf16, K-major, built at creation; see mol_tc.cu)
+  __nv_bfloat16* w1t_bf16 = nullptr;  // (H, Kpad) : W1^T with b1 hi/lo folded as extra K rows
+  __nv_bfloat16* w2t_bf16 = nullptr;  // (G, H)    : W2^T
+};
+
+namespace molr {
+
+inline cudaStream_t pick_stream(molr_ctx* ctx, void* s) {
+  return s ? reinterpret_cast<cudaStream_t>(s) : ctx->stream;
+}
+
+// True if the kernel can dereference p directly (device or managed memory).
+bool is_device_ptr(const void* p);
+
+// Stream-ordered scratch that frees itself.
+struct Scratch {
+  void* p = nullptr;
+  cudaStream_t s = nullptr;
+  Scratch() = default;
+  Scratch(const Scratch&) = delete;
+  Scratch& operator=(const Scratch&) = delete;
+  ~Scratch() {
+    if (p) cudaFreeAsync(p, s);
+  }
+  int alloc(size_t bytes, cudaStream_t stream) {
+    s = stream;
+    if (bytes == 0) bytes = 16;
+    cudaError_t e = cudaMallocAsync(&p, bytes, stream);
+    if (e != cudaSuccess) {
+      p = nullptr;
+      set_error(std::string("cudaMallocAsync: ") + cudaGetErrorString(e));
+      return MOLR_ERR_CUDA;
+    }
+    return MOLR_OK;
+  }
+  void reset() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+  }
+  template <class T>
+  T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+// Input view: device pointer to `bytes` of data from a host-or-device pointer.
+struct In {
+  const void* dptr = nullptr;
+  Scratch buf;
+  int stage(const void* src, size_t bytes, cudaStream_t s) {
+    if (src == nullptr || bytes == 0 || is_device_ptr(src)) {
+      dptr = src;
+      return MOLR_OK;
+    }
+    int st = buf.alloc(bytes, s);
+    if (st) return st;
+    cudaError_t e = cudaMemcpyAsync(buf.p, src, bytes, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) {
+      set_error(std::string("H2D: ") + cudaGetErrorString(e));
+      return MOLR_ERR_CUDA;
+    }
+    dptr = buf.p;
+    return MOLR_OK;
+  }
+  template <class T>
+  const T* as() const { return reinterpret_cast<const T*>(dptr); }
+};
+
+// Output view: device buffer written by kernels; finish() copies back to a host destination.
+struct Out {
+  void* user = nullptr;
+  void* dptr = nullptr;
+  size_t bytes = 0;
+  Scratch buf;
+  int stage(void* dst, size_t nbytes, cudaStream_t s) {
+    user = dst;
+    bytes = nbytes;
+    if (dst == nullptr || nbytes == 0 || is_device_ptr(dst)) {
+      dptr = dst;
+      return MOLR_OK;
+    }
+    int st = buf.alloc(nbytes, s);
+    if (st) return st;
+    dptr = buf.p;
+    return MOLR_OK;
+  }
+  int finish(cudaStream_t s) {
+    if (dptr != user && user != nullptr && bytes) {
+      cudaError_t e = cudaMemcpyAsync(user, dptr, bytes, cudaMemcpyDeviceToHost, s);
+      if (e != cudaSuccess) {
+        set_error(std::string("D2H: ") + cudaGetErrorString(e));
+        return MOLR_ERR_CUDA;
+      }
+    }
+    return MOLR_OK;
+  }
+  bool host() const { return dptr != user; }
+  template <class T>
+  T* as() const { return reinterpret_cast<T*>(dptr); }
+};
+
+// Synchronise when any output lives in host memory (the call must return with it filled).
+int finish_outputs(cudaStream_t s, std::initializer_list<Out*> outs);
+
+// ------------------------------------------------------------------------------------------
+// device helpers
+// ------------------------------------------------------------------------------------------
+// Monotone map float -> uint32: a < b (as floats, no NaN) <=> key(a) < key(b).
+__host__ __device__ __forceinline__ uint32_t f32_key(float f) {
+  uint32_t u;
+#ifdef __CUDA_ARCH__
+  u = __float_as_uint(f);
+#else
+  memcpy(&u, &f, 4);
+#endif
+  if (u == 0x80000000u) u = 0u;  // -0 == +0 as floats: same key
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__host__ __device__ __forceinline__ float key_f32(uint32_t k) {
+  uint32_t u = (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
+  float f;
+#ifdef __CUDA_ARCH__
+  f = __uint_as_float(u);
+#else
+  memcpy(&f, &u, 4);
+#endif
+  return f;
+}
+__host__ __device__ __forceinline__ uint32_t i32_key(int32_t v) { return uint32_t(v) ^ 0x80000000u; }
+__host__ __device__ __forceinline__ int32_t key_i32(uint32_t k) { return int32_t(k ^ 0x80000000u); }
+
+__device__ __forceinline__ float silu_f32(float x) {
+  // x * sigmoid(x) with full-precision expf (reference: x * scipy.special.expit(x))
+  return x / (1.0f + expf(-x));
+}
+
+__host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+__host__ __device__ __forceinline__ int64_t imax64(int64_t a, int64_t b) { return a > b ? a : b; }
+
+inline int div_up(int64_t a, int64_t b) { return int((a + b - 1) / b); }
+
+}  // namespace molr

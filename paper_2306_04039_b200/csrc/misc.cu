@@ -1,0 +1,199 @@
+// Small exact elementwise/reduction kernels behind the cache build and the drop-in API:
+// l2_normalize_rows (numerics.py:41-50), stage-1 mean (mol.py:318), dequantize (quant.py:45-46),
+// cache read-back, estimate_threshold (hindexer.py:115-132).
+#include <algorithm>
+
+#include "kernels.cuh"
+#include "stage1.cuh"
+
+namespace molr {
+
+// NumPy's pairwise summation for a contiguous row (numpy/_core/src/umath/loops_utils.h.src):
+// n < 8: sequential; n <= 128: eight strided partial sums combined ((0+1)+(2+3))+((4+5)+(6+7))
+// plus a sequential tail; larger n: split at n/2 rounded down to a multiple of 8 and recurse.
+__device__ float np_pairwise_sumsq(const float* a, int n) {
+  if (n < 8) {
+    float r = 0.f;
+    for (int i = 0; i < n; ++i) r += a[i] * a[i];
+    return r;
+  }
+  if (n <= 128) {
+    float r[8];
+    for (int j = 0; j < 8; ++j) r[j] = a[j] * a[j];
+    int i;
+    for (i = 8; i < n - (n % 8); i += 8)
+      for (int j = 0; j < 8; ++j) r[j] += a[i + j] * a[i + j];
+    float res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+    for (; i < n; ++i) res += a[i] * a[i];
+    return res;
+  }
+  int n2 = n / 2;
+  n2 -= n2 % 8;
+  return np_pairwise_sumsq(a, n2) + np_pairwise_sumsq(a + n2, n - n2);
+}
+
+__global__ void l2norm_kernel(int64_t rows, int dim, const float* __restrict__ x, float eps, float* __restrict__ out,
+                              int* __restrict__ bad) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+    const float* xr = x + r * dim;
+    float nrm = __fsqrt_rn(np_pairwise_sumsq(xr, dim));
+    if (!(nrm > eps)) atomicOr(bad, 1);
+    for (int k = 0; k < dim; ++k) out[r * dim + k] = __fdiv_rn(xr[k], nrm);
+  }
+}
+
+__global__ void mean_mid_kernel(int64_t n, int k, int d, const float* __restrict__ x, float* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * d; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = i / d, c = i % d;
+    float acc = x[(r * k) * d + c];
+    for (int a = 1; a < k; ++a) acc = __fadd_rn(acc, x[(r * k + a) * d + c]);
+    out[i] = __fdiv_rn(acc, (float)k);
+  }
+}
+
+__global__ void dequant_kernel(int64_t rows, int dim, const int8_t* __restrict__ c, const float* __restrict__ s,
+                               float* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows * dim; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = __fmul_rn((float)c[i], s[i / dim]);
+}
+
+__global__ void bf16_to_f32_kernel(const __nv_bfloat16* __restrict__ a, int64_t n, float* __restrict__ o) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    o[i] = __bfloat162float(a[i]);
+}
+
+static int grid_for(molr_ctx* ctx, int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, ctx->num_sms * 16)); }
+
+}  // namespace molr
+
+using namespace molr;
+
+extern "C" {
+
+int molr_l2_normalize_rows(molr_ctx* ctx, int64_t rows, int dim, const float* x, float eps, float* out, void* stream) {
+  if (!ctx) MOLR_FAIL(MOLR_ERR_INVALID, "null ctx");
+  if (rows < 0 || dim < 1) MOLR_FAIL(MOLR_ERR_DIMENSION, "bad shape");
+  MOLR_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t s = pick_stream(ctx, stream);
+  if (rows == 0) return MOLR_OK;
+  In xi;
+  Out o;
+  Scratch bad;
+  MOLR_TRY(xi.stage(x, size_t(rows) * dim * 4, s));
+  MOLR_TRY(o.stage(out, size_t(rows) * dim * 4, s));
+  MOLR_TRY(bad.alloc(4, s));
+  MOLR_CUDA(cudaMemsetAsync(bad.p, 0, 4, s));
+  l2norm_kernel<<<grid_for(ctx, rows), 256, 0, s>>>(rows, dim, xi.as<float>(), eps, o.as<float>(), bad.as<int>());
+  MOLR_LAUNCHED(ctx);
+  int hb = 0;
+  MOLR_CUDA(cudaMemcpyAsync(&hb, bad.p, 4, cudaMemcpyDeviceToHost, s));
+  MOLR_TRY(finish_outputs(s, {&o}));
+  MOLR_CUDA(cudaStreamSynchronize(s));
+  if (hb) MOLR_FAIL(MOLR_ERR_ZERO_NORM, "at least one row has norm <= eps");
+  return MOLR_OK;
+}
+
+int molr_mean_rows(molr_ctx* ctx, int64_t n, int k, int d, const float* x, float* out, void* stream) {
+  if (!ctx) MOLR_FAIL(MOLR_ERR_INVALID, "null ctx");
+  MOLR_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t s = pick_stream(ctx, stream);
+  if (n <= 0) return MOLR_OK;
+  In xi;
+  Out o;
+  MOLR_TRY(xi.stage(x, size_t(n) * k * d * 4, s));
+  MOLR_TRY(o.stage(out, size_t(n) * d * 4, s));
+  mean_mid_kernel<<<grid_for(ctx, n * d), 256, 0, s>>>(n, k, d, xi.as<float>(), o.as<float>());
+  MOLR_LAUNCHED(ctx);
+  return finish_outputs(s, {&o});
+}
+
+int molr_dequantize_rows(molr_ctx* ctx, int64_t rows, int dim, const int8_t* codes, const float* scales, float* out,
+                         void* stream) {
+  if (!ctx) MOLR_FAIL(MOLR_ERR_INVALID, "null ctx");
+  MOLR_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t s = pick_stream(ctx, stream);
+  if (rows <= 0) return MOLR_OK;
+  In c, sc;
+  Out o;
+  MOLR_TRY(c.stage(codes, size_t(rows) * dim, s));
+  MOLR_TRY(sc.stage(scales, size_t(rows) * 4, s));
+  MOLR_TRY(o.stage(out, size_t(rows) * dim * 4, s));
+  dequant_kernel<<<grid_for(ctx, rows * dim), 256, 0, s>>>(rows, dim, c.as<int8_t>(), sc.as<float>(), o.as<float>());
+  MOLR_LAUNCHED(ctx);
+  return finish_outputs(s, {&o});
+}
+
+int molr_cache_read(const molr_cache* c, int64_t row0, int64_t n, float* embs, float* gp, float* s1, int8_t* codes,
+                    float* scales, void* stream) {
+  if (!c) MOLR_FAIL(MOLR_ERR_INVALID, "null cache");
+  if (row0 < 0 || n < 0 || row0 + n > c->X) MOLR_FAIL(MOLR_ERR_OUT_OF_RANGE, "rows out of range");
+  molr_ctx* ctx = c->ctx;
+  MOLR_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t s = pick_stream(ctx, stream);
+  if (n == 0) return MOLR_OK;
+  const int64_t ne = int64_t(c->k_x) * c->d;
+  Out oe, og, os1, oc, osc;
+  if (embs) {
+    MOLR_TRY(oe.stage(embs, size_t(n) * ne * 4, s));
+    if (c->embs_f32)
+      MOLR_CUDA(cudaMemcpyAsync(oe.dptr, c->embs_f32 + row0 * ne, size_t(n) * ne * 4, cudaMemcpyDeviceToDevice, s));
+    else {
+      bf16_to_f32_kernel<<<grid_for(ctx, n * ne), 256, 0, s>>>(c->embs_bf16 + row0 * ne, n * ne, oe.as<float>());
+      MOLR_LAUNCHED(ctx);
+    }
+  }
+  if (gp) {
+    MOLR_TRY(og.stage(gp, size_t(n) * c->G * 4, s));
+    if (c->gp_f32)
+      MOLR_CUDA(cudaMemcpyAsync(og.dptr, c->gp_f32 + row0 * c->G, size_t(n) * c->G * 4, cudaMemcpyDeviceToDevice, s));
+    else {
+      bf16_to_f32_kernel<<<grid_for(ctx, n * c->G), 256, 0, s>>>(c->gp_bf16 + row0 * c->G, n * c->G, og.as<float>());
+      MOLR_LAUNCHED(ctx);
+    }
+  }
+  if (s1 && c->s1_f32) MOLR_CUDA(cudaMemcpyAsync(s1, c->s1_f32 + row0 * c->d1, size_t(n) * c->d1 * 4, cudaMemcpyDefault, s));
+  if (codes && c->s1_codes)
+    MOLR_CUDA(cudaMemcpyAsync(codes, c->s1_codes + row0 * c->d1, size_t(n) * c->d1, cudaMemcpyDefault, s));
+  if (scales && c->s1_scales)
+    MOLR_CUDA(cudaMemcpyAsync(scales, c->s1_scales + row0, size_t(n) * 4, cudaMemcpyDefault, s));
+  MOLR_TRY(finish_outputs(s, {&oe, &og}));
+  MOLR_CUDA(cudaStreamSynchronize(s));
+  return MOLR_OK;
+}
+
+int molr_estimate_threshold(molr_ctx* ctx, const molr_cache* c, int mode, int B, const float* q, int64_t lam,
+                            const int64_t* sample, int64_t n_rank, double* out_t, void* stream) {
+  if (!ctx || !c) MOLR_FAIL(MOLR_ERR_INVALID, "null argument");
+  MOLR_TRY(check_view(c, mode));
+  if (lam < 1 || lam > c->X) MOLR_FAIL(MOLR_ERR_OUT_OF_RANGE, "lambda %lld outside [1, %lld]", (long long)lam,
+                                       (long long)c->X);
+  if (n_rank < 1 || n_rank > lam) MOLR_FAIL(MOLR_ERR_OUT_OF_RANGE, "n=%lld outside [1, %lld]", (long long)n_rank,
+                                            (long long)lam);
+  MOLR_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t s = pick_stream(ctx, stream);
+  if (B <= 0) return MOLR_OK;
+  In qi, si;
+  MOLR_TRY(qi.stage(q, size_t(B) * c->d1 * 4, s));
+  MOLR_TRY(si.stage(sample, size_t(B) * lam * 8, s));
+  Scratch qc, qs, ss, tk;
+  if (mode != MOLR_S1_FLOAT) {
+    MOLR_TRY(qc.alloc(size_t(B) * c->d1, s));
+    MOLR_TRY(qs.alloc(size_t(B) * 4, s));
+    MOLR_TRY(prepare_queries(ctx, mode, B, c->d1, qi.as<float>(), qc.as<int8_t>(), qs.as<float>(), s));
+  }
+  MOLR_TRY(ss.alloc(size_t(B) * lam * 4, s));
+  MOLR_TRY(tk.alloc(size_t(B) * 4, s));
+  for (int b = 0; b < B; ++b) {  // each query has its own sample rows
+    MOLR_TRY(scan_scores(ctx, mode, lam, c->d1, c->s1_f32, c->s1_codes, c->s1_scales, si.as<int64_t>() + size_t(b) * lam,
+                         1, qi.as<float>() + size_t(b) * c->d1, qc.as<int8_t>() ? qc.as<int8_t>() + size_t(b) * c->d1 : nullptr,
+                         ss.as<float>() + size_t(b) * lam, lam, s));
+  }
+  MOLR_TRY(nth_largest_rows(ctx, B, lam, ss.p, mode == MOLR_S1_INT8_RAW, lam, nullptr, 0, n_rank, tk.as<uint32_t>(), s));
+  std::vector<uint32_t> hk(B);
+  MOLR_CUDA(cudaMemcpyAsync(hk.data(), tk.p, size_t(B) * 4, cudaMemcpyDeviceToHost, s));
+  MOLR_CUDA(cudaStreamSynchronize(s));
+  for (int b = 0; b < B; ++b) out_t[b] = mode == MOLR_S1_INT8_RAW ? double(key_i32(hk[b])) : double(key_f32(hk[b]));
+  return MOLR_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,438 @@
+// Cache-level MoL entry points (score_candidates / mol_top_k / batch_score_all, mol.py:329-408),
+// index_select (hindexer.py:181-201) and the fused batched two-stage retrieval
+// (RetrievalEngine.query batched, engine.py:117-138).
+#include <algorithm>
+#include <cmath>
+
+#include "kernels.cuh"
+#include "stage1.cuh"
+
+namespace molr {
+
+// Dispatch: tcgen05 production kernel for the production shape, generic SIMT otherwise.
+template <class Id>
+int mol_score_any(molr_ctx* ctx, const molr_cache* c, const molr_gating* g, int B, int k_u, const float* ue,
+                  const float* uw, float tau, Segs<Id> segs, float* out, int64_t out_ld, cudaStream_t s) {
+  if (mol_tc_supported(c, g, k_u)) return mol_score_tc<Id>(ctx, c, g, B, ue, uw, tau, segs, out, out_ld, s);
+  return mol_score_generic<Id>(ctx, c, g, B, k_u, ue, uw, tau, segs, out, out_ld, s);
+}
+
+// begin[b] = off[b], end[b] = off[b+1]
+__global__ void csr_to_segs_kernel(int B, const int64_t* __restrict__ off, int64_t* __restrict__ beg,
+                                   int64_t* __restrict__ end) {
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < B; b += gridDim.x * blockDim.x) {
+    beg[b] = off[b];
+    end[b] = off[b + 1];
+  }
+}
+
+__global__ void validate_ids_kernel(int64_t n, const int64_t* __restrict__ ids, int64_t X, int* __restrict__ bad) {
+  int b = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    b |= (ids[i] < 0 || ids[i] >= X);
+  if (__syncthreads_or(b) && threadIdx.x == 0) atomicOr(bad, 1);
+}
+
+// mean over k_u component rows -> stage-1 query (engine.py:131; numpy axis-0 reduction is a
+// sequential fp32 sum over rows followed by one division)
+__global__ void s1_query_kernel(int B, int k_u, int d, const float* __restrict__ ue, float* __restrict__ q) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < int64_t(B) * d;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t b = i / d, k = i % d;
+    float acc = ue[(b * k_u) * d + k];
+    for (int a = 1; a < k_u; ++a) acc = __fadd_rn(acc, ue[(b * k_u + a) * d + k]);
+    q[i] = __fdiv_rn(acc, (float)k_u);
+  }
+}
+
+// ---- device sampling: seeded Feistel permutation of [0, X), prefix of length lam -------------
+__device__ __forceinline__ uint32_t mix32(uint32_t h) {
+  h ^= h >> 16;
+  h *= 0x85ebca6bu;
+  h ^= h >> 13;
+  h *= 0xc2b2ae35u;
+  h ^= h >> 16;
+  return h;
+}
+
+__global__ void feistel_sample_kernel(int64_t X, int64_t lam, uint64_t seed, int half_bits, int64_t* __restrict__ out) {
+  const uint32_t mask = (1u << half_bits) - 1u;
+  const uint32_t k0 = mix32(uint32_t(seed) ^ 0x9e3779b9u), k1 = mix32(uint32_t(seed >> 32) ^ 0x7f4a7c15u);
+  const uint32_t keys[4] = {k0, k1, mix32(k0 + 0x632be59bu), mix32(k1 + 0x3c6ef372u)};
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < lam; j += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t x = (uint64_t)j;
+    do {  // cycle-walk until inside [0, X)
+      uint32_t L = uint32_t(x >> half_bits), R = uint32_t(x) & mask;
+      for (int r = 0; r < 4; ++r) {
+        uint32_t nL = R;
+        R = L ^ (mix32(R * 0x9e3779b1u ^ keys[r]) & mask);
+        L = nL;
+      }
+      x = (uint64_t(L) << half_bits) | R;
+    } while (x >= (uint64_t)X);
+    out[j] = (int64_t)x;
+  }
+}
+
+// filter scan: every row against every query; append passers (int32 local ids) per query
+template <int MODE>
+__global__ void __launch_bounds__(256)
+filter_scan_kernel(int64_t n, int dim, const float* __restrict__ vf, const int8_t* __restrict__ codes,
+                   const float* __restrict__ scales, int B, const float* __restrict__ qf,
+                   const int8_t* __restrict__ qc, const uint32_t* __restrict__ tkey, int strict, int64_t cap,
+                   int32_t* __restrict__ cand, int64_t* __restrict__ counts) {
+  extern __shared__ __align__(16) unsigned char sq[];
+  uint32_t* tk = reinterpret_cast<uint32_t*>(sq);
+  unsigned char* qs = sq + ((B * 4 + 15) / 16) * 16;
+  const int qbytes = MODE == MOLR_S1_FLOAT ? B * dim * 4 : B * dim;
+  const unsigned char* src = MODE == MOLR_S1_FLOAT ? (const unsigned char*)qf : (const unsigned char*)qc;
+  for (int i = threadIdx.x; i < qbytes; i += blockDim.x) qs[i] = src[i];
+  for (int i = threadIdx.x; i < B; i += blockDim.x) tk[i] = tkey[i];
+  __syncthreads();
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+    for (int b = 0; b < B; ++b) {
+      uint32_t key;
+      if (MODE == MOLR_S1_FLOAT) {
+        const float* v = vf + r * dim;
+        const float* q = reinterpret_cast<const float*>(qs) + b * dim;
+        float acc = 0.f;
+        for (int k = 0; k < dim; ++k) acc = fmaf(v[k], q[k], acc);
+        key = f32_key(acc);
+      } else {
+        int32_t acc = 0;
+        const int4* cr = reinterpret_cast<const int4*>(codes + r * dim);
+        const int4* qq = reinterpret_cast<const int4*>(qs + b * dim);
+        for (int k = 0; k < dim / 16; ++k) {
+          int4 x = cr[k], y = qq[k];
+          acc = __dp4a(x.x, y.x, acc);
+          acc = __dp4a(x.y, y.y, acc);
+          acc = __dp4a(x.z, y.z, acc);
+          acc = __dp4a(x.w, y.w, acc);
+        }
+        key = MODE == MOLR_S1_INT8_RAW ? i32_key(acc) : f32_key(__fmul_rn((float)acc, scales[r]));
+      }
+      bool pass = strict ? key > tk[b] : key >= tk[b];
+      if (pass) {
+        int64_t pos = (int64_t)atomicAdd(reinterpret_cast<unsigned long long*>(counts + b), 1ull);
+        if (pos < cap) cand[int64_t(b) * cap + pos] = (int32_t)r;
+      }
+    }
+  }
+}
+
+__global__ void cap_segs_kernel(int B, int64_t cap, const int64_t* __restrict__ counts, int64_t* __restrict__ beg,
+                                int64_t* __restrict__ end) {
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < B; b += gridDim.x * blockDim.x) {
+    beg[b] = int64_t(b) * cap;
+    end[b] = int64_t(b) * cap + min(counts[b], cap);
+  }
+}
+
+// sort each candidate list so the downstream result never depends on atomic arrival order
+// (scores are per-pair and top-k ties break by id, so this is only for reproducible traces)
+
+}  // namespace molr
+
+using namespace molr;
+
+extern "C" {
+
+static int mol_common_checks(const molr_cache* c, const molr_gating* g, int k_u) {
+  if (!c || !g) MOLR_FAIL(MOLR_ERR_INVALID, "null cache/gating");
+  if (g->G != k_u * c->k_x || c->G != g->G)
+    MOLR_FAIL(MOLR_ERR_DIMENSION, "logit grid mismatch: k_u*k_x=%d, cache G=%d, gating G=%d", k_u * c->k_x, c->G,
+              g->G);
+  return MOLR_OK;
+}
+
+int molr_score(molr_ctx* ctx, const molr_cache* c, const molr_gating* g, int B, int k_u, const float* ue,
+               const float* uw, float tau, const int64_t* off, const int64_t* ids, float* out, void* stream) {
+  if (!ctx) MOLR_FAIL(MOLR_ERR_INVALID, "null ctx");
+  MOLR_TRY(mol_common_checks(c, g, k_u));
+  MOLR_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t s = pick_stream(ctx, stream);
+  if (B <= 0) return MOLR_OK;
+  int64_t total = int64_t(B) * c->X;
+  std::vector<int64_t> hoff;
+  if (off) {
+    hoff.resize(B + 1);
+    MOLR_CUDA(cudaMemcpyAsync(hoff.data(), off, size_t(B + 1) * 8, cudaMemcpyDefault, s));
+    MOLR_CUDA(cudaStreamSynchronize(s));
+    total = hoff[B];
+    for (int b = 0; b < B; ++b)
+      if (hoff[b + 1] - hoff[b] <= 0) MOLR_FAIL(MOLR_ERR_EMPTY_CANDIDATES, "no candidates to score");
+  }
+  In iue, iuw, ioff, iids;
+  MOLR_TRY(iue.stage(ue, size_t(B) * k_u * c->d * 4, s));
+  MOLR_TRY(iuw.stage(uw, size_t(B) * g->G * 4, s));
+  Scratch sb, se, bad;
+  Segs<int64_t> segs;
+  segs.X = c->X;
+  if (off) {
+    MOLR_TRY(ioff.stage(off, size_t(B + 1) * 8, s));
+    MOLR_TRY(iids.stage(ids, size_t(total) * 8, s));
+    MOLR_TRY(sb.alloc(size_t(B) * 8, s));
+    MOLR_TRY(se.alloc(size_t(B) * 8, s));
+    csr_to_segs_kernel<<<div_up(B, 256), 256, 0, s>>>(B, ioff.as<int64_t>(), sb.as<int64_t>(), se.as<int64_t>());
+    MOLR_LAUNCHED(ctx);
+    // ids must lie inside the corpus (mol.py:339-340)
+    MOLR_TRY(bad.alloc(4, s));
+    MOLR_CUDA(cudaMemsetAsync(bad.p, 0, 4, s));
+    validate_ids_kernel<<<std::min(div_up(total, 256), ctx->num_sms * 8), 256, 0, s>>>(total, iids.as<int64_t>(),
+                                                                                       c->X, bad.as<int>());
+    MOLR_LAUNCHED(ctx);
+    int hb = 0;
+    MOLR_CUDA(cudaMemcpyAsync(&hb, bad.p, 4, cudaMemcpyDeviceToHost, s));
+    MOLR_CUDA(cudaStreamSynchronize(s));
+    if (hb) MOLR_FAIL(MOLR_ERR_OUT_OF_RANGE, "candidate id outside the corpus");
+    segs.begin = sb.as<int64_t>();
+    segs.end = se.as<int64_t>();
+    segs.ids = iids.as<int64_t>();
+  }
+  Out o;
+  MOLR_TRY(o.stage(out, size_t(total) * 4, s));
+  MOLR_TRY(mol_score_any<int64_t>(ctx, c, g, B, k_u, iue.as<float>(), iuw.as<float>(), tau, segs, o.as<float>(),
+                                  c->X, s));
+  return finish_outputs(s, {&o});
+}
+
+int molr_mol_top_k(molr_ctx* ctx, const molr_cache* c, const molr_gating* g, int B, int k_u, const float* ue,
+                   const float* uw, float tau, const int64_t* off, const int64_t* ids, int k, int64_t* out_ids,
+                   float* out_scores, void* stream) {
+  if (!ctx) MOLR_FAIL(MOLR_ERR_INVALID, "null ctx");
+  MOLR_TRY(mol_common_checks(c, g, k_u));
+  MOLR_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t s = pick_stream(ctx, stream);
+  if (B <= 0) return MOLR_OK;
+  int64_t total = int64_t(B) * c->X;
+  if (off) {
+    std::vector<int64_t> hoff(B + 1);
+    MOLR_CUDA(cudaMemcpyAsync(hoff.data(), off, size_t(B + 1) * 8, cudaMemcpyDefault, s));
+    MOLR_CUDA(cudaStreamSynchronize(s));
+    total = hoff[B];
+    for (int b = 0; b < B; ++b) {
+      int64_t n = hoff[b + 1] - hoff[b];
+      if (n <= 0) MOLR_FAIL(MOLR_ERR_EMPTY_CANDIDATES, "no candidates to rank");
+      if (k < 1 || k > n) MOLR_FAIL(MOLR_ERR_OUT_OF_RANGE, "k=%d outside [1, %lld]", k, (long long)n);
+    }
+  } else if (k < 1 || k > c->X) {
+    MOLR_FAIL(MOLR_ERR_OUT_OF_RANGE, "k=%d outside [1, %lld]", k, (long long)c->X);
+  }
+  Scratch sc;
+  MOLR_TRY(sc.alloc(size_t(total) * 4, s));
+  MOLR_TRY(molr_score(ctx, c, g, B, k_u, ue, uw, tau, off, ids, sc.as<float>(), s));
+  In ioff, iids;
+  Scratch sb, se;
+  Segs<int64_t> segs;
+  segs.X = c->X;
+  if (off) {
+    MOLR_TRY(ioff.stage(off, size_t(B + 1) * 8, s));
+    MOLR_TRY(iids.stage(ids, size_t(total) * 8, s));
+    MOLR_TRY(sb.alloc(size_t(B) * 8, s));
+    MOLR_TRY(se.alloc(size_t(B) * 8, s));
+    csr_to_segs_kernel<<<div_up(B, 256), 256, 0, s>>>(B, ioff.as<int64_t>(), sb.as<int64_t>(), se.as<int64_t>());
+    MOLR_LAUNCHED(ctx);
+    segs.begin = sb.as<int64_t>();
+    segs.end = se.as<int64_t>();
+    segs.ids = iids.as<int64_t>();
+  }
+  Out oi, os;
+  MOLR_TRY(oi.stage(out_ids, size_t(B) * k * 8, s));
+  MOLR_TRY(os.stage(out_scores, size_t(B) * k * 4, s));
+  MOLR_TRY(segmented_top_k<int64_t>(ctx, B, segs, sc.as<float>(), c->X, k, 0, oi.as<int64_t>(), os.as<float>(), s));
+  return finish_outputs(s, {&oi, &os});
+}
+
+int molr_index_select(molr_ctx* ctx, const molr_cache* c, int64_t n, const int64_t* ids, molr_cache** out) {
+  if (!ctx || !c || !out) MOLR_FAIL(MOLR_ERR_INVALID, "null argument");
+  MOLR_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t s = ctx->stream;
+  molr_cache* r = nullptr;
+  MOLR_TRY(molr_cache_alloc(ctx, n, c->k_x, c->d, c->G, c->d1, c->storage, &r));
+  if (n > 0) {
+    In ii;
+    int st = ii.stage(ids, size_t(n) * 8, s);
+    auto g = [&](const void* src, void* dst, int64_t row_bytes) {
+      if (st == MOLR_OK && src) st = gather_rows(ctx, n, row_bytes, src, ii.as<int64_t>(), dst, s);
+    };
+    g(c->embs_bf16, r->embs_bf16, int64_t(c->k_x) * c->d * 2);
+    g(c->embs_f32, r->embs_f32, int64_t(c->k_x) * c->d * 4);
+    g(c->gp_bf16, r->gp_bf16, int64_t(c->G) * 2);
+    g(c->gp_f32, r->gp_f32, int64_t(c->G) * 4);
+    g(c->s1_f32, r->s1_f32, int64_t(c->d1) * 4);
+    g(c->s1_codes, r->s1_codes, int64_t(c->d1));
+    g(c->s1_scales, r->s1_scales, 4);
+    if (st == MOLR_OK && cudaStreamSynchronize(s) != cudaSuccess) st = MOLR_ERR_CUDA;
+    if (st) {
+      molr_cache_destroy(r);
+      return st;
+    }
+  }
+  *out = r;
+  return MOLR_OK;
+}
+
+// Fused batched two-stage retrieval.  See header.  Steps:
+//  1. stage-1 query = mean of user components; quantize (int8 views)          engine.py:131
+//  2. lam distinct rows from a seeded Feistel permutation prefix (batch-shared) hindexer.py:125
+//  3. sample scores with the same arithmetic as the scan; n-th largest         hindexer.py:156-158
+//  4. scan + threshold filter, passers appended per query                      hindexer.py:155,159-163
+//  5. MoL scoring of each query's passers; fallback to the corpus if < k      engine.py:134-137
+//  6. top-k by (score desc, id asc)                                            mol.py:407
+int molr_two_stage_top_k(molr_ctx* ctx, const molr_cache* c, const molr_gating* g, int B, int k_u, const float* ue,
+                         const float* uw, float tau, int mode, int64_t k_prime, int64_t lam, uint64_t seed,
+                         int comparator, int k, int64_t id_offset, int64_t* out_ids, float* out_scores,
+                         int64_t* out_cand, void* stream) {
+  if (!ctx) MOLR_FAIL(MOLR_ERR_INVALID, "null ctx");
+  MOLR_TRY(mol_common_checks(c, g, k_u));
+  MOLR_TRY(check_view(c, mode));
+  if (c->d1 != c->d) MOLR_FAIL(MOLR_ERR_DIMENSION, "stage-1 dim %d != d %d", c->d1, c->d);
+  if (k_prime < 1) MOLR_FAIL(MOLR_ERR_INVALID, "k_prime must be >= 1");
+  if (k_prime > c->X) MOLR_FAIL(MOLR_ERR_OUT_OF_RANGE, "k_prime %lld exceeds corpus %lld", (long long)k_prime,
+                                (long long)c->X);
+  if (lam < 1 || lam > c->X) MOLR_FAIL(MOLR_ERR_OUT_OF_RANGE, "lambda %lld outside [1, %lld]", (long long)lam,
+                                       (long long)c->X);
+  if (k < 1) MOLR_FAIL(MOLR_ERR_OUT_OF_RANGE, "k=%d", k);
+  if (mode != MOLR_S1_FLOAT && (c->d1 % 16) != 0) MOLR_FAIL(MOLR_ERR_DIMENSION, "int8 batched scan needs d1%%16==0");
+  MOLR_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t s = pick_stream(ctx, stream);
+  if (B <= 0) return MOLR_OK;
+  const int64_t X = c->X;
+  const int kk = (int)imin64(k, X);
+  In iue, iuw;
+  MOLR_TRY(iue.stage(ue, size_t(B) * k_u * c->d * 4, s));
+  MOLR_TRY(iuw.stage(uw, size_t(B) * g->G * 4, s));
+  Out oi, os, oc;
+  MOLR_TRY(oi.stage(out_ids, size_t(B) * k * 8, s));
+  MOLR_TRY(os.stage(out_scores, size_t(B) * k * 4, s));
+  MOLR_TRY(oc.stage(out_cand, out_cand ? size_t(B) * 8 : 0, s));
+  if (kk < k) {  // short corpus: pad the tail
+    MOLR_CUDA(cudaMemsetAsync(oi.dptr, 0xff, size_t(B) * k * 8, s));
+  }
+
+  Segs<int32_t> segs;
+  segs.X = X;
+  Scratch cand, counts, sb, se;
+  std::vector<int64_t> hcnt(B, X);
+  if (k_prime < X) {
+    // 1. queries
+    Scratch q, qc, qs;
+    MOLR_TRY(q.alloc(size_t(B) * c->d * 4, s));
+    s1_query_kernel<<<div_up(int64_t(B) * c->d, 256), 256, 0, s>>>(B, k_u, c->d, iue.as<float>(), q.as<float>());
+    MOLR_LAUNCHED(ctx);
+    if (mode != MOLR_S1_FLOAT) {
+      MOLR_TRY(qc.alloc(size_t(B) * c->d1, s));
+      MOLR_TRY(qs.alloc(size_t(B) * 4, s));
+      MOLR_TRY(prepare_queries(ctx, mode, B, c->d1, q.as<float>(), qc.as<int8_t>(), qs.as<float>(), s));
+    }
+    // 2. sample
+    int bits = 2;
+    while ((int64_t(1) << bits) < X) bits += 2;
+    Scratch samp;
+    MOLR_TRY(samp.alloc(size_t(lam) * 8, s));
+    feistel_sample_kernel<<<std::min(div_up(lam, 256), ctx->num_sms * 8), 256, 0, s>>>(X, lam, seed, bits / 2,
+                                                                                       samp.as<int64_t>());
+    MOLR_LAUNCHED(ctx);
+    // 3. sample scores [B][lam] then n-th largest per query
+    const double nr = std::nearbyint(double(k_prime * lam) / double(X));  // Python round(): half-even
+    const int64_t n_rank = std::max<int64_t>(1, (int64_t)nr);
+    Scratch ss, tkey;
+    MOLR_TRY(ss.alloc(size_t(B) * lam * 4, s));
+    MOLR_TRY(scan_scores(ctx, mode, lam, c->d1, c->s1_f32, c->s1_codes, c->s1_scales, samp.as<int64_t>(), B,
+                         q.as<float>(), qc.as<int8_t>(), ss.p, lam, s));
+    MOLR_TRY(tkey.alloc(size_t(B) * 4, s));
+    MOLR_TRY(nth_largest_rows(ctx, B, lam, ss.p, mode == MOLR_S1_INT8_RAW, lam, nullptr, 0, n_rank,
+                              tkey.as<uint32_t>(), s));
+    // 4. filter scan with capacity; retry once with the exact maximum if it overflowed
+    int64_t cap = imin64(X, k_prime + k_prime / 4 + 1024);
+    MOLR_TRY(counts.alloc(size_t(B) * 8, s));
+    for (int attempt = 0; attempt < 2; ++attempt) {
+      MOLR_TRY(cand.alloc(size_t(B) * cap * 4, s));
+      MOLR_CUDA(cudaMemsetAsync(counts.p, 0, size_t(B) * 8, s));
+      const int qbytes = mode == MOLR_S1_FLOAT ? B * c->d1 * 4 : B * c->d1;
+      const size_t smem = size_t((B * 4 + 15) / 16) * 16 + qbytes;
+      if (smem > 200 * 1024) MOLR_FAIL(MOLR_ERR_OUT_OF_RANGE, "batch %d too large for one scan", B);
+      auto launch = [&](auto kern) -> int {
+        MOLR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int blocks = std::min(div_up(X, 256), ctx->num_sms * std::max(1, int((220 * 1024) / (smem + 1024))));
+        kern<<<blocks, 256, smem, s>>>(X, c->d1, c->s1_f32, c->s1_codes, c->s1_scales, B, q.as<float>(),
+                                       qc.as<int8_t>(), tkey.as<uint32_t>(), comparator == MOLR_STRICT, cap,
+                                       cand.as<int32_t>(), counts.as<int64_t>());
+        MOLR_LAUNCHED(ctx);
+        return MOLR_OK;
+      };
+      if (mode == MOLR_S1_FLOAT) MOLR_TRY(launch(filter_scan_kernel<MOLR_S1_FLOAT>));
+      else if (mode == MOLR_S1_INT8) MOLR_TRY(launch(filter_scan_kernel<MOLR_S1_INT8>));
+      else MOLR_TRY(launch(filter_scan_kernel<MOLR_S1_INT8_RAW>));
+      MOLR_CUDA(cudaMemcpyAsync(hcnt.data(), counts.p, size_t(B) * 8, cudaMemcpyDeviceToHost, s));
+      MOLR_CUDA(cudaStreamSynchronize(s));
+      int64_t mx = *std::max_element(hcnt.begin(), hcnt.end());
+      if (mx <= cap) break;
+      cand.reset();
+      cap = mx;
+    }
+    MOLR_TRY(sb.alloc(size_t(B) * 8, s));
+    MOLR_TRY(se.alloc(size_t(B) * 8, s));
+    cap_segs_kernel<<<div_up(B, 256), 256, 0, s>>>(B, cap, counts.as<int64_t>(), sb.as<int64_t>(), se.as<int64_t>());
+    MOLR_LAUNCHED(ctx);
+    segs.begin = sb.as<int64_t>();
+    segs.end = se.as<int64_t>();
+    segs.ids = cand.as<int32_t>();
+    // 5. MoL over passers; queries with < k passers fall back to the whole corpus (engine.py:134-135)
+    std::vector<int> fallback;
+    for (int b = 0; b < B; ++b)
+      if (hcnt[b] < kk) fallback.push_back(b);
+    int64_t cand_total = int64_t(B) * cap;
+    Scratch sc;
+    MOLR_TRY(sc.alloc(size_t(cand_total) * 4, s));
+    MOLR_TRY(mol_score_any<int32_t>(ctx, c, g, B, k_u, iue.as<float>(), iuw.as<float>(), tau, segs, sc.as<float>(),
+                                    0, s));
+    // 6. top-k per query
+    MOLR_TRY(segmented_top_k<int32_t>(ctx, B, segs, sc.as<float>(), 0, k, id_offset, oi.as<int64_t>(),
+                                      os.as<float>(), s));
+    if (!fallback.empty()) {
+      // dense MoL for the few queries whose candidate set came back smaller than k
+      const int F = (int)fallback.size();
+      Scratch fue, fuw, fsc, fid, fso;
+      MOLR_TRY(fue.alloc(size_t(F) * k_u * c->d * 4, s));
+      MOLR_TRY(fuw.alloc(size_t(F) * g->G * 4, s));
+      for (int i = 0; i < F; ++i) {
+        int b = fallback[i];
+        MOLR_CUDA(cudaMemcpyAsync(fue.as<float>() + size_t(i) * k_u * c->d, iue.as<float>() + size_t(b) * k_u * c->d,
+                                  size_t(k_u) * c->d * 4, cudaMemcpyDeviceToDevice, s));
+        MOLR_CUDA(cudaMemcpyAsync(fuw.as<float>() + size_t(i) * g->G, iuw.as<float>() + size_t(b) * g->G,
+                                  size_t(g->G) * 4, cudaMemcpyDeviceToDevice, s));
+      }
+      MOLR_TRY(fsc.alloc(size_t(F) * X * 4, s));
+      Segs<int32_t> dense;
+      dense.X = X;
+      MOLR_TRY(mol_score_any<int32_t>(ctx, c, g, F, k_u, fue.as<float>(), fuw.as<float>(), tau, dense,
+                                      fsc.as<float>(), X, s));
+      MOLR_TRY(fid.alloc(size_t(F) * k * 8, s));
+      MOLR_TRY(fso.alloc(size_t(F) * k * 4, s));
+      MOLR_TRY(segmented_top_k<int32_t>(ctx, F, dense, fsc.as<float>(), X, k, id_offset, fid.as<int64_t>(),
+                                        fso.as<float>(), s));
+      for (int i = 0; i < F; ++i) {
+        int b = fallback[i];
+        MOLR_CUDA(cudaMemcpyAsync(oi.as<int64_t>() + size_t(b) * k, fid.as<int64_t>() + size_t(i) * k, size_t(k) * 8,
+                                  cudaMemcpyDeviceToDevice, s));
+        MOLR_CUDA(cudaMemcpyAsync(os.as<float>() + size_t(b) * k, fso.as<float>() + size_t(i) * k, size_t(k) * 4,
+                                  cudaMemcpyDeviceToDevice, s));
+        hcnt[b] = X;
+      }
+    }
+  } else {
+    // k' >= X: every item is a candidate (engine.py:127-128)
+    Scratch sc;
+    MOLR_TRY(sc.alloc(size_t(B) * X * 4, s));
+    MOLR_TRY(mol_score_any<int32_t>(ctx, c, g, B, k_u, iue.as<float>(), iuw.as<float>(), tau, segs, sc.as<float>(),
+                                    X, s));
+    MOLR_TRY(segmented_top_k<int32_t>(ctx, B, segs, sc.as<float>(), X, k, id_offset, oi.as<int64_t>(),
+                                      os.as<float>(), s));
+  }
+  if (out_cand) MOLR_CUDA(cudaMemcpyAsync(oc.dptr, hcnt.data(), size_t(B) * 8, cudaMemcpyDefault, s));
+  MOLR_CUDA(cudaStreamSynchronize(s));  // hcnt lives on this stack frame
+  return finish_outputs(s, {&oi, &os, &oc});
+}
+
+}  // extern "C"

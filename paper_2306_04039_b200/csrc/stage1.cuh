@@ -1,0 +1,18 @@
+// Stage-1 building blocks shared by stage1.cu and pipeline.cu.
+#pragma once
+#include "kernels.cuh"
+
+namespace molr {
+
+int scan_scores(molr_ctx* ctx, int mode, int64_t n, int dim, const float* vf, const int8_t* codes,
+                const float* scales, const int64_t* rows_idx, int B, const float* qf, const int8_t* qc, void* out,
+                int64_t ld, cudaStream_t s);
+int compact_passers(molr_ctx* ctx, int B, int64_t n, const void* sc, int is_int, int64_t ld, const uint32_t* tkey,
+                    int strict, int64_t cap, int64_t id_base, int64_t* out_ids, int64_t* totals, cudaStream_t s);
+int gather_rows(molr_ctx* ctx, int64_t m, int64_t dim_bytes, const void* src, const int64_t* idx, void* dst,
+                cudaStream_t s);
+int prepare_queries(molr_ctx* ctx, int mode, int B, int dim, const float* q, int8_t* qc, float* qs, cudaStream_t s);
+int check_view(const molr_cache* c, int mode);
+int int_to_float_inplace(molr_ctx* ctx, int32_t* p, int64_t n, cudaStream_t s);
+
+}  // namespace molr
