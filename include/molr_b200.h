@@ -64,6 +64,13 @@ int molr_ctx_destroy(molr_ctx* ctx);
 int molr_ctx_sync(molr_ctx* ctx, void* stream);
 /* number of hot-path kernel launches this context has issued (all threads) */
 int64_t molr_ctx_launch_count(molr_ctx* ctx);
+/* Per-kernel CUDA-event timing (off by default).  When on, the hot kernels are bracketed by
+ * events on their own launch stream; read back (name, launches, total ms, algorithmic work in
+ * bytes or flops) per kernel name by index until MOLR_ERR_OUT_OF_RANGE. */
+int molr_ctx_set_profiling(molr_ctx* ctx, int on);
+int molr_ctx_prof_read(molr_ctx* ctx, int idx, char* name, int name_len, int64_t* count,
+                       double* total_ms, double* work);
+int molr_ctx_prof_reset(molr_ctx* ctx);
 
 /* ---- ItemCache: immutable device snapshot — mol.py:216-291 ---------------------------------
  * item_embs (X, k_x, d) f32, item_gate_pre (X, G) f32, stage1_embs (X, d1) f32 or NULL,

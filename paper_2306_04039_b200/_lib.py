@@ -39,6 +39,9 @@ SIGNATURES = {
     "molr_ctx_destroy": [P],
     "molr_ctx_sync": [P, P],
     "molr_ctx_launch_count": [P],
+    "molr_ctx_set_profiling": [P, I],
+    "molr_ctx_prof_read": [P, I, P, I, P, P, P],
+    "molr_ctx_prof_reset": [P],
     "molr_cache_create": [P, L, I, I, I, P, P, I, P, P, P, P],
     "molr_cache_alloc": [P, L, I, I, I, I, I, P],
     "molr_cache_fill": [P, L, L, P, P, P, P, P, P],
@@ -143,6 +146,30 @@ def ctx(device: int | None = None) -> int:
 
 def launch_count(device: int | None = None) -> int:
     return int(load().molr_ctx_launch_count(ctx(device)))
+
+
+def set_profiling(on: bool, device: int | None = None) -> None:
+    call("molr_ctx_set_profiling", ctx(device), int(bool(on)))
+
+
+def prof_reset(device: int | None = None) -> None:
+    call("molr_ctx_prof_reset", ctx(device))
+
+
+def prof_read(device: int | None = None) -> dict:
+    """{kernel name: (launches, total ms, algorithmic work)} accumulated since the last reset."""
+    out = {}
+    i = 0
+    name = C.create_string_buffer(128)
+    cnt, ms, work = C.c_int64(), C.c_double(), C.c_double()
+    while True:
+        st = load().molr_ctx_prof_read(ctx(device), i, name, 128, C.byref(cnt), C.byref(ms), C.byref(work))
+        if st == ERR_RANGE:
+            break
+        check(st, "molr_ctx_prof_read")
+        out[name.value.decode()] = (int(cnt.value), float(ms.value), float(work.value))
+        i += 1
+    return out
 
 
 # ---- array helpers ------------------------------------------------------------------------

@@ -319,3 +319,68 @@ int molr_gating_destroy(molr_gating* g) {
 }
 
 }  // extern "C"
+
+// ---- per-kernel timing registry -------------------------------------------------------------
+extern "C" {
+
+int molr_ctx_set_profiling(molr_ctx* ctx, int on) {
+  if (!ctx) MOLR_FAIL(MOLR_ERR_INVALID, "null ctx");
+  ctx->prof.store(on ? 1 : 0);
+  return MOLR_OK;
+}
+
+static int prof_drain(molr_ctx* ctx) {
+  std::lock_guard<std::mutex> g(ctx->prof_mu);
+  for (auto& r : ctx->prof_pending) {
+    MOLR_CUDA(cudaEventSynchronize(r.end));
+    float ms = 0;
+    MOLR_CUDA(cudaEventElapsedTime(&ms, r.start, r.end));
+    bool found = false;
+    for (auto& kv : ctx->prof_sums)
+      if (kv.first == r.name) {
+        kv.second.count++;
+        kv.second.ms += ms;
+        kv.second.work += r.work;
+        found = true;
+        break;
+      }
+    if (!found) {
+      molr_prof_sum s;
+      s.count = 1;
+      s.ms = ms;
+      s.work = r.work;
+      ctx->prof_sums.emplace_back(r.name, s);
+    }
+    ctx->prof_free.push_back(r.start);
+    ctx->prof_free.push_back(r.end);
+  }
+  ctx->prof_pending.clear();
+  return MOLR_OK;
+}
+
+int molr_ctx_prof_read(molr_ctx* ctx, int idx, char* name, int name_len, int64_t* count, double* total_ms,
+                       double* work) {
+  if (!ctx) MOLR_FAIL(MOLR_ERR_INVALID, "null ctx");
+  MOLR_TRY(prof_drain(ctx));
+  std::lock_guard<std::mutex> g(ctx->prof_mu);
+  if (idx < 0 || idx >= (int)ctx->prof_sums.size()) return MOLR_ERR_OUT_OF_RANGE;
+  const auto& kv = ctx->prof_sums[idx];
+  if (name && name_len > 0) {
+    strncpy(name, kv.first.c_str(), name_len - 1);
+    name[name_len - 1] = 0;
+  }
+  if (count) *count = kv.second.count;
+  if (total_ms) *total_ms = kv.second.ms;
+  if (work) *work = kv.second.work;
+  return MOLR_OK;
+}
+
+int molr_ctx_prof_reset(molr_ctx* ctx) {
+  if (!ctx) MOLR_FAIL(MOLR_ERR_INVALID, "null ctx");
+  MOLR_TRY(prof_drain(ctx));
+  std::lock_guard<std::mutex> g(ctx->prof_mu);
+  ctx->prof_sums.clear();
+  return MOLR_OK;
+}
+
+}  // extern "C"

@@ -8,6 +8,8 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <mutex>
+#include <utility>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -64,12 +66,63 @@ struct Status {
 // ------------------------------------------------------------------------------------------
 // handles
 // ------------------------------------------------------------------------------------------
+struct molr_prof_rec {
+  const char* name;
+  cudaEvent_t start, end;
+  double work;  // algorithmic units (bytes or flops) of this launch
+};
+struct molr_prof_sum {
+  int64_t count = 0;
+  double ms = 0, work = 0;
+};
+
 struct molr_ctx {
   int device = 0;
   int num_sms = 148;
   cudaStream_t stream = nullptr;
   std::atomic<int64_t> launches{0};
+  // per-kernel CUDA-event timing registry (molr_ctx_set_profiling)
+  std::atomic<int> prof{0};
+  std::mutex prof_mu;
+  std::vector<molr_prof_rec> prof_pending;
+  std::vector<cudaEvent_t> prof_free;
+  std::vector<std::pair<std::string, molr_prof_sum>> prof_sums;
 };
+
+namespace molr {
+// RAII launch timer: records CUDA events around the kernel(s) launched in its scope on `s`
+// when profiling is enabled.  `work` = algorithmic bytes or flops of the launch.
+struct KTimer {
+  molr_ctx* ctx;
+  const char* name;
+  cudaStream_t s;
+  double work;
+  cudaEvent_t a = nullptr, b = nullptr;
+  KTimer(molr_ctx* c, const char* n, cudaStream_t st, double w = 0) : ctx(c), name(n), s(st), work(w) {
+    if (!ctx->prof.load(std::memory_order_relaxed)) return;
+    {
+      std::lock_guard<std::mutex> g(ctx->prof_mu);
+      if (ctx->prof_free.size() >= 2) {
+        a = ctx->prof_free.back();
+        ctx->prof_free.pop_back();
+        b = ctx->prof_free.back();
+        ctx->prof_free.pop_back();
+      }
+    }
+    if (!a) {
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+    }
+    cudaEventRecord(a, s);
+  }
+  ~KTimer() {
+    if (!a) return;
+    cudaEventRecord(b, s);
+    std::lock_guard<std::mutex> g(ctx->prof_mu);
+    ctx->prof_pending.push_back({name, a, b, work});
+  }
+};
+}  // namespace molr
 
 struct molr_cache {
   molr_ctx* ctx = nullptr;

@@ -338,11 +338,17 @@ int molr_two_stage_top_k(molr_ctx* ctx, const molr_cache* c, const molr_gating* 
     const int64_t n_rank = std::max<int64_t>(1, (int64_t)nr);
     Scratch ss, tkey;
     MOLR_TRY(ss.alloc(size_t(B) * lam * 4, s));
-    MOLR_TRY(scan_scores(ctx, mode, lam, c->d1, c->s1_f32, c->s1_codes, c->s1_scales, samp.as<int64_t>(), B,
-                         q.as<float>(), qc.as<int8_t>(), ss.p, lam, s));
     MOLR_TRY(tkey.alloc(size_t(B) * 4, s));
-    MOLR_TRY(nth_largest_rows(ctx, B, lam, ss.p, mode == MOLR_S1_INT8_RAW, lam, nullptr, 0, n_rank,
-                              tkey.as<uint32_t>(), s));
+    {
+      KTimer t(ctx, "stage1_sample_scan", s, double(B) * lam);
+      MOLR_TRY(scan_scores(ctx, mode, lam, c->d1, c->s1_f32, c->s1_codes, c->s1_scales, samp.as<int64_t>(), B,
+                           q.as<float>(), qc.as<int8_t>(), ss.p, lam, s));
+    }
+    {
+      KTimer t(ctx, "select_nth", s, double(B) * lam);
+      MOLR_TRY(nth_largest_rows(ctx, B, lam, ss.p, mode == MOLR_S1_INT8_RAW, lam, nullptr, 0, n_rank,
+                                tkey.as<uint32_t>(), s));
+    }
     // 4. filter scan with capacity; retry once with the exact maximum if it overflowed
     int64_t cap = imin64(X, k_prime + k_prime / 4 + 1024);
     MOLR_TRY(counts.alloc(size_t(B) * 8, s));
@@ -361,9 +367,12 @@ int molr_two_stage_top_k(molr_ctx* ctx, const molr_cache* c, const molr_gating* 
         MOLR_LAUNCHED(ctx);
         return MOLR_OK;
       };
-      if (mode == MOLR_S1_FLOAT) MOLR_TRY(launch(filter_scan_kernel<MOLR_S1_FLOAT>));
-      else if (mode == MOLR_S1_INT8) MOLR_TRY(launch(filter_scan_kernel<MOLR_S1_INT8>));
-      else MOLR_TRY(launch(filter_scan_kernel<MOLR_S1_INT8_RAW>));
+      {
+        KTimer t(ctx, "stage1_filter_scan", s, double(B) * X);
+        if (mode == MOLR_S1_FLOAT) MOLR_TRY(launch(filter_scan_kernel<MOLR_S1_FLOAT>));
+        else if (mode == MOLR_S1_INT8) MOLR_TRY(launch(filter_scan_kernel<MOLR_S1_INT8>));
+        else MOLR_TRY(launch(filter_scan_kernel<MOLR_S1_INT8_RAW>));
+      }
       MOLR_CUDA(cudaMemcpyAsync(hcnt.data(), counts.p, size_t(B) * 8, cudaMemcpyDeviceToHost, s));
       MOLR_CUDA(cudaStreamSynchronize(s));
       int64_t mx = *std::max_element(hcnt.begin(), hcnt.end());
@@ -383,13 +392,21 @@ int molr_two_stage_top_k(molr_ctx* ctx, const molr_cache* c, const molr_gating* 
     for (int b = 0; b < B; ++b)
       if (hcnt[b] < kk) fallback.push_back(b);
     int64_t cand_total = int64_t(B) * cap;
+    double pairs = 0;
+    for (int b = 0; b < B; ++b) pairs += double(std::min<int64_t>(hcnt[b], cap));
     Scratch sc;
     MOLR_TRY(sc.alloc(size_t(cand_total) * 4, s));
-    MOLR_TRY(mol_score_any<int32_t>(ctx, c, g, B, k_u, iue.as<float>(), iuw.as<float>(), tau, segs, sc.as<float>(),
-                                    0, s));
+    {
+      KTimer t(ctx, "mol_score", s, pairs);
+      MOLR_TRY(mol_score_any<int32_t>(ctx, c, g, B, k_u, iue.as<float>(), iuw.as<float>(), tau, segs,
+                                      sc.as<float>(), 0, s));
+    }
     // 6. top-k per query
-    MOLR_TRY(segmented_top_k<int32_t>(ctx, B, segs, sc.as<float>(), 0, k, id_offset, oi.as<int64_t>(),
-                                      os.as<float>(), s));
+    {
+      KTimer t(ctx, "topk_segmented", s, pairs);
+      MOLR_TRY(segmented_top_k<int32_t>(ctx, B, segs, sc.as<float>(), 0, k, id_offset, oi.as<int64_t>(),
+                                        os.as<float>(), s));
+    }
     if (!fallback.empty()) {
       // dense MoL for the few queries whose candidate set came back smaller than k
       const int F = (int)fallback.size();
