@@ -374,6 +374,7 @@ def main():
     launches0 = L.launch_count(local)
     evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     with Clocks(local) as clk:
+        time.sleep(1.0)  # let nvidia-smi initialise before the timed region
         barrier()
         evs[0].record(stream)
         for i in range(args.steps):
@@ -505,7 +506,7 @@ def main():
                    "k_prime": cfg["k_prime"], "k_prime_per_gpu": kp_local, "sample_ratio": cfg["ratio"],
                    "lambda_per_gpu": lam_local, "stage1": "int8 (bit-exact)", "parallelism": f"item-shard x{world}",
                    "l2": "inputs larger than L2 (corpus shard >= 12.5M items x 1.2 KB)"},
-        "p50_batch_latency_ms": float(np.median(step_ms)), "p50_single_query_latency_ms": float(np.median(lat)),
+        "p50_batch_latency_ms": float(np.median(step_ms)), "step_ms": [round(x, 3) for x in step_ms], "p50_single_query_latency_ms": float(np.median(lat)),
         "recall_at_k_vs_exact_mol": recall, "recall_queries": R,
         "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
         "gpu_launches": int(launches), "roofline": roof, "kernels": kernels,

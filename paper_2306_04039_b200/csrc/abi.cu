@@ -46,6 +46,23 @@ __global__ void to_bf16_kernel(const float* __restrict__ x, int64_t n, __nv_bflo
   if (local_bad) atomicOr(bad, 1);
 }
 
+// item components -> bf16 in the cache layout (swizzled when emb_swizzled); bad |= rounding.
+__global__ void embs_to_bf16_kernel(const float* __restrict__ x, int64_t rows, int k_x, int d,
+                                    __nv_bfloat16* __restrict__ out, int* __restrict__ bad) {
+  const int64_t ne = int64_t(k_x) * d;
+  const bool swz = emb_swizzled(k_x, d);
+  int local_bad = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows * ne; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = i / ne;
+    int e = int(i % ne), b = e / d, k = e % d;
+    float v = x[i];
+    __nv_bfloat16 h = __float2bfloat16_rn(v);
+    local_bad |= (__bfloat162float(h) != v);
+    out[r * ne + emb_offset(b, k, d, swz)] = h;
+  }
+  if (local_bad) atomicOr(bad, 1);
+}
+
 }  // namespace molr
 
 using namespace molr;
@@ -161,7 +178,8 @@ int molr_cache_fill(molr_cache* c, int64_t row0, int64_t n, const float* embs, c
       } else {
         In e;
         MOLR_TRY(e.stage(embs + r * per_row, size_t(m * per_row) * 4, s));
-        to_bf16_kernel<<<ctx->num_sms * 8, 256, 0, s>>>(e.as<float>(), m * per_row, c->embs_bf16 + off, bad.as<int>());
+        embs_to_bf16_kernel<<<ctx->num_sms * 8, 256, 0, s>>>(e.as<float>(), m, c->k_x, c->d, c->embs_bf16 + off,
+                                                             bad.as<int>());
         MOLR_LAUNCHED(ctx);
       }
     }

@@ -129,7 +129,7 @@ struct molr_cache {
   int64_t X = 0;
   int k_x = 0, d = 0, G = 0, d1 = 0;
   int storage = 0;                     // molr_storage bits
-  __nv_bfloat16* embs_bf16 = nullptr;  // (X, k_x, d) when bf16-exact
+  __nv_bfloat16* embs_bf16 = nullptr;  // (X, k_x, d) when bf16-exact; see emb_offset (pre-swizzled)
   float* embs_f32 = nullptr;           // (X, k_x, d) otherwise
   __nv_bfloat16* gp_bf16 = nullptr;    // (X, G) when bf16-exact
   float* gp_f32 = nullptr;             // (X, G) otherwise
@@ -281,6 +281,15 @@ __device__ __forceinline__ float silu_f32(float x) {
   // x * sigmoid(x) with full-precision expf (reference: x * scipy.special.expit(x))
   return x / (1.0f + expf(-x));
 }
+
+// bf16 item-component blocks with d = 64 (128-byte rows) and k_x % 8 == 0 are stored in the
+// UMMA K-major SWIZZLE_128B atom order: the 16-byte chunk c of component row b sits at chunk
+// position c ^ (b % 8).  One 1 KB bulk copy of an item (k_x = 8) into a 1024-aligned shared slot
+// is then a ready tcgen05 operand (8 rows x 64 K).  Offset (elements) of (b, k) within an item:
+__host__ __device__ __forceinline__ int emb_offset(int b, int k, int d, bool swz) {
+  return swz ? b * d + ((((k >> 3) ^ (b & 7)) << 3) | (k & 7)) : b * d + k;
+}
+__host__ __device__ __forceinline__ bool emb_swizzled(int k_x, int d) { return d == 64 && (k_x % 8) == 0; }
 
 __host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
 __host__ __device__ __forceinline__ int64_t imax64(int64_t a, int64_t b) { return a > b ? a : b; }

@@ -62,6 +62,18 @@ __global__ void bf16_to_f32_kernel(const __nv_bfloat16* __restrict__ a, int64_t 
     o[i] = __bfloat162float(a[i]);
 }
 
+// cache item components (bf16, possibly swizzled) -> plain (rows, k_x, d) f32
+__global__ void embs_to_f32_kernel(const __nv_bfloat16* __restrict__ a, int64_t rows, int k_x, int d,
+                                   float* __restrict__ o) {
+  const int64_t ne = int64_t(k_x) * d;
+  const bool swz = emb_swizzled(k_x, d);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows * ne; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = i / ne;
+    int e = int(i % ne);
+    o[i] = __bfloat162float(a[r * ne + emb_offset(e / d, e % d, d, swz)]);
+  }
+}
+
 static int grid_for(molr_ctx* ctx, int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, ctx->num_sms * 16)); }
 
 }  // namespace molr
@@ -138,7 +150,7 @@ int molr_cache_read(const molr_cache* c, int64_t row0, int64_t n, float* embs, f
     if (c->embs_f32)
       MOLR_CUDA(cudaMemcpyAsync(oe.dptr, c->embs_f32 + row0 * ne, size_t(n) * ne * 4, cudaMemcpyDeviceToDevice, s));
     else {
-      bf16_to_f32_kernel<<<grid_for(ctx, n * ne), 256, 0, s>>>(c->embs_bf16 + row0 * ne, n * ne, oe.as<float>());
+      embs_to_f32_kernel<<<grid_for(ctx, n * ne), 256, 0, s>>>(c->embs_bf16 + row0 * ne, n, c->k_x, c->d, oe.as<float>());
       MOLR_LAUNCHED(ctx);
     }
   }

@@ -225,11 +225,12 @@ mol_fused_generic_kernel(int B, int k_u, int k_x, int d, int G, int H, float tau
     if (t < kGenP) xs[t] = t < np ? (ids ? (int64_t)ids[seg0 + j0 + t] : j0 + t) : 0;
     __syncthreads();
     // stage item rows (bf16) into SMEM
+    const bool swz = emb_swizzled(k_x, d);
     for (int i = t; i < kGenP * ne; i += blockDim.x) {
       int p = i / ne, r = i % ne;
       int64_t x = xs[p];
       eh[i] = EF32 ? reinterpret_cast<const float*>(ev)[x * ne + r]
-                   : __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(ev)[x * ne + r]);
+                   : __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(ev)[x * ne + emb_offset(r / d, r % d, d, swz)]);
     }
     __syncthreads();
     // phase A: component logits

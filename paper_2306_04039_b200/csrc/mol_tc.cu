@@ -1,20 +1,629 @@
-// tcgen05 production MoL kernel (k_u = k_x = 8, d = 64, G = 64, H = 128).  Placeholder until
-// the tensor-core path lands: the dispatcher falls back to the generic SIMT kernel.
+// Fused MoL scorer on the 5th-gen tensor cores (tcgen05 + TMEM), production shape
+// k_u = k_x = 8, d = 64, G = k_u * k_x = 64, H = 128 — score_candidates / batch_score_all /
+// mol_top_k's scoring (mol.py:139-205, 329-386).
+//
+// One persistent CTA per SM, warp-specialised:
+//   warp 0       producer: per candidate, one 1 KB cp.async.bulk of the item's component block
+//                (the cache stores it pre-swizzled, see emb_offset) into a ring of 16-item stages
+//   warp 1       MMA issuer (one thread) + TMEM owner
+//   warps 2..    NE epilogue warpgroups (4 warps each); tile t belongs to group t % NE, so one
+//                group's SIMT epilogue overlaps the other's MMAs
+// Per tile of 128 (query, candidate) pairs of ONE query:
+//   C : 8 x [M=128 rows = 16 items x 8 components] x [N=16 = (hi,lo) x 8 user components] x K=64
+//       -> D0 (TMEM).  The query side is split u = hi + lo in bf16 (~2^-17 relative), the item
+//       side is exact bf16, accumulation fp32: component logits to ~1e-7 relative.
+//   E0: TMEM -> (hi+lo)/tau -> fp32 logits, transposed to one row per pair through smem (CL)
+//   E0.5: row p -> bf16 A-operand (A1) + fp32 copy kept in TMEM (CLT) for the final gated sum
+//   L1: [128 x 64] A1 . W1^T (+ a K=16 MMA that adds b1 as bf16 hi+lo)  -> D1 (TMEM, N=128)
+//   E1: h = silu(D1) -> A2 = [bf16(h) | bf16(h - bf16(h))]  (hidden rounding dominates the
+//       cross-net error; the hi/lo split keeps h to ~2^-17 so hard gating stays in tolerance)
+//   L2: [128 x 256] A2 . [W2^T ; W2^T] -> D2 (TMEM, N=64)
+//   E2: pi = softmax(silu(uw * gate_pre + D2)); score = sum pi * CLT  -> global
+// The G logits and H hidden units never leave the SM.
+#include <algorithm>
+#include <cstdlib>
+
 #include "kernels.cuh"
 
 namespace molr {
+namespace tc {
 
-bool mol_tc_supported(const molr_cache*, const molr_gating*, int) { return false; }
+constexpr int KX = 8, D = 64, G = 64, H = 128;
+constexpr int TILE = 128;           // pairs per tile (MMA M)
+constexpr int GROUP = 16;           // items per component MMA (16 items x 8 rows = 128)
+constexpr int NGROUPS = TILE / GROUP;
+constexpr int NSTAGE = 3;           // ring stages (16 KB each)
+constexpr int CL_LD = 68;           // fp32 row stride of the logit transpose buffer
+constexpr int TMEM_COLS_PER_GROUP = 256;
+
+// ---- shared memory map (bytes, 1024-aligned regions) ----------------------------------------
+constexpr int SZ_STAGE = GROUP * 1024;                  // 16 KB
+constexpr int OFF_RING = 0;
+constexpr int OFF_W1T = OFF_RING + NSTAGE * SZ_STAGE;   // 128 x 64 bf16, SW128     16 KB
+constexpr int OFF_W2T = OFF_W1T + 16384;                // 2 x (64 x 64) bf16, SW128 16 KB
+constexpr int OFF_W1B = OFF_W2T + 16384;                // 128 x 16 bf16, interleave 4 KB
+constexpr int OFF_BIASA = OFF_W1B + 4096;               // 128 x 16 bf16, interleave 4 KB
+constexpr int OFF_GRP = OFF_BIASA + 4096;               // per epilogue group:
+constexpr int G_B0 = 0;                                 //   16 x 64 bf16 SW128 (u hi ; u lo)   2 KB
+constexpr int G_R = 2048;                               //   64 KB region R, time-shared:
+//   A2 = [h_hi | h_lo] as 4 SW128 atoms of 128 x 64 bf16 (K = 256)   R[0, 64K)   (E1 -> L2)
+//   CL = fp32 logits [128 x 68]                                       R[0, 34K)   (E0 -> E0.5)
+//   A1 = bf16 logits, SW128 128 x 64                                  R[48K, 64K) (E0.5 -> L1)
+constexpr int G_A2 = G_R;
+constexpr int G_CL = G_R;
+constexpr int G_A1 = G_R + 49152;
+constexpr int SZ_CL = TILE * CL_LD * 4;                 //   34816
+constexpr int G_UW = G_R + 65536;                       //   64 f32
+constexpr int SZ_GRP = G_UW + 1024;
+static_assert(SZ_CL <= 49152, "CL must not reach A1");
+static_assert((G_A1 % 1024) == 0 && (G_A2 % 1024) == 0 && (SZ_GRP % 1024) == 0, "alignment");
+
+template <int NE>
+struct Smem {
+  static constexpr int OFF_BAR = OFF_GRP + NE * SZ_GRP;
+  // barriers: full[NSTAGE], empty[NSTAGE], then per group: b0_ready, d0_full, a1_ready, d1_full, a2_ready, d2_full
+  static constexpr int NBAR = 2 * NSTAGE + 6 * NE;
+  static constexpr int OFF_TMEM = OFF_BAR + NBAR * 8;
+  static constexpr int BYTES = OFF_TMEM + 16 + 1024;  // + alignment slack
+};
+
+// ---- PTX wrappers ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(bar),
+      "r"(parity), "r"(0x989680)
+      : "memory");
+}
+__device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.b32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+// SW128 K-major descriptor: rows of 128 B, 8-row atoms 1024 B apart.
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t addr) {
+  return uint64_t((addr >> 4) & 0x3FFF) | (uint64_t(1024 >> 4) << 32) | (1ull << 46) | (2ull << 61);
+}
+// no-swizzle ("interleave") K-major descriptor: core matrices 8 rows x 16 B; LBO = K stride, SBO = M stride
+__device__ __forceinline__ uint64_t desc_interleave(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  return uint64_t((addr >> 4) & 0x3FFF) | (uint64_t((lbo >> 4) & 0x3FFF) << 16) | (uint64_t((sbo >> 4) & 0x3FFF) << 32) |
+         (1ull << 46);
+}
+// kind::f16 instruction descriptor: A = B = bf16, D = f32, both K-major, M = 128
+__host__ __device__ constexpr uint32_t idesc_bf16(int n) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(n >> 3) << 17) | (uint32_t(128 >> 4) << 24);
+}
+__device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(accum)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+
+#define TMEM_LD16(taddr, r)                                                                                       \
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];" \
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),   \
+                 "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),          \
+                 "=r"(r[15])                                                                                       \
+               : "r"(taddr))
+#define TMEM_ST16(taddr, r)                                                                                        \
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" \
+               ::"r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), \
+               "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]))
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);  // .x = lo (low 16 bits), .y = hi
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+__device__ __forceinline__ float fast_tanh(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rcp(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// SiLU with one MUFU (tanh.approx, ~5e-4 relative): kept for experiments; the production path
+// uses silu_acc because the hidden units are carried at ~2^-17 (hi/lo split) into layer 2
+__device__ __forceinline__ float silu_fast(float x) {
+  float h = 0.5f * x;
+  return fmaf(h, fast_tanh(h), h);
+}
+// SiLU as x * rcp(1 + 2^(-x log2 e)) with ex2 + rcp (~1e-7 relative)
+__device__ __forceinline__ float silu_acc(float x) { return x * rcp(1.0f + ex2(-1.4426950408889634f * x)); }
+
+// SW128 K-major byte offset of 16-byte chunk `c` of row `r` within a [rows x 128 B] region.
+__device__ __forceinline__ uint32_t sw128(int r, int c) { return (r >> 3) * 1024 + (r & 7) * 128 + ((c ^ (r & 7)) << 4); }
+// interleave (no-swizzle) K-major offset of chunk c (0/1) of row r, LBO = 128, SBO = 256.
+__device__ __forceinline__ uint32_t ilv(int r, int c) { return (r >> 3) * 256 + c * 128 + (r & 7) * 16; }
+
+struct TileInfo {
+  int b;
+  int64_t seg0, j0;
+  int np;
+};
+
+__device__ __forceinline__ TileInfo tile_info(int64_t tile, int B, const int64_t* __restrict__ pre,
+                                              const int64_t* __restrict__ begin, const int64_t* __restrict__ end,
+                                              int64_t X) {
+  int lo = 0, hi = B - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (__ldg(pre + mid) <= tile) lo = mid; else hi = mid - 1;
+  }
+  TileInfo t;
+  t.b = lo;
+  t.seg0 = begin ? begin[lo] : 0;
+  int64_t len = begin ? end[lo] - begin[lo] : X;
+  t.j0 = (tile - pre[lo]) * TILE;
+  t.np = (int)imin64(TILE, len - t.j0);
+  return t;
+}
 
 template <class Id>
-int mol_score_tc(molr_ctx*, const molr_cache*, const molr_gating*, int, const float*, const float*, float, Segs<Id>,
-                 float*, int64_t, cudaStream_t) {
-  MOLR_FAIL(MOLR_ERR_INVALID, "tcgen05 MoL kernel not built");
+__device__ __forceinline__ int64_t cand_id(const Id* __restrict__ ids, const TileInfo& t, int q) {
+  return ids ? (int64_t)ids[t.seg0 + t.j0 + q] : t.j0 + q;
 }
+
+struct Params {
+  int B;
+  float inv_tau;
+  const __nv_bfloat16* embs;  // (X, 8, 64) pre-swizzled item blocks
+  const __nv_bfloat16* gp;    // (X, 64)
+  const __nv_bfloat16* w1t;   // SW128 image (16 KB)
+  const __nv_bfloat16* w2t;   // SW128 image (16 KB)
+  const __nv_bfloat16* w1b;   // interleave image (4 KB)
+  const float* user_embs;     // (B, 8, 64)
+  const float* uw;            // (B, 64)
+  const int64_t* begin;
+  const int64_t* end;
+  int64_t X;
+  const int64_t* tile_pre;
+  float* out;
+  int64_t out_ld;
+};
+
+template <class Id, int NE>
+__global__ void __launch_bounds__(64 + NE * 128, 1) mol_tc_kernel(Params P, const Id* __restrict__ ids) {
+  using S = Smem<NE>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sbase = smem_u32(sm);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + S::OFF_BAR);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + S::OFF_TMEM);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  auto bar = [&](int i) { return smem_u32(bars + i); };
+  auto full_bar = [&](int s) { return bar(s); };
+  auto empty_bar = [&](int s) { return bar(NSTAGE + s); };
+  auto gbar = [&](int g, int k) { return bar(2 * NSTAGE + 6 * g + k); };  // k: 0 b0_ready 1 d0_full 2 a1_ready 3 d1_full 4 a2_ready 5 d2_full
+
+  // ---- one-time setup: weight images + constant bias operand, barriers, TMEM ----
+  {
+    const uint4* src1 = reinterpret_cast<const uint4*>(P.w1t);
+    const uint4* src2 = reinterpret_cast<const uint4*>(P.w2t);
+    const uint4* src3 = reinterpret_cast<const uint4*>(P.w1b);
+    for (int i = threadIdx.x; i < 1024; i += blockDim.x) {
+      reinterpret_cast<uint4*>(sm + OFF_W1T)[i] = src1[i];
+      reinterpret_cast<uint4*>(sm + OFF_W2T)[i] = src2[i];
+    }
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) reinterpret_cast<uint4*>(sm + OFF_W1B)[i] = src3[i];
+    // bias A operand: column 0 and 1 of every row = 1.0 (pairs with b1 hi / lo rows of W1B)
+    for (int r = threadIdx.x; r < TILE; r += blockDim.x) {
+      uint4 c0 = make_uint4(0x3F803F80u, 0u, 0u, 0u), z = make_uint4(0u, 0u, 0u, 0u);
+      *reinterpret_cast<uint4*>(sm + OFF_BIASA + ilv(r, 0)) = c0;
+      *reinterpret_cast<uint4*>(sm + OFF_BIASA + ilv(r, 1)) = z;
+    }
+    if (threadIdx.x == 0) {
+      for (int s = 0; s < NSTAGE; ++s) {
+        mbar_init(full_bar(s), 1);
+        mbar_init(empty_bar(s), 1);
+      }
+      for (int g = 0; g < NE; ++g) {
+        mbar_init(gbar(g, 0), 128);
+        mbar_init(gbar(g, 1), 1);
+        mbar_init(gbar(g, 2), 128);
+        mbar_init(gbar(g, 3), 1);
+        mbar_init(gbar(g, 4), 128);
+        mbar_init(gbar(g, 5), 1);
+      }
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(NE * TMEM_COLS_PER_GROUP));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    fence_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+  }
+  const uint32_t tmem_base = *tmem_slot;
+  const int64_t T = P.tile_pre[P.B];
+
+  if (warp == 0) {
+    // ================= producer: item blocks -> ring =================
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int64_t tile = blockIdx.x; tile < T; tile += gridDim.x) {
+      const TileInfo t = tile_info(tile, P.B, P.tile_pre, P.begin, P.end, P.X);
+      const int64_t x0 = cand_id(ids, t, 0);
+      for (int g = 0; g < NGROUPS; ++g) {
+        mbar_wait(empty_bar(stage), phase ^ 1);
+        if (lane == 0) mbar_arrive_expect_tx(full_bar(stage), SZ_STAGE);
+        __syncwarp();
+        if (lane < GROUP) {
+          const int q = g * GROUP + lane;
+          const int64_t x = q < t.np ? cand_id(ids, t, q) : x0;
+          bulk_g2s(sbase + OFF_RING + stage * SZ_STAGE + lane * 1024, P.embs + x * (KX * D), 1024, full_bar(stage));
+        }
+        __syncwarp();
+        if (++stage == NSTAGE) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ================= MMA issuer (one thread) =================
+    if (lane == 0) {
+      constexpr uint32_t ID16 = idesc_bf16(16), ID128 = idesc_bf16(128), ID64 = idesc_bf16(64);
+      int stage = 0;
+      uint32_t rphase = 0;
+      // per-group state machine: 0 = need C, 1 = need L1, 2 = need L2; tiles in order per group
+      int64_t gtile[NE];
+      int gstate[NE];
+      uint32_t gphase[NE];
+      for (int g = 0; g < NE; ++g) {
+        gtile[g] = blockIdx.x + (int64_t)g * gridDim.x;
+        gstate[g] = 0;
+        gphase[g] = 0;
+      }
+      int64_t next_c = blockIdx.x;  // component MMAs must follow ring (tile) order
+      int live = 0;
+      for (int g = 0; g < NE; ++g) live += gtile[g] < T;
+      while (live > 0) {
+        for (int g = 0; g < NE; ++g) {
+          if (gtile[g] >= T) continue;
+          const uint32_t gb = sbase + OFF_GRP + g * SZ_GRP;
+          const uint32_t tm = tmem_base + g * TMEM_COLS_PER_GROUP;
+          if (gstate[g] == 0) {
+            if (gtile[g] != next_c || !mbar_test(gbar(g, 0), gphase[g])) continue;
+            tc_fence_after();
+            for (int grp = 0; grp < NGROUPS; ++grp) {
+              mbar_wait(full_bar(stage), rphase);
+              tc_fence_after();
+              const uint32_t a0 = sbase + OFF_RING + stage * SZ_STAGE;
+              for (int kk = 0; kk < 4; ++kk)
+                mma_bf16(tm + grp * 16, desc_sw128(a0 + kk * 32), desc_sw128(gb + G_B0 + kk * 32), ID16, kk > 0);
+              mma_commit(empty_bar(stage));
+              if (++stage == NSTAGE) {
+                stage = 0;
+                rphase ^= 1;
+              }
+            }
+            mma_commit(gbar(g, 1));
+            next_c += gridDim.x;
+            gstate[g] = 1;
+          } else if (gstate[g] == 1) {
+            if (!mbar_test(gbar(g, 2), gphase[g])) continue;
+            tc_fence_after();
+            for (int kk = 0; kk < 4; ++kk)
+              mma_bf16(tm + 128, desc_sw128(gb + G_A1 + kk * 32), desc_sw128(sbase + OFF_W1T + kk * 32), ID128, kk > 0);
+            mma_bf16(tm + 128, desc_interleave(sbase + OFF_BIASA, 128, 256),
+                     desc_interleave(sbase + OFF_W1B, 128, 256), ID128, 1);
+            mma_commit(gbar(g, 3));
+            gstate[g] = 2;
+          } else {
+            if (!mbar_test(gbar(g, 4), gphase[g])) continue;
+            tc_fence_after();
+            for (int kk = 0; kk < 16; ++kk) {  // A2 atoms 0,1 = h_hi, 2,3 = h_lo; B = W2^T atoms 0,1 twice
+              const uint32_t at = (kk >> 2) * 16384, ko = (kk & 3) * 32;
+              const uint32_t bt = ((kk >> 2) & 1) * 8192;
+              mma_bf16(tm + 64, desc_sw128(gb + G_A2 + at + ko), desc_sw128(sbase + OFF_W2T + bt + ko), ID64, kk > 0);
+            }
+            mma_commit(gbar(g, 5));
+            gstate[g] = 0;
+            gphase[g] ^= 1;
+            gtile[g] += (int64_t)NE * gridDim.x;
+            if (gtile[g] >= T) --live;
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    // ================= epilogue warpgroup(s) =================
+    const int eg = (warp - 2) / 4;           // group id
+    const int quarter = warp & 3;            // TMEM lane quarter this warp may access
+    const int p = quarter * 32 + lane;       // tile row = TMEM lane
+    uint8_t* gs = sm + OFF_GRP + eg * SZ_GRP;
+    const uint32_t gsu = sbase + OFF_GRP + eg * SZ_GRP;
+    float* CL = reinterpret_cast<float*>(gs + G_CL);  // time-shares region R with A1 / A2
+    float* UW = reinterpret_cast<float*>(gs + G_UW);
+    const uint32_t tm = tmem_base + eg * TMEM_COLS_PER_GROUP + ((uint32_t)(quarter * 32) << 16);
+    const int bar_id = 1 + eg;
+    uint32_t ph = 0;
+    for (int64_t tile = blockIdx.x + (int64_t)eg * gridDim.x; tile < T; tile += (int64_t)NE * gridDim.x) {
+      const TileInfo t = tile_info(tile, P.B, P.tile_pre, P.begin, P.end, P.X);
+      // ---- query operand B0 = [u_hi ; u_lo] (16 x 64 bf16, SW128) and uw ----
+      {
+        const int r = p >> 3, c = p & 7, a = r & 7;  // 128 threads = 16 rows x 8 chunks
+        const float* u = P.user_embs + (int64_t)t.b * (KX * D) + a * D + c * 8;
+        float4 v0 = __ldg(reinterpret_cast<const float4*>(u)), v1 = __ldg(reinterpret_cast<const float4*>(u) + 1);
+        float f[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+        uint32_t w[4];
+        #pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          float h0 = __bfloat162float(__float2bfloat16_rn(f[2 * m])), h1 = __bfloat162float(__float2bfloat16_rn(f[2 * m + 1]));
+          w[m] = (r < 8) ? pack_bf16(h0, h1) : pack_bf16(f[2 * m] - h0, f[2 * m + 1] - h1);
+        }
+        *reinterpret_cast<uint4*>(gs + G_B0 + sw128(r, c)) = make_uint4(w[0], w[1], w[2], w[3]);
+        if (p < G) UW[p] = P.uw[(int64_t)t.b * G + p];
+      }
+      fence_async_smem();
+      tc_fence_before();
+      mbar_arrive(gbar(eg, 0));
+      // prefetch this row's gate pre-activations (bf16 x 64 = 128 B)
+      uint4 gpr[8];
+      {
+        const int64_t x = p < t.np ? cand_id(ids, t, p) : cand_id(ids, t, 0);
+        const uint4* src = reinterpret_cast<const uint4*>(P.gp + x * G);
+        #pragma unroll
+        for (int m = 0; m < 8; ++m) gpr[m] = __ldg(src + m);
+      }
+      // ---- E0: component logits -> CL (transpose to one row per pair) ----
+      mbar_wait(gbar(eg, 1), ph);
+      tc_fence_after();
+      #pragma unroll
+      for (int grp = 0; grp < NGROUPS; ++grp) {
+        uint32_t v[16];
+        TMEM_LD16(tm + grp * 16, v);
+        tmem_wait_ld();
+        const int q = grp * GROUP + (p >> 3), bb = p & 7;
+        #pragma unroll
+        for (int a = 0; a < 8; ++a)
+          CL[q * CL_LD + a * 8 + bb] = (__uint_as_float(v[a]) + __uint_as_float(v[8 + a])) * P.inv_tau;
+      }
+      tc_fence_before();
+      named_sync(bar_id, 128);
+      tc_fence_after();
+      // ---- E0.5: row p -> A1 (bf16) and CLT (fp32, TMEM cols [0, 64)) ----
+      {
+        const float4* row = reinterpret_cast<const float4*>(CL + p * CL_LD);
+        #pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          float4 x0 = row[2 * c], x1 = row[2 * c + 1];
+          uint4 pk = make_uint4(pack_bf16(x0.x, x0.y), pack_bf16(x0.z, x0.w), pack_bf16(x1.x, x1.y), pack_bf16(x1.z, x1.w));
+          *reinterpret_cast<uint4*>(gs + G_A1 + sw128(p, c)) = pk;
+        }
+        #pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          uint32_t v[16];
+          #pragma unroll
+          for (int m = 0; m < 4; ++m) {
+            float4 x = row[h * 4 + m];
+            v[4 * m] = __float_as_uint(x.x);
+            v[4 * m + 1] = __float_as_uint(x.y);
+            v[4 * m + 2] = __float_as_uint(x.z);
+            v[4 * m + 3] = __float_as_uint(x.w);
+          }
+          TMEM_ST16(tm + h * 16, v);
+        }
+        tmem_wait_st();
+      }
+      fence_async_smem();
+      tc_fence_before();
+      mbar_arrive(gbar(eg, 2));
+      // ---- E1: hidden = silu(D1) -> A2 (bf16) ----
+      mbar_wait(gbar(eg, 3), ph);
+      tc_fence_after();
+      #pragma unroll
+      for (int ch = 0; ch < 8; ++ch) {  // 16 hidden units per chunk
+        uint32_t v[16];
+        TMEM_LD16(tm + 128 + ch * 16, v);
+        tmem_wait_ld();
+        uint32_t w[8], r[8];
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+          const float h0 = silu_acc(__uint_as_float(v[2 * m])), h1 = silu_acc(__uint_as_float(v[2 * m + 1]));
+          w[m] = pack_bf16(h0, h1);
+          const float l0 = h0 - __uint_as_float(w[m] << 16), l1 = h1 - __uint_as_float(w[m] & 0xFFFF0000u);
+          r[m] = pack_bf16(l0, l1);
+        }
+        const int j0 = ch * 16, atom = j0 >> 6, c0 = (j0 & 63) >> 3;
+        uint8_t* hi = gs + G_A2 + atom * 16384;
+        uint8_t* lo = gs + G_A2 + (2 + atom) * 16384;
+        *reinterpret_cast<uint4*>(hi + sw128(p, c0)) = make_uint4(w[0], w[1], w[2], w[3]);
+        *reinterpret_cast<uint4*>(hi + sw128(p, c0 + 1)) = make_uint4(w[4], w[5], w[6], w[7]);
+        *reinterpret_cast<uint4*>(lo + sw128(p, c0)) = make_uint4(r[0], r[1], r[2], r[3]);
+        *reinterpret_cast<uint4*>(lo + sw128(p, c0 + 1)) = make_uint4(r[4], r[5], r[6], r[7]);
+      }
+      fence_async_smem();
+      tc_fence_before();
+      mbar_arrive(gbar(eg, 4));
+      // ---- E2: combine + softmax + gated sum ----
+      mbar_wait(gbar(eg, 5), ph);
+      tc_fence_after();
+      float pre[64];
+      float mx = -INFINITY;
+      #pragma unroll
+      for (int ch = 0; ch < 4; ++ch) {
+        uint32_t v[16];
+        TMEM_LD16(tm + 64 + ch * 16, v);
+        tmem_wait_ld();
+        #pragma unroll
+        for (int m = 0; m < 16; ++m) {
+          const int g = ch * 16 + m;
+          const uint32_t wv = (&gpr[g >> 3].x)[(g & 7) >> 1];
+          const float gpv = __uint_as_float((g & 1) ? (wv & 0xFFFF0000u) : (wv << 16));
+          const float x = silu_acc(fmaf(UW[g], gpv, __uint_as_float(v[m])));
+          pre[g] = x;
+          mx = fmaxf(mx, x);
+        }
+      }
+      const float ml = mx * 1.4426950408889634f;
+      float sum = 0.f, acc = 0.f;
+      #pragma unroll
+      for (int ch = 0; ch < 4; ++ch) {
+        uint32_t v[16];
+        TMEM_LD16(tm + ch * 16, v);
+        tmem_wait_ld();
+        #pragma unroll
+        for (int m = 0; m < 16; ++m) {
+          const float e = ex2(fmaf(pre[ch * 16 + m], 1.4426950408889634f, -ml));
+          sum += e;
+          acc = fmaf(e, __uint_as_float(v[m]), acc);
+        }
+      }
+      if (p < t.np) {
+        const float s = __fdiv_rn(acc, sum);
+        if (P.begin) P.out[t.seg0 + t.j0 + p] = s;
+        else P.out[(int64_t)t.b * P.out_ld + t.j0 + p] = s;
+      }
+      tc_fence_before();
+      ph ^= 1;
+    }
+  }
+  // ---- teardown ----
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(NE * TMEM_COLS_PER_GROUP));
+  }
+}
+
+constexpr int NE_DEFAULT = 2;
+
+}  // namespace tc
+
+bool mol_tc_supported(const molr_cache* c, const molr_gating* g, int k_u) {
+  return c && g && k_u == 8 && c->k_x == 8 && c->d == 64 && c->G == 64 && g->G == 64 && g->H == 128 &&
+         c->embs_bf16 != nullptr && c->gp_bf16 != nullptr && g->w1t_bf16 != nullptr && !getenv("MOLR_DISABLE_TC");
+}
+
+__global__ void tile_prefix_kernel(int B, const int64_t* begin, const int64_t* end, int64_t X, int P, int64_t* pre);
+
+template <class Id>
+int mol_score_tc(molr_ctx* ctx, const molr_cache* c, const molr_gating* g, int B, const float* ue, const float* uw,
+                 float tau, Segs<Id> segs, float* out, int64_t out_ld, cudaStream_t s) {
+  if (B <= 0) return MOLR_OK;
+  Scratch pre;
+  MOLR_TRY(pre.alloc(size_t(B + 1) * 8, s));
+  tile_prefix_kernel<<<1, 1024, 0, s>>>(B, segs.begin, segs.end, segs.X, tc::TILE, pre.as<int64_t>());
+  MOLR_LAUNCHED(ctx);
+  int64_t T = 0;
+  MOLR_CUDA(cudaMemcpyAsync(&T, pre.as<int64_t>() + B, 8, cudaMemcpyDeviceToHost, s));
+  MOLR_CUDA(cudaStreamSynchronize(s));
+  if (T == 0) return MOLR_OK;
+  constexpr int NE = tc::NE_DEFAULT;
+  tc::Params P;
+  P.B = B;
+  P.inv_tau = 1.0f / tau;
+  P.embs = c->embs_bf16;
+  P.gp = c->gp_bf16;
+  P.w1t = g->w1t_bf16;
+  P.w2t = g->w2t_bf16;
+  P.w1b = g->w1t_bf16 + 8192;
+  P.user_embs = ue;
+  P.uw = uw;
+  P.begin = segs.begin;
+  P.end = segs.end;
+  P.X = segs.X;
+  P.tile_pre = pre.as<int64_t>();
+  P.out = out;
+  P.out_ld = out_ld;
+  auto kern = tc::mol_tc_kernel<Id, NE>;
+  const int smem = tc::Smem<NE>::BYTES;
+  MOLR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  const int grid = (int)std::min<int64_t>(T, ctx->num_sms);
+  kern<<<grid, 64 + NE * 128, smem, s>>>(P, segs.ids);
+  MOLR_LAUNCHED(ctx);
+  return MOLR_OK;
+}
+
 template int mol_score_tc<int64_t>(molr_ctx*, const molr_cache*, const molr_gating*, int, const float*, const float*,
                                    float, Segs<int64_t>, float*, int64_t, cudaStream_t);
 template int mol_score_tc<int32_t>(molr_ctx*, const molr_cache*, const molr_gating*, int, const float*, const float*,
                                    float, Segs<int32_t>, float*, int64_t, cudaStream_t);
+
 }  // namespace molr
 
-extern "C" int molr_gating_tc_prepare(molr_gating*) { return MOLR_OK; }
+using namespace molr;
+
+// Weight operand images for the tensor-core path (built once per gating handle):
+//   W1T  [128 hidden rows j][64 K = logit g]      bf16, SW128 K-major   (16 KB)
+//   W1B  [128 rows j][16 K]: K0 = bf16(b1[j]), K1 = bf16(b1[j] - K0)   interleave (4 KB)
+//   W2T  2 atoms x [64 rows g][64 K = hidden j]  bf16, SW128 K-major   (16 KB)
+extern "C" int molr_gating_tc_prepare(molr_gating* g) {
+  if (g->G != 64 || g->H != 128) return MOLR_OK;  // the generic kernel serves other shapes
+  std::vector<float> w1(size_t(64) * 128), b1(128), w2(size_t(128) * 64);
+  MOLR_CUDA(cudaMemcpy(w1.data(), g->w1, w1.size() * 4, cudaMemcpyDefault));
+  MOLR_CUDA(cudaMemcpy(b1.data(), g->b1, b1.size() * 4, cudaMemcpyDefault));
+  MOLR_CUDA(cudaMemcpy(w2.data(), g->w2, w2.size() * 4, cudaMemcpyDefault));
+  std::vector<__nv_bfloat16> img(8192 + 2048 + 8192, __float2bfloat16(0.0f));
+  auto sw = [](int r, int k) {  // element offset in an SW128 K-major [rows x 64] region
+    return (r >> 3) * 512 + (r & 7) * 64 + ((((k >> 3) ^ (r & 7))) << 3) + (k & 7);
+  };
+  for (int j = 0; j < 128; ++j)
+    for (int gg = 0; gg < 64; ++gg) img[sw(j, gg)] = __float2bfloat16(w1[size_t(gg) * 128 + j]);
+  for (int j = 0; j < 128; ++j) {
+    __nv_bfloat16 hi = __float2bfloat16(b1[j]);
+    __nv_bfloat16 lo = __float2bfloat16(b1[j] - __bfloat162float(hi));
+    const int base = 8192 + (j >> 3) * 128 + (j & 7) * 8;  // ilv(j, 0) in elements (chunk 0: K 0..7)
+    img[base + 0] = hi;
+    img[base + 1] = lo;
+  }
+  for (int gg = 0; gg < 64; ++gg)
+    for (int j = 0; j < 128; ++j) img[8192 + 2048 + (j >> 6) * 4096 + sw(gg, j & 63)] = __float2bfloat16(w2[size_t(j) * 64 + gg]);
+  // layout in device memory: [W1T 8192][W1B 2048][W2T 8192] -> w1t_bf16 points at the start,
+  // w2t_bf16 at +10240
+  MOLR_CUDA(cudaMalloc(&g->w1t_bf16, img.size() * 2));
+  MOLR_CUDA(cudaMemcpy(g->w1t_bf16, img.data(), img.size() * 2, cudaMemcpyHostToDevice));
+  g->w2t_bf16 = g->w1t_bf16 + 10240;
+  return MOLR_OK;
+}

@@ -443,3 +443,80 @@ def test_launch_counter_moves():
     before = L.launch_count()
     quantize_rowwise(np.ones((3, 8), np.float32))
     assert L.launch_count() > before
+
+
+# ---------------------------------------------------------------------------------- tcgen05 path
+def _synthetic_prod_cache(n_items, seed=0, gate_scale=1.0):
+    """Production-shape synthetic corpus (bf16-representable) through the oracle generator."""
+    from paper_2306_04039_b200.mol import ItemCache, MoLConfig
+    from paper_2306_04039_b200.quant import quantize_rowwise
+
+    syn = O.init_synthetic(32, n_items, k_u=8, k_x=8, d=64, gating_hidden=128, seed=seed)
+    c = O.build_item_cache(syn.item_table, syn.item_proj, syn.gating.item_net, 8, 64, 20.0, 8, quantized=False)
+    embs = O.round_bf16(c.item_embs)
+    gp = O.round_bf16(c.item_gate_pre * gate_scale)
+    s1 = embs.mean(axis=1).astype(np.float32)
+    cfg = MoLConfig(k_u=8, k_x=8, d=64, tau=20.0, gating_hidden=128, dropout_p=0.0)
+    cache = ItemCache(config=cfg, item_embs=embs, item_gate_pre=gp, stage1_embs=s1, stage1_q=quantize_rowwise(s1))
+    ue = O.user_components(syn, np.arange(32), 8, 64).astype(np.float32)
+    g = syn.gating
+    return cache, syn, ue, syn.user_table[:32]
+
+
+def _prod_gating(syn, cross_scale=1.0):
+    from paper_2306_04039_b200.mol import GatingNetwork, Mlp
+
+    g = syn.gating
+    cn = Mlp(g.cross_net.w1 * cross_scale, g.cross_net.b1 * cross_scale, g.cross_net.w2 * cross_scale)
+    return GatingNetwork(Mlp(*g.user_net), Mlp(*g.item_net), cn), O.Gating(g.user_net, g.item_net, O.MlpW(*cn.__dict__.values()))
+
+
+@pytest.mark.parametrize("scale", [1.0, 4.0])
+def test_tc_kernel_matches_oracle_dense(scale):
+    """The tcgen05 kernel (production shape) against the oracle on 20k items x 32 queries,
+    default and x4 ("hard") gating; also against the generic SIMT kernel."""
+    import os
+
+    from paper_2306_04039_b200.mol import batch_score_all
+
+    cache, syn, ue, feats = _synthetic_prod_cache(20_000, seed=5, gate_scale=scale)
+    gating, og = _prod_gating(syn, cross_scale=scale)
+    got = batch_score_all(cache, gating, ue, feats)
+    oc = O.Cache(cache.item_embs, cache.item_gate_pre, cache.stage1_embs, None, 20.0, 8)
+    ref = O.batch_score_all(oc, og, ue, feats)
+    err = np.abs(got.astype(np.float64) - ref)
+    print(f"scale={scale}: max |tc - oracle| = {err.max():.3e}, frac outside tol = "
+          f"{1 - O.score_close(got, ref).mean():.2e}")
+    assert O.score_close(got, ref, REL, ABS).all()
+    os.environ["MOLR_DISABLE_TC"] = "1"
+    try:
+        gen = batch_score_all(cache, gating, ue, feats)
+    finally:
+        del os.environ["MOLR_DISABLE_TC"]
+    assert O.score_close(gen, ref, REL, ABS).all()
+    for u in range(ue.shape[0]):
+        top_ref = np.lexsort((np.arange(ref.shape[1]), -ref[u]))[:100]
+        top_got = np.lexsort((np.arange(got.shape[1]), -got[u]))[:100]
+        assert topk_equal_modulo_ties(top_got, top_ref, ref[u])
+
+
+def test_tc_kernel_candidates_partial_tiles():
+    """Ragged candidate lists (1, 127, 128, 129, 1000 ids, unsorted, duplicated) through the tc kernel."""
+    from paper_2306_04039_b200.mol import QueryState, batch_mol_top_k, score_candidates
+
+    cache, syn, ue, feats = _synthetic_prod_cache(5_000, seed=9)
+    gating, og = _prod_gating(syn)
+    oc = O.Cache(cache.item_embs, cache.item_gate_pre, cache.stage1_embs, None, 20.0, 8)
+    rng = np.random.default_rng(3)
+    for n in (1, 127, 128, 129, 1000):
+        ids = rng.integers(0, cache.num_items, n)
+        got = score_candidates(cache, gating, ids, QueryState(ue[1], feats[1]))
+        ref = O.score_candidates(oc, og, ids, ue[1], feats[1])
+        assert O.score_close(got, ref, REL, ABS).all(), n
+    lists = [rng.permutation(cache.num_items)[: rng.integers(100, 3000)] for _ in range(8)]
+    ids, sc = batch_mol_top_k(cache, gating, ue[:8], feats[:8], 50, candidates=lists)
+    for u in range(8):
+        ref_all = np.full(cache.num_items, -np.inf)
+        ref_all[lists[u]] = O.score_candidates(oc, og, lists[u], ue[u], feats[u])
+        oi, _ = O.mol_top_k(oc, og, lists[u], ue[u], feats[u], 50)
+        assert topk_equal_modulo_ties(ids[u], oi, ref_all)
