@@ -405,15 +405,16 @@ def main():
         ue_stage.copy_(ue_pin, non_blocking=True)
         step(i, ue_stage.data_ptr(), feats_stage.data_ptr(), (host_ids, host_sc))
     barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
+    eev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    eev[0].record(stream)
     for i in range(args.steps):
         feats_stage.copy_(feats_pin, non_blocking=True)  # H2D of the step's inputs
         ue_stage.copy_(ue_pin, non_blocking=True)
         step(args.warmup + i, ue_stage.data_ptr(), feats_stage.data_ptr(), (host_ids, host_sc))  # + D2H
-    e1.record(stream)
+        eev[i + 1].record(stream)
     barrier()
-    e2e_ms = e0.elapsed_time(e1)
+    e2e_ms = eev[0].elapsed_time(eev[-1])
+    e2e_step_ms = [eev[i].elapsed_time(eev[i + 1]) for i in range(args.steps)]
     if world > 1:
         tt = torch.tensor([e2e_ms], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -508,7 +509,8 @@ def main():
                    "l2": "inputs larger than L2 (corpus shard >= 12.5M items x 1.2 KB)"},
         "p50_batch_latency_ms": float(np.median(step_ms)), "step_ms": [round(x, 3) for x in step_ms], "p50_single_query_latency_ms": float(np.median(lat)),
         "recall_at_k_vs_exact_mol": recall, "recall_queries": R,
-        "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+        "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "step_ms": [round(x, 3) for x in e2e_step_ms]},
         "gpu_launches": int(launches), "roofline": roof, "kernels": kernels,
         "build_s": t_build,
     }

@@ -5,19 +5,21 @@
 // One persistent CTA per SM, warp-specialised:
 //   warp 0       producer: per candidate, one 1 KB cp.async.bulk of the item's component block
 //                (the cache stores it pre-swizzled, see emb_offset) into a ring of 16-item stages
-//   warp 1       MMA issuer (one thread) + TMEM owner
-//   warps 2..    NE epilogue warpgroups (4 warps each); tile t belongs to group t % NE, so one
-//                group's SIMT epilogue overlaps the other's MMAs
-// Per tile of 128 (query, candidate) pairs of ONE query:
+//   warp 1       MMA issuer (one thread, non-blocking state machine) + TMEM owner
+//   warps 2..9   two epilogue warpgroups; tile t belongs to group t % 2, so one group's SIMT
+//                epilogue overlaps the other group's MMAs
+// Per tile of 128 (query, candidate) pairs of ONE query, per group TMEM columns [0, 256):
 //   C : 8 x [M=128 rows = 16 items x 8 components] x [N=16 = (hi,lo) x 8 user components] x K=64
-//       -> D0 (TMEM).  The query side is split u = hi + lo in bf16 (~2^-17 relative), the item
-//       side is exact bf16, accumulation fp32: component logits to ~1e-7 relative.
+//       (SS) -> D0 = cols [0,128).  Query side split u = hi + lo in bf16 (~2^-17 relative), item
+//       side exact bf16, fp32 accumulation.
 //   E0: TMEM -> (hi+lo)/tau -> fp32 logits, transposed to one row per pair through smem (CL)
-//   E0.5: row p -> bf16 A-operand (A1) + fp32 copy kept in TMEM (CLT) for the final gated sum
-//   L1: [128 x 64] A1 . W1^T (+ a K=16 MMA that adds b1 as bf16 hi+lo)  -> D1 (TMEM, N=128)
-//   E1: h = silu(D1) -> A2 = [bf16(h) | bf16(h - bf16(h))]  (hidden rounding dominates the
-//       cross-net error; the hi/lo split keeps h to ~2^-17 so hard gating stays in tolerance)
-//   L2: [128 x 256] A2 . [W2^T ; W2^T] -> D2 (TMEM, N=64)
+//   E0.5: row p -> CLT (fp32, cols [0,64)) for the final gated sum, and A1 = bf16 logits packed
+//       two per column in cols [64,96) (the A operand of layer 1, read straight from TMEM)
+//   L1: A1 (TMEM) . W1^T (smem) + [1 1 0..] . [b1_hi b1_lo 0..]^T (SS, K=16) -> D1 cols [128,256)
+//   E1: h = silu(D1) -> A2 = [bf16(h) | bf16(h - bf16(h))] written in place over D1 (each
+//       16-column chunk: 8 cols hi + 8 cols lo); keeping h to ~2^-17 keeps the cross-net within
+//       tolerance for sharp gating
+//   L2: A2 (TMEM, K = 256) . [W2^T ; W2^T] -> D2 cols [64,128)
 //   E2: pi = softmax(silu(uw * gate_pre + D2)); score = sum pi * CLT  -> global
 // The G logits and H hidden units never leave the SM.
 #include <algorithm>
@@ -32,40 +34,30 @@ constexpr int KX = 8, D = 64, G = 64, H = 128;
 constexpr int TILE = 128;           // pairs per tile (MMA M)
 constexpr int GROUP = 16;           // items per component MMA (16 items x 8 rows = 128)
 constexpr int NGROUPS = TILE / GROUP;
-constexpr int NSTAGE = 3;           // ring stages (16 KB each)
-constexpr int CL_LD = 68;           // fp32 row stride of the logit transpose buffer
+constexpr int NSTAGE = 6;           // ring stages (16 KB each): ~96 KB of item blocks in flight per SM
+constexpr int NE = 2;               // epilogue groups
+constexpr int CL_LD = 68;           // fp32 row stride of the logit transpose buffer (conflict-free LDS.128)
 constexpr int TMEM_COLS_PER_GROUP = 256;
 
-// ---- shared memory map (bytes, 1024-aligned regions) ----------------------------------------
+// ---- shared memory map (bytes; regions holding MMA operands are 1024-aligned) --------------
 constexpr int SZ_STAGE = GROUP * 1024;                  // 16 KB
 constexpr int OFF_RING = 0;
-constexpr int OFF_W1T = OFF_RING + NSTAGE * SZ_STAGE;   // 128 x 64 bf16, SW128     16 KB
+constexpr int OFF_W1T = OFF_RING + NSTAGE * SZ_STAGE;   // 128 x 64 bf16, SW128      16 KB
 constexpr int OFF_W2T = OFF_W1T + 16384;                // 2 x (64 x 64) bf16, SW128 16 KB
-constexpr int OFF_W1B = OFF_W2T + 16384;                // 128 x 16 bf16, interleave 4 KB
-constexpr int OFF_BIASA = OFF_W1B + 4096;               // 128 x 16 bf16, interleave 4 KB
+constexpr int OFF_W1B = OFF_W2T + 16384;                // 128 x 16 bf16, interleave  4 KB
+constexpr int OFF_BIASA = OFF_W1B + 4096;               // 128 x 16 bf16, interleave  4 KB
 constexpr int OFF_GRP = OFF_BIASA + 4096;               // per epilogue group:
-constexpr int G_B0 = 0;                                 //   16 x 64 bf16 SW128 (u hi ; u lo)   2 KB
-constexpr int G_R = 2048;                               //   64 KB region R, time-shared:
-//   A2 = [h_hi | h_lo] as 4 SW128 atoms of 128 x 64 bf16 (K = 256)   R[0, 64K)   (E1 -> L2)
-//   CL = fp32 logits [128 x 68]                                       R[0, 34K)   (E0 -> E0.5)
-//   A1 = bf16 logits, SW128 128 x 64                                  R[48K, 64K) (E0.5 -> L1)
-constexpr int G_A2 = G_R;
-constexpr int G_CL = G_R;
-constexpr int G_A1 = G_R + 49152;
-constexpr int SZ_CL = TILE * CL_LD * 4;                 //   34816
-constexpr int G_UW = G_R + 65536;                       //   64 f32
-constexpr int SZ_GRP = G_UW + 1024;
-static_assert(SZ_CL <= 49152, "CL must not reach A1");
-static_assert((G_A1 % 1024) == 0 && (G_A2 % 1024) == 0 && (SZ_GRP % 1024) == 0, "alignment");
-
-template <int NE>
-struct Smem {
-  static constexpr int OFF_BAR = OFF_GRP + NE * SZ_GRP;
-  // barriers: full[NSTAGE], empty[NSTAGE], then per group: b0_ready, d0_full, a1_ready, d1_full, a2_ready, d2_full
-  static constexpr int NBAR = 2 * NSTAGE + 6 * NE;
-  static constexpr int OFF_TMEM = OFF_BAR + NBAR * 8;
-  static constexpr int BYTES = OFF_TMEM + 16 + 1024;  // + alignment slack
-};
+constexpr int G_B0 = 0;                                 //   16 x 64 bf16 SW128 (u_hi ; u_lo)  2 KB
+constexpr int G_CL = 2048;                              //   fp32 logits [128 x 68]        34 KB
+constexpr int G_UW = G_CL + TILE * CL_LD * 4;           //   64 f32
+constexpr int SZ_GRP = 37888;                           //   (rounded to 1 KB)
+static_assert(G_UW + 256 <= SZ_GRP, "group region");
+constexpr int OFF_BAR = OFF_GRP + NE * SZ_GRP;
+// barriers: full[NSTAGE], empty[NSTAGE], then per group: b0_ready, d0_full, a1_ready, d1_full, a2_ready, d2_full
+constexpr int NBAR = 2 * NSTAGE + 6 * NE;
+constexpr int OFF_TMEM = OFF_BAR + NBAR * 8;
+constexpr int SMEM_BYTES = OFF_TMEM + 16;
+static_assert(SMEM_BYTES <= 232448, "shared memory budget");
 
 // ---- PTX wrappers ---------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -130,6 +122,16 @@ __device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b
       "l"(a), "l"(b), "r"(idesc), "r"(accum)
       : "memory");
 }
+// A operand from TMEM (packed bf16 pairs per 32-bit column, row m = lane m), B from smem
+__device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc,
+                                            uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, {%5, %5, %5, %5}, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(accum), "r"(0u)
+      : "memory");
+}
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
 }
@@ -144,6 +146,9 @@ __device__ __forceinline__ void mma_commit(uint32_t bar) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" \
                ::"r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), \
                "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]))
+#define TMEM_ST8(taddr, r)                                                                                  \
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),   \
+               "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]))
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
@@ -180,32 +185,37 @@ __device__ __forceinline__ uint32_t sw128(int r, int c) { return (r >> 3) * 1024
 // interleave (no-swizzle) K-major offset of chunk c (0/1) of row r, LBO = 128, SBO = 256.
 __device__ __forceinline__ uint32_t ilv(int r, int c) { return (r >> 3) * 256 + c * 128 + (r & 7) * 16; }
 
+// Walks a CTA's strided tile sequence; the query cursor only moves forward (tiles of one query
+// are contiguous in the global tile order), so locating a tile costs O(1) amortised loads.
+struct TileCursor {
+  int b = 0;
+  __device__ __forceinline__ void seek(int64_t tile, int B, const int64_t* __restrict__ pre) {
+    while (b + 1 < B && __ldg(pre + b + 1) <= tile) ++b;
+  }
+};
+
 struct TileInfo {
   int b;
   int64_t seg0, j0;
   int np;
 };
 
-__device__ __forceinline__ TileInfo tile_info(int64_t tile, int B, const int64_t* __restrict__ pre,
+__device__ __forceinline__ TileInfo tile_info(TileCursor& cur, int64_t tile, int B, const int64_t* __restrict__ pre,
                                               const int64_t* __restrict__ begin, const int64_t* __restrict__ end,
                                               int64_t X) {
-  int lo = 0, hi = B - 1;
-  while (lo < hi) {
-    int mid = (lo + hi + 1) >> 1;
-    if (__ldg(pre + mid) <= tile) lo = mid; else hi = mid - 1;
-  }
+  cur.seek(tile, B, pre);
   TileInfo t;
-  t.b = lo;
-  t.seg0 = begin ? begin[lo] : 0;
-  int64_t len = begin ? end[lo] - begin[lo] : X;
-  t.j0 = (tile - pre[lo]) * TILE;
+  t.b = cur.b;
+  t.seg0 = begin ? __ldg(begin + t.b) : 0;
+  const int64_t len = begin ? __ldg(end + t.b) - t.seg0 : X;
+  t.j0 = (tile - __ldg(pre + t.b)) * TILE;
   t.np = (int)imin64(TILE, len - t.j0);
   return t;
 }
 
 template <class Id>
 __device__ __forceinline__ int64_t cand_id(const Id* __restrict__ ids, const TileInfo& t, int q) {
-  return ids ? (int64_t)ids[t.seg0 + t.j0 + q] : t.j0 + q;
+  return ids ? (int64_t)__ldg(ids + t.seg0 + t.j0 + q) : t.j0 + q;
 }
 
 struct Params {
@@ -226,19 +236,19 @@ struct Params {
   int64_t out_ld;
 };
 
-template <class Id, int NE>
+template <class Id>
 __global__ void __launch_bounds__(64 + NE * 128, 1) mol_tc_kernel(Params P, const Id* __restrict__ ids) {
-  using S = Smem<NE>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t sm[];
   const uint32_t sbase = smem_u32(sm);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + S::OFF_BAR);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + S::OFF_TMEM);
+  if ((sbase & 1023u) != 0u) __trap();  // SW128 operands need 1024-aligned atoms
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + OFF_BAR);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + OFF_TMEM);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  auto bar = [&](int i) { return smem_u32(bars + i); };
+  auto bar = [&](int i) { return sbase + OFF_BAR + 8 * i; };
   auto full_bar = [&](int s) { return bar(s); };
   auto empty_bar = [&](int s) { return bar(NSTAGE + s); };
-  auto gbar = [&](int g, int k) { return bar(2 * NSTAGE + 6 * g + k); };  // k: 0 b0_ready 1 d0_full 2 a1_ready 3 d1_full 4 a2_ready 5 d2_full
+  // k: 0 b0_ready 1 d0_full 2 a1_ready 3 d1_full 4 a2_ready 5 d2_full
+  auto gbar = [&](int g, int k) { return bar(2 * NSTAGE + 6 * g + k); };
 
   // ---- one-time setup: weight images + constant bias operand, barriers, TMEM ----
   {
@@ -246,15 +256,14 @@ __global__ void __launch_bounds__(64 + NE * 128, 1) mol_tc_kernel(Params P, cons
     const uint4* src2 = reinterpret_cast<const uint4*>(P.w2t);
     const uint4* src3 = reinterpret_cast<const uint4*>(P.w1b);
     for (int i = threadIdx.x; i < 1024; i += blockDim.x) {
-      reinterpret_cast<uint4*>(sm + OFF_W1T)[i] = src1[i];
-      reinterpret_cast<uint4*>(sm + OFF_W2T)[i] = src2[i];
+      reinterpret_cast<uint4*>(sm + OFF_W1T)[i] = __ldg(src1 + i);
+      reinterpret_cast<uint4*>(sm + OFF_W2T)[i] = __ldg(src2 + i);
     }
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) reinterpret_cast<uint4*>(sm + OFF_W1B)[i] = src3[i];
-    // bias A operand: column 0 and 1 of every row = 1.0 (pairs with b1 hi / lo rows of W1B)
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) reinterpret_cast<uint4*>(sm + OFF_W1B)[i] = __ldg(src3 + i);
+    // bias A operand: K columns 0 and 1 of every row = 1.0 (pairs with the b1 hi / lo rows of W1B)
     for (int r = threadIdx.x; r < TILE; r += blockDim.x) {
-      uint4 c0 = make_uint4(0x3F803F80u, 0u, 0u, 0u), z = make_uint4(0u, 0u, 0u, 0u);
-      *reinterpret_cast<uint4*>(sm + OFF_BIASA + ilv(r, 0)) = c0;
-      *reinterpret_cast<uint4*>(sm + OFF_BIASA + ilv(r, 1)) = z;
+      *reinterpret_cast<uint4*>(sm + OFF_BIASA + ilv(r, 0)) = make_uint4(0x3F803F80u, 0u, 0u, 0u);
+      *reinterpret_cast<uint4*>(sm + OFF_BIASA + ilv(r, 1)) = make_uint4(0u, 0u, 0u, 0u);
     }
     if (threadIdx.x == 0) {
       for (int s = 0; s < NSTAGE; ++s) {
@@ -288,18 +297,24 @@ __global__ void __launch_bounds__(64 + NE * 128, 1) mol_tc_kernel(Params P, cons
     // ================= producer: item blocks -> ring =================
     int stage = 0;
     uint32_t phase = 0;
+    TileCursor cur;
     for (int64_t tile = blockIdx.x; tile < T; tile += gridDim.x) {
-      const TileInfo t = tile_info(tile, P.B, P.tile_pre, P.begin, P.end, P.X);
-      const int64_t x0 = cand_id(ids, t, 0);
+      const TileInfo t = tile_info(cur, tile, P.B, P.tile_pre, P.begin, P.end, P.X);
+      // the tile's 128 candidate ids, 4 per lane (q = lane + 32 i); padding rows reuse row 0
+      int64_t xid[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int q = lane + 32 * i;
+        xid[i] = cand_id(ids, t, q < t.np ? q : 0);
+      }
+#pragma unroll
       for (int g = 0; g < NGROUPS; ++g) {
+        const int64_t x = __shfl_sync(0xffffffffu, xid[g >> 1], 16 * (g & 1) + (lane & 15));
         mbar_wait(empty_bar(stage), phase ^ 1);
         if (lane == 0) mbar_arrive_expect_tx(full_bar(stage), SZ_STAGE);
         __syncwarp();
-        if (lane < GROUP) {
-          const int q = g * GROUP + lane;
-          const int64_t x = q < t.np ? cand_id(ids, t, q) : x0;
+        if (lane < GROUP)
           bulk_g2s(sbase + OFF_RING + stage * SZ_STAGE + lane * 1024, P.embs + x * (KX * D), 1024, full_bar(stage));
-        }
         __syncwarp();
         if (++stage == NSTAGE) {
           stage = 0;
@@ -308,24 +323,28 @@ __global__ void __launch_bounds__(64 + NE * 128, 1) mol_tc_kernel(Params P, cons
       }
     }
   } else if (warp == 1) {
-    // ================= MMA issuer (one thread) =================
+    // ================= MMA issuer (one thread, never blocks on a single barrier) =================
     if (lane == 0) {
       constexpr uint32_t ID16 = idesc_bf16(16), ID128 = idesc_bf16(128), ID64 = idesc_bf16(64);
       int stage = 0;
       uint32_t rphase = 0;
-      // per-group state machine: 0 = need C, 1 = need L1, 2 = need L2; tiles in order per group
+      // per group: 0 wait B0, 1 component MMAs (grp progress), 2 need L1, 3 need L2
       int64_t gtile[NE];
-      int gstate[NE];
+      int gstate[NE], ggrp[NE];
       uint32_t gphase[NE];
+#pragma unroll
       for (int g = 0; g < NE; ++g) {
         gtile[g] = blockIdx.x + (int64_t)g * gridDim.x;
         gstate[g] = 0;
+        ggrp[g] = 0;
         gphase[g] = 0;
       }
-      int64_t next_c = blockIdx.x;  // component MMAs must follow ring (tile) order
+      int64_t next_c = blockIdx.x;  // component MMAs follow ring (= tile) order
       int live = 0;
+#pragma unroll
       for (int g = 0; g < NE; ++g) live += gtile[g] < T;
       while (live > 0) {
+#pragma unroll
         for (int g = 0; g < NE; ++g) {
           if (gtile[g] >= T) continue;
           const uint32_t gb = sbase + OFF_GRP + g * SZ_GRP;
@@ -333,37 +352,45 @@ __global__ void __launch_bounds__(64 + NE * 128, 1) mol_tc_kernel(Params P, cons
           if (gstate[g] == 0) {
             if (gtile[g] != next_c || !mbar_test(gbar(g, 0), gphase[g])) continue;
             tc_fence_after();
-            for (int grp = 0; grp < NGROUPS; ++grp) {
-              mbar_wait(full_bar(stage), rphase);
+            gstate[g] = 1;
+          }
+          if (gstate[g] == 1) {
+            while (ggrp[g] < NGROUPS && mbar_test(full_bar(stage), rphase)) {
               tc_fence_after();
               const uint32_t a0 = sbase + OFF_RING + stage * SZ_STAGE;
+#pragma unroll
               for (int kk = 0; kk < 4; ++kk)
-                mma_bf16(tm + grp * 16, desc_sw128(a0 + kk * 32), desc_sw128(gb + G_B0 + kk * 32), ID16, kk > 0);
+                mma_bf16(tm + ggrp[g] * 16, desc_sw128(a0 + kk * 32), desc_sw128(gb + G_B0 + kk * 32), ID16, kk > 0);
               mma_commit(empty_bar(stage));
               if (++stage == NSTAGE) {
                 stage = 0;
                 rphase ^= 1;
               }
+              ++ggrp[g];
             }
+            if (ggrp[g] < NGROUPS) continue;
             mma_commit(gbar(g, 1));
             next_c += gridDim.x;
-            gstate[g] = 1;
-          } else if (gstate[g] == 1) {
+            ggrp[g] = 0;
+            gstate[g] = 2;
+          } else if (gstate[g] == 2) {
             if (!mbar_test(gbar(g, 2), gphase[g])) continue;
             tc_fence_after();
+#pragma unroll
             for (int kk = 0; kk < 4; ++kk)
-              mma_bf16(tm + 128, desc_sw128(gb + G_A1 + kk * 32), desc_sw128(sbase + OFF_W1T + kk * 32), ID128, kk > 0);
-            mma_bf16(tm + 128, desc_interleave(sbase + OFF_BIASA, 128, 256),
-                     desc_interleave(sbase + OFF_W1B, 128, 256), ID128, 1);
+              mma_bf16_ts(tm + 128, tm + 64 + kk * 8, desc_sw128(sbase + OFF_W1T + kk * 32), ID128, kk > 0);
+            mma_bf16(tm + 128, desc_interleave(sbase + OFF_BIASA, 128, 256), desc_interleave(sbase + OFF_W1B, 128, 256),
+                     ID128, 1);
             mma_commit(gbar(g, 3));
-            gstate[g] = 2;
+            gstate[g] = 3;
           } else {
             if (!mbar_test(gbar(g, 4), gphase[g])) continue;
             tc_fence_after();
-            for (int kk = 0; kk < 16; ++kk) {  // A2 atoms 0,1 = h_hi, 2,3 = h_lo; B = W2^T atoms 0,1 twice
-              const uint32_t at = (kk >> 2) * 16384, ko = (kk & 3) * 32;
-              const uint32_t bt = ((kk >> 2) & 1) * 8192;
-              mma_bf16(tm + 64, desc_sw128(gb + G_A2 + at + ko), desc_sw128(sbase + OFF_W2T + bt + ko), ID64, kk > 0);
+#pragma unroll
+            for (int ch = 0; ch < 8; ++ch) {  // hidden chunk ch = K [16ch, 16ch+16): hi then lo
+              const uint64_t bd = desc_sw128(sbase + OFF_W2T + (ch >> 2) * 8192 + (ch & 3) * 32);
+              mma_bf16_ts(tm + 64, tm + 128 + ch * 16, bd, ID64, ch > 0);
+              mma_bf16_ts(tm + 64, tm + 128 + ch * 16 + 8, bd, ID64, 1);
             }
             mma_commit(gbar(g, 5));
             gstate[g] = 0;
@@ -376,33 +403,33 @@ __global__ void __launch_bounds__(64 + NE * 128, 1) mol_tc_kernel(Params P, cons
     }
     __syncwarp();
   } else {
-    // ================= epilogue warpgroup(s) =================
-    const int eg = (warp - 2) / 4;           // group id
+    // ================= epilogue warpgroups =================
+    const int eg = (warp - 2) >> 2;          // group id
     const int quarter = warp & 3;            // TMEM lane quarter this warp may access
     const int p = quarter * 32 + lane;       // tile row = TMEM lane
     uint8_t* gs = sm + OFF_GRP + eg * SZ_GRP;
-    const uint32_t gsu = sbase + OFF_GRP + eg * SZ_GRP;
-    float* CL = reinterpret_cast<float*>(gs + G_CL);  // time-shares region R with A1 / A2
+    float* CL = reinterpret_cast<float*>(gs + G_CL);
     float* UW = reinterpret_cast<float*>(gs + G_UW);
     const uint32_t tm = tmem_base + eg * TMEM_COLS_PER_GROUP + ((uint32_t)(quarter * 32) << 16);
     const int bar_id = 1 + eg;
     uint32_t ph = 0;
+    TileCursor cur;
     for (int64_t tile = blockIdx.x + (int64_t)eg * gridDim.x; tile < T; tile += (int64_t)NE * gridDim.x) {
-      const TileInfo t = tile_info(tile, P.B, P.tile_pre, P.begin, P.end, P.X);
+      const TileInfo t = tile_info(cur, tile, P.B, P.tile_pre, P.begin, P.end, P.X);
       // ---- query operand B0 = [u_hi ; u_lo] (16 x 64 bf16, SW128) and uw ----
       {
         const int r = p >> 3, c = p & 7, a = r & 7;  // 128 threads = 16 rows x 8 chunks
         const float* u = P.user_embs + (int64_t)t.b * (KX * D) + a * D + c * 8;
-        float4 v0 = __ldg(reinterpret_cast<const float4*>(u)), v1 = __ldg(reinterpret_cast<const float4*>(u) + 1);
-        float f[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+        const float4 v0 = __ldg(reinterpret_cast<const float4*>(u)), v1 = __ldg(reinterpret_cast<const float4*>(u) + 1);
+        const float f[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
         uint32_t w[4];
-        #pragma unroll
+#pragma unroll
         for (int m = 0; m < 4; ++m) {
-          float h0 = __bfloat162float(__float2bfloat16_rn(f[2 * m])), h1 = __bfloat162float(__float2bfloat16_rn(f[2 * m + 1]));
-          w[m] = (r < 8) ? pack_bf16(h0, h1) : pack_bf16(f[2 * m] - h0, f[2 * m + 1] - h1);
+          const uint32_t hw = pack_bf16(f[2 * m], f[2 * m + 1]);
+          w[m] = (r < 8) ? hw : pack_bf16(f[2 * m] - __uint_as_float(hw << 16), f[2 * m + 1] - __uint_as_float(hw & 0xFFFF0000u));
         }
         *reinterpret_cast<uint4*>(gs + G_B0 + sw128(r, c)) = make_uint4(w[0], w[1], w[2], w[3]);
-        if (p < G) UW[p] = P.uw[(int64_t)t.b * G + p];
+        if (p < G) UW[p] = __ldg(P.uw + (int64_t)t.b * G + p);
       }
       fence_async_smem();
       tc_fence_before();
@@ -410,79 +437,72 @@ __global__ void __launch_bounds__(64 + NE * 128, 1) mol_tc_kernel(Params P, cons
       // prefetch this row's gate pre-activations (bf16 x 64 = 128 B)
       uint4 gpr[8];
       {
-        const int64_t x = p < t.np ? cand_id(ids, t, p) : cand_id(ids, t, 0);
+        const int64_t x = cand_id(ids, t, p < t.np ? p : 0);
         const uint4* src = reinterpret_cast<const uint4*>(P.gp + x * G);
-        #pragma unroll
+#pragma unroll
         for (int m = 0; m < 8; ++m) gpr[m] = __ldg(src + m);
       }
       // ---- E0: component logits -> CL (transpose to one row per pair) ----
       mbar_wait(gbar(eg, 1), ph);
       tc_fence_after();
-      #pragma unroll
-      for (int grp = 0; grp < NGROUPS; ++grp) {
-        uint32_t v[16];
+#pragma unroll
+      for (int grp = 0; grp < NGROUPS; grp += 2) {
+        uint32_t v[16], w[16];
         TMEM_LD16(tm + grp * 16, v);
+        TMEM_LD16(tm + grp * 16 + 16, w);
         tmem_wait_ld();
         const int q = grp * GROUP + (p >> 3), bb = p & 7;
-        #pragma unroll
-        for (int a = 0; a < 8; ++a)
+#pragma unroll
+        for (int a = 0; a < 8; ++a) {
           CL[q * CL_LD + a * 8 + bb] = (__uint_as_float(v[a]) + __uint_as_float(v[8 + a])) * P.inv_tau;
+          CL[(q + GROUP) * CL_LD + a * 8 + bb] = (__uint_as_float(w[a]) + __uint_as_float(w[8 + a])) * P.inv_tau;
+        }
       }
       tc_fence_before();
       named_sync(bar_id, 128);
       tc_fence_after();
-      // ---- E0.5: row p -> A1 (bf16) and CLT (fp32, TMEM cols [0, 64)) ----
+      // ---- E0.5: row p -> CLT (fp32, cols [0,64)) and A1 (bf16 pairs, cols [64,96)) ----
       {
         const float4* row = reinterpret_cast<const float4*>(CL + p * CL_LD);
-        #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          float4 x0 = row[2 * c], x1 = row[2 * c + 1];
-          uint4 pk = make_uint4(pack_bf16(x0.x, x0.y), pack_bf16(x0.z, x0.w), pack_bf16(x1.x, x1.y), pack_bf16(x1.z, x1.w));
-          *reinterpret_cast<uint4*>(gs + G_A1 + sw128(p, c)) = pk;
-        }
-        #pragma unroll
+#pragma unroll
         for (int h = 0; h < 4; ++h) {
-          uint32_t v[16];
-          #pragma unroll
+          uint32_t v[16], a1[8];
+#pragma unroll
           for (int m = 0; m < 4; ++m) {
-            float4 x = row[h * 4 + m];
+            const float4 x = row[h * 4 + m];
             v[4 * m] = __float_as_uint(x.x);
             v[4 * m + 1] = __float_as_uint(x.y);
             v[4 * m + 2] = __float_as_uint(x.z);
             v[4 * m + 3] = __float_as_uint(x.w);
+            a1[2 * m] = pack_bf16(x.x, x.y);
+            a1[2 * m + 1] = pack_bf16(x.z, x.w);
           }
           TMEM_ST16(tm + h * 16, v);
+          TMEM_ST8(tm + 64 + h * 8, a1);
         }
         tmem_wait_st();
       }
-      fence_async_smem();
       tc_fence_before();
       mbar_arrive(gbar(eg, 2));
-      // ---- E1: hidden = silu(D1) -> A2 (bf16) ----
+      // ---- E1: h = silu(D1) -> A2 hi/lo in place (cols [128+16ch, +8) hi, [+8, +16) lo) ----
       mbar_wait(gbar(eg, 3), ph);
       tc_fence_after();
-      #pragma unroll
-      for (int ch = 0; ch < 8; ++ch) {  // 16 hidden units per chunk
+#pragma unroll
+      for (int ch = 0; ch < 8; ++ch) {
         uint32_t v[16];
         TMEM_LD16(tm + 128 + ch * 16, v);
         tmem_wait_ld();
-        uint32_t w[8], r[8];
+        uint32_t w[16];
 #pragma unroll
         for (int m = 0; m < 8; ++m) {
           const float h0 = silu_acc(__uint_as_float(v[2 * m])), h1 = silu_acc(__uint_as_float(v[2 * m + 1]));
-          w[m] = pack_bf16(h0, h1);
-          const float l0 = h0 - __uint_as_float(w[m] << 16), l1 = h1 - __uint_as_float(w[m] & 0xFFFF0000u);
-          r[m] = pack_bf16(l0, l1);
+          const uint32_t hw = pack_bf16(h0, h1);
+          w[m] = hw;
+          w[8 + m] = pack_bf16(h0 - __uint_as_float(hw << 16), h1 - __uint_as_float(hw & 0xFFFF0000u));
         }
-        const int j0 = ch * 16, atom = j0 >> 6, c0 = (j0 & 63) >> 3;
-        uint8_t* hi = gs + G_A2 + atom * 16384;
-        uint8_t* lo = gs + G_A2 + (2 + atom) * 16384;
-        *reinterpret_cast<uint4*>(hi + sw128(p, c0)) = make_uint4(w[0], w[1], w[2], w[3]);
-        *reinterpret_cast<uint4*>(hi + sw128(p, c0 + 1)) = make_uint4(w[4], w[5], w[6], w[7]);
-        *reinterpret_cast<uint4*>(lo + sw128(p, c0)) = make_uint4(r[0], r[1], r[2], r[3]);
-        *reinterpret_cast<uint4*>(lo + sw128(p, c0 + 1)) = make_uint4(r[4], r[5], r[6], r[7]);
+        TMEM_ST16(tm + 128 + ch * 16, w);
       }
-      fence_async_smem();
+      tmem_wait_st();
       tc_fence_before();
       mbar_arrive(gbar(eg, 4));
       // ---- E2: combine + softmax + gated sum ----
@@ -490,12 +510,12 @@ __global__ void __launch_bounds__(64 + NE * 128, 1) mol_tc_kernel(Params P, cons
       tc_fence_after();
       float pre[64];
       float mx = -INFINITY;
-      #pragma unroll
+#pragma unroll
       for (int ch = 0; ch < 4; ++ch) {
         uint32_t v[16];
         TMEM_LD16(tm + 64 + ch * 16, v);
         tmem_wait_ld();
-        #pragma unroll
+#pragma unroll
         for (int m = 0; m < 16; ++m) {
           const int g = ch * 16 + m;
           const uint32_t wv = (&gpr[g >> 3].x)[(g & 7) >> 1];
@@ -507,12 +527,12 @@ __global__ void __launch_bounds__(64 + NE * 128, 1) mol_tc_kernel(Params P, cons
       }
       const float ml = mx * 1.4426950408889634f;
       float sum = 0.f, acc = 0.f;
-      #pragma unroll
+#pragma unroll
       for (int ch = 0; ch < 4; ++ch) {
         uint32_t v[16];
         TMEM_LD16(tm + ch * 16, v);
         tmem_wait_ld();
-        #pragma unroll
+#pragma unroll
         for (int m = 0; m < 16; ++m) {
           const float e = ex2(fmaf(pre[ch * 16 + m], 1.4426950408889634f, -ml));
           sum += e;
@@ -537,8 +557,6 @@ __global__ void __launch_bounds__(64 + NE * 128, 1) mol_tc_kernel(Params P, cons
   }
 }
 
-constexpr int NE_DEFAULT = 2;
-
 }  // namespace tc
 
 bool mol_tc_supported(const molr_cache* c, const molr_gating* g, int k_u) {
@@ -560,7 +578,6 @@ int mol_score_tc(molr_ctx* ctx, const molr_cache* c, const molr_gating* g, int B
   MOLR_CUDA(cudaMemcpyAsync(&T, pre.as<int64_t>() + B, 8, cudaMemcpyDeviceToHost, s));
   MOLR_CUDA(cudaStreamSynchronize(s));
   if (T == 0) return MOLR_OK;
-  constexpr int NE = tc::NE_DEFAULT;
   tc::Params P;
   P.B = B;
   P.inv_tau = 1.0f / tau;
@@ -577,11 +594,11 @@ int mol_score_tc(molr_ctx* ctx, const molr_cache* c, const molr_gating* g, int B
   P.tile_pre = pre.as<int64_t>();
   P.out = out;
   P.out_ld = out_ld;
-  auto kern = tc::mol_tc_kernel<Id, NE>;
-  const int smem = tc::Smem<NE>::BYTES;
+  auto kern = tc::mol_tc_kernel<Id>;
+  const int smem = tc::SMEM_BYTES;
   MOLR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const int grid = (int)std::min<int64_t>(T, ctx->num_sms);
-  kern<<<grid, 64 + NE * 128, smem, s>>>(P, segs.ids);
+  kern<<<grid, 64 + tc::NE * 128, smem, s>>>(P, segs.ids);
   MOLR_LAUNCHED(ctx);
   return MOLR_OK;
 }
