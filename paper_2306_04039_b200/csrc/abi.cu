@@ -63,6 +63,36 @@ __global__ void embs_to_bf16_kernel(const float* __restrict__ x, int64_t rows, i
   if (local_bad) atomicOr(bad, 1);
 }
 
+// linear (m, 64) int8 rows -> interleaved cache layout starting at row r0
+__global__ void codes_to_ilv_kernel(const int8_t* __restrict__ src, int64_t m, int64_t r0, int8_t* __restrict__ dst) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m * 4; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i >> 2;
+    const int c = int(i & 3);
+    *reinterpret_cast<int4*>(dst + s1_chunk_offset(r0 + r, c, 64)) = *reinterpret_cast<const int4*>(src + r * 64 + c * 16);
+  }
+}
+
+__global__ void chunk_mm_kernel(const float* __restrict__ scales, int64_t c0, int64_t c1, float2* __restrict__ mm) {
+  for (int64_t c = c0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < c1; c += (int64_t)gridDim.x * blockDim.x) {
+    float lo = INFINITY, hi = 0.f;
+    for (int j = 0; j < 32; ++j) {
+      const float v = scales[c * 32 + j];
+      if (v > 0.f) {  // padding rows have scale 0 and are never scored
+        lo = fminf(lo, v);
+        hi = fmaxf(hi, v);
+      }
+    }
+    mm[c] = make_float2(lo, hi);
+  }
+}
+
+int s1_update_chunk_mm(molr_cache* c, int64_t row0, int64_t n, cudaStream_t s) {
+  const int64_t c0 = row0 / 32, c1 = (row0 + n + 31) / 32;
+  chunk_mm_kernel<<<div_up(c1 - c0, 256), 256, 0, s>>>(c->s1_scales, c0, c1, c->s1_chunk_mm);
+  MOLR_LAUNCHED(c->ctx);
+  return MOLR_OK;
+}
+
 }  // namespace molr
 
 using namespace molr;
@@ -145,8 +175,15 @@ int molr_cache_alloc(molr_ctx* ctx, int64_t X, int k_x, int d, int G, int d1, in
   if (!st && (storage & MOLR_STORE_GP_F32)) st = grab((void**)&c->gp_f32, size_t(X) * G * 4);
   if (!st && !(storage & MOLR_STORE_GP_F32)) st = grab((void**)&c->gp_bf16, size_t(X) * G * 2);
   if (!st && (storage & MOLR_STORE_S1_F32)) st = grab((void**)&c->s1_f32, size_t(X) * d1 * 4);
-  if (!st && (storage & MOLR_STORE_S1_INT8)) st = grab((void**)&c->s1_codes, size_t(X) * d1);
-  if (!st && (storage & MOLR_STORE_S1_INT8)) st = grab((void**)&c->s1_scales, size_t(X) * 4);
+  const int64_t xr = s1_rows_alloc(X, d1);
+  if (!st && (storage & MOLR_STORE_S1_INT8)) st = grab((void**)&c->s1_codes, size_t(xr) * d1);
+  if (!st && (storage & MOLR_STORE_S1_INT8)) st = grab((void**)&c->s1_scales, size_t(xr) * 4);
+  if (!st && (storage & MOLR_STORE_S1_INT8) && s1_interleaved(d1))
+    st = grab((void**)&c->s1_chunk_mm, size_t(xr / 32) * sizeof(float2));
+  if (!st && (storage & MOLR_STORE_S1_INT8)) {  // zero the padding rows
+    if (cudaMemset(c->s1_codes, 0, size_t(xr) * d1) != cudaSuccess || cudaMemset(c->s1_scales, 0, size_t(xr) * 4) != cudaSuccess)
+      st = MOLR_ERR_CUDA;
+  }
   if (st) {
     molr_cache_destroy(c);
     return st;
@@ -197,12 +234,21 @@ int molr_cache_fill(molr_cache* c, int64_t row0, int64_t n, const float* embs, c
     if (s1 && c->s1_f32)
       MOLR_CUDA(cudaMemcpyAsync(c->s1_f32 + size_t(row0 + r) * c->d1, s1 + r * c->d1,
                                 size_t(m) * c->d1 * 4, cudaMemcpyDefault, s));
-    if (codes && c->s1_codes)
-      MOLR_CUDA(cudaMemcpyAsync(c->s1_codes + size_t(row0 + r) * c->d1, codes + r * c->d1,
-                                size_t(m) * c->d1, cudaMemcpyDefault, s));
+    if (codes && c->s1_codes) {
+      if (s1_interleaved(c->d1)) {
+        In e;
+        MOLR_TRY(e.stage(codes + r * c->d1, size_t(m) * c->d1, s));
+        codes_to_ilv_kernel<<<ctx->num_sms * 8, 256, 0, s>>>(e.as<int8_t>(), m, row0 + r, c->s1_codes);
+        MOLR_LAUNCHED(ctx);
+      } else {
+        MOLR_CUDA(cudaMemcpyAsync(c->s1_codes + size_t(row0 + r) * c->d1, codes + r * c->d1, size_t(m) * c->d1,
+                                  cudaMemcpyDefault, s));
+      }
+    }
     if (scales && c->s1_scales)
       MOLR_CUDA(cudaMemcpyAsync(c->s1_scales + row0 + r, scales + r, size_t(m) * 4, cudaMemcpyDefault, s));
   }
+  if (scales && c->s1_chunk_mm) MOLR_TRY(s1_update_chunk_mm(c, row0, n, s));
   int hbad = 0;
   MOLR_CUDA(cudaMemcpyAsync(&hbad, bad.p, 4, cudaMemcpyDeviceToHost, s));
   MOLR_CUDA(cudaStreamSynchronize(s));
@@ -271,6 +317,7 @@ int molr_cache_destroy(molr_cache* c) {
   cudaFree(c->s1_f32);
   cudaFree(c->s1_codes);
   cudaFree(c->s1_scales);
+  cudaFree(c->s1_chunk_mm);
   delete c;
   return MOLR_OK;
 }

@@ -135,7 +135,8 @@ struct molr_cache {
   float* gp_f32 = nullptr;             // (X, G) otherwise
   float* s1_f32 = nullptr;             // (X, d1)
   int8_t* s1_codes = nullptr;          // (X, d1)
-  float* s1_scales = nullptr;          // (X,)
+  float* s1_scales = nullptr;          // (X,) (padded like the codes)
+  float2* s1_chunk_mm = nullptr;       // per 32-row chunk (min, max) of s1_scales (d1 = 64)
   int64_t bytes = 0;
 };
 
@@ -290,6 +291,19 @@ __host__ __device__ __forceinline__ int emb_offset(int b, int k, int d, bool swz
   return swz ? b * d + ((((k >> 3) ^ (b & 7)) << 3) | (k & 7)) : b * d + k;
 }
 __host__ __device__ __forceinline__ bool emb_swizzled(int k_x, int d) { return d == 64 && (k_x % 8) == 0; }
+
+// Stage-1 int8 codes with d1 = 64 are stored in the tcgen05 K-major "interleave" (no-swizzle)
+// layout: blocks of 8 rows x 64 B = 512 B, each block ordered [16-byte K chunk c][row r%8][16 B],
+// so a bulk copy of 256 consecutive rows (16 KB) is directly an MMA operand (LBO 128 B, SBO
+// 512 B).  Rows are padded to a multiple of 256 (zero codes, zero scales).  Byte offset of 16-byte
+// chunk c of row r:
+__host__ __device__ __forceinline__ bool s1_interleaved(int d1) { return d1 == 64; }
+__host__ __device__ __forceinline__ int64_t s1_chunk_offset(int64_t r, int c, int d1) {
+  return d1 == 64 ? ((r >> 3) << 9) + (int64_t(c) << 7) + ((r & 7) << 4) : r * d1 + int64_t(c) * 16;
+}
+__host__ __device__ __forceinline__ int64_t s1_rows_alloc(int64_t X, int d1) {
+  return d1 == 64 ? (X + 255) / 256 * 256 : X;
+}
 
 __host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
 __host__ __device__ __forceinline__ int64_t imax64(int64_t a, int64_t b) { return a > b ? a : b; }

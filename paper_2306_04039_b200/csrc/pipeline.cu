@@ -100,10 +100,9 @@ filter_scan_kernel(int64_t n, int dim, const float* __restrict__ vf, const int8_
         key = f32_key(acc);
       } else {
         int32_t acc = 0;
-        const int4* cr = reinterpret_cast<const int4*>(codes + r * dim);
         const int4* qq = reinterpret_cast<const int4*>(qs + b * dim);
         for (int k = 0; k < dim / 16; ++k) {
-          int4 x = cr[k], y = qq[k];
+          int4 x = *reinterpret_cast<const int4*>(codes + s1_chunk_offset(r, k, dim)), y = qq[k];
           acc = __dp4a(x.x, y.x, acc);
           acc = __dp4a(x.y, y.y, acc);
           acc = __dp4a(x.z, y.z, acc);
@@ -128,8 +127,28 @@ __global__ void cap_segs_kernel(int B, int64_t cap, const int64_t* __restrict__ 
   }
 }
 
-// sort each candidate list so the downstream result never depends on atomic arrival order
-// (scores are per-pair and top-k ties break by id, so this is only for reproducible traces)
+// gather sampled stage-1 rows (codes interleaved + scales) into a contiguous padded operand
+__global__ void gather_sample_kernel(const int8_t* __restrict__ codes, const float* __restrict__ scales,
+                                     const int64_t* __restrict__ idx, int64_t n, int8_t* __restrict__ dcodes,
+                                     float* __restrict__ dscales) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * 4; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i >> 2;
+    const int c = int(i & 3);
+    const int64_t src = idx[r];
+    *reinterpret_cast<int4*>(dcodes + s1_chunk_offset(r, c, 64)) = *reinterpret_cast<const int4*>(codes + s1_chunk_offset(src, c, 64));
+    if (c == 0) dscales[r] = scales[src];
+  }
+}
+
+// gather interleaved stage-1 code rows (index_select)
+__global__ void gather_codes_kernel(const int8_t* __restrict__ src, const int64_t* __restrict__ idx, int64_t n,
+                                    int8_t* __restrict__ dst) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * 4; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i >> 2;
+    const int c = int(i & 3);
+    *reinterpret_cast<int4*>(dst + s1_chunk_offset(r, c, 64)) = *reinterpret_cast<const int4*>(src + s1_chunk_offset(idx[r], c, 64));
+  }
+}
 
 }  // namespace molr
 
@@ -260,8 +279,18 @@ int molr_index_select(molr_ctx* ctx, const molr_cache* c, int64_t n, const int64
     g(c->gp_bf16, r->gp_bf16, int64_t(c->G) * 2);
     g(c->gp_f32, r->gp_f32, int64_t(c->G) * 4);
     g(c->s1_f32, r->s1_f32, int64_t(c->d1) * 4);
-    g(c->s1_codes, r->s1_codes, int64_t(c->d1));
+    if (st == MOLR_OK && c->s1_codes) {
+      if (s1_interleaved(c->d1)) {
+        gather_codes_kernel<<<std::min(div_up(n * 4, 256), ctx->num_sms * 8), 256, 0, s>>>(c->s1_codes, ii.as<int64_t>(),
+                                                                                         n, r->s1_codes);
+        if (cudaGetLastError() != cudaSuccess) st = MOLR_ERR_CUDA;
+        ctx->launches++;
+      } else {
+        g(c->s1_codes, r->s1_codes, int64_t(c->d1));
+      }
+    }
     g(c->s1_scales, r->s1_scales, 4);
+    if (st == MOLR_OK && r->s1_chunk_mm) st = s1_update_chunk_mm(r, 0, n, s);
     if (st == MOLR_OK && cudaStreamSynchronize(s) != cudaSuccess) st = MOLR_ERR_CUDA;
     if (st) {
       molr_cache_destroy(r);
@@ -339,10 +368,25 @@ int molr_two_stage_top_k(molr_ctx* ctx, const molr_cache* c, const molr_gating* 
     Scratch ss, tkey;
     MOLR_TRY(ss.alloc(size_t(B) * lam * 4, s));
     MOLR_TRY(tkey.alloc(size_t(B) * 4, s));
-    {
+    const bool use_tc = s1_tc_supported(c, mode);
+    if (use_tc) {
+      // gather the sample rows into a contiguous operand, then the tensor-core scan writes scores
+      const int64_t lp = (lam + 255) / 256 * 256;
+      Scratch scodes, sscales;
+      MOLR_TRY(scodes.alloc(size_t(lp) * 64, s));
+      MOLR_TRY(sscales.alloc(size_t(lp) * 4, s));
+      MOLR_CUDA(cudaMemsetAsync(scodes.p, 0, size_t(lp) * 64, s));
+      MOLR_CUDA(cudaMemsetAsync(sscales.p, 0, size_t(lp) * 4, s));
+      gather_sample_kernel<<<std::min(div_up(lam * 4, 256), ctx->num_sms * 8), 256, 0, s>>>(
+          c->s1_codes, c->s1_scales, samp.as<int64_t>(), lam, scodes.as<int8_t>(), sscales.as<float>());
+      MOLR_LAUNCHED(ctx);
+      KTimer t(ctx, "stage1_sample_scan_tc", s, double(B) * lam);
+      MOLR_TRY(s1_tc_scan(ctx, mode, scodes.as<int8_t>(), sscales.as<float>(), nullptr, lam, B, qc.as<int8_t>(), nullptr,
+                          0, 0, nullptr, nullptr, ss.p, lam, s));
+    } else {
       KTimer t(ctx, "stage1_sample_scan", s, double(B) * lam);
-      MOLR_TRY(scan_scores(ctx, mode, lam, c->d1, c->s1_f32, c->s1_codes, c->s1_scales, samp.as<int64_t>(), B,
-                           q.as<float>(), qc.as<int8_t>(), ss.p, lam, s));
+      MOLR_TRY(scan_scores(ctx, mode, lam, c->d1, c->s1_f32, c->s1_codes, s1_interleaved(c->d1), c->s1_scales,
+                           samp.as<int64_t>(), B, q.as<float>(), qc.as<int8_t>(), ss.p, lam, s));
     }
     {
       KTimer t(ctx, "select_nth", s, double(B) * lam);
@@ -367,7 +411,12 @@ int molr_two_stage_top_k(molr_ctx* ctx, const molr_cache* c, const molr_gating* 
         MOLR_LAUNCHED(ctx);
         return MOLR_OK;
       };
-      {
+      if (use_tc) {
+        KTimer t(ctx, "stage1_filter_tc", s, double(B) * X);
+        MOLR_TRY(s1_tc_scan(ctx, mode, c->s1_codes, c->s1_scales, c->s1_chunk_mm, X, B, qc.as<int8_t>(),
+                            tkey.as<uint32_t>(), comparator == MOLR_STRICT, cap, cand.as<int32_t>(), counts.as<int64_t>(),
+                            nullptr, 0, s));
+      } else {
         KTimer t(ctx, "stage1_filter_scan", s, double(B) * X);
         if (mode == MOLR_S1_FLOAT) MOLR_TRY(launch(filter_scan_kernel<MOLR_S1_FLOAT>));
         else if (mode == MOLR_S1_INT8) MOLR_TRY(launch(filter_scan_kernel<MOLR_S1_INT8>));

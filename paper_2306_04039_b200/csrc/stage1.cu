@@ -44,26 +44,29 @@ int quantize_rows(molr_ctx* ctx, int64_t rows, int dim, const float* x, int8_t* 
 // ------------------------------------------------------------------------------------------
 // scans: out[b*ld + r] for B queries against rows [0, n) of a stage-1 view
 // ------------------------------------------------------------------------------------------
-__device__ __forceinline__ int32_t dot_i8(const int8_t* __restrict__ a, const int8_t* __restrict__ b, int dim) {
+// int8 dot of stage-1 row r (cache layout, see s1_chunk_offset) with a linear query
+__device__ __forceinline__ int32_t dot_row_i8(const int8_t* __restrict__ codes, int64_t r, const int8_t* __restrict__ q,
+                                              int dim, bool ilv) {
   int32_t acc = 0;
-  if ((dim & 15) == 0 && ((uintptr_t)a & 15) == 0 && ((uintptr_t)b & 15) == 0) {
-    for (int k = 0; k < dim; k += 16) {
-      int4 x = *reinterpret_cast<const int4*>(a + k);
-      int4 y = *reinterpret_cast<const int4*>(b + k);
+  if ((dim & 15) == 0 && ((uintptr_t)q & 15) == 0 && (ilv || ((uintptr_t)codes & 15) == 0)) {
+    for (int c = 0; c < dim / 16; ++c) {
+      const int4 x = *reinterpret_cast<const int4*>(codes + (ilv ? s1_chunk_offset(r, c, dim) : r * dim + c * 16));
+      const int4 y = *reinterpret_cast<const int4*>(q + c * 16);
       acc = __dp4a(x.x, y.x, acc);
       acc = __dp4a(x.y, y.y, acc);
       acc = __dp4a(x.z, y.z, acc);
       acc = __dp4a(x.w, y.w, acc);
     }
   } else {
-    for (int k = 0; k < dim; ++k) acc += int32_t(a[k]) * int32_t(b[k]);
+    const int8_t* a = codes + r * dim;
+    for (int k = 0; k < dim; ++k) acc += int32_t(a[k]) * int32_t(q[k]);
   }
   return acc;
 }
 
 // mode: MOLR_S1_FLOAT (f32 out), MOLR_S1_INT8 (f32 out = acc.f32 * scale), MOLR_S1_INT8_RAW (i32 out)
 __global__ void scan_scores_kernel(int mode, int64_t n, int dim, const float* __restrict__ vf,
-                                   const int8_t* __restrict__ codes, const float* __restrict__ scales,
+                                   const int8_t* __restrict__ codes, bool ilv, const float* __restrict__ scales,
                                    const int64_t* __restrict__ rows_idx, int B, const float* __restrict__ qf,
                                    const int8_t* __restrict__ qc, void* __restrict__ out, int64_t ld) {
   extern __shared__ __align__(16) unsigned char sq[];
@@ -83,10 +86,9 @@ __global__ void scan_scores_kernel(int mode, int64_t n, int dim, const float* __
         reinterpret_cast<float*>(out)[b * ld + i] = acc;
       }
     } else {
-      const int8_t* c = codes + r * dim;
       const float scale = mode == MOLR_S1_INT8 ? scales[r] : 0.f;
       for (int b = 0; b < B; ++b) {
-        int32_t acc = dot_i8(c, reinterpret_cast<const int8_t*>(sq) + b * dim, dim);
+        int32_t acc = dot_row_i8(codes, r, reinterpret_cast<const int8_t*>(sq) + b * dim, dim, ilv);
         if (mode == MOLR_S1_INT8_RAW) reinterpret_cast<int32_t*>(out)[b * ld + i] = acc;
         else reinterpret_cast<float*>(out)[b * ld + i] = __fmul_rn((float)acc, scale);
       }
@@ -94,7 +96,7 @@ __global__ void scan_scores_kernel(int mode, int64_t n, int dim, const float* __
   }
 }
 
-int scan_scores(molr_ctx* ctx, int mode, int64_t n, int dim, const float* vf, const int8_t* codes,
+int scan_scores(molr_ctx* ctx, int mode, int64_t n, int dim, const float* vf, const int8_t* codes, bool ilv,
                 const float* scales, const int64_t* rows_idx, int B, const float* qf, const int8_t* qc, void* out,
                 int64_t ld, cudaStream_t s) {
   if (n <= 0 || B <= 0) return MOLR_OK;
@@ -108,7 +110,7 @@ int scan_scores(molr_ctx* ctx, int mode, int64_t n, int dim, const float* vf, co
     size_t esz = mode == MOLR_S1_INT8_RAW ? 4 : 4;
     void* o = reinterpret_cast<char*>(out) + size_t(b0) * ld * esz;
     scan_scores_kernel<<<blocks, 256, size_t(bb) * per_q, s>>>(
-        mode, n, dim, vf, codes, scales, rows_idx, bb, qf ? qf + size_t(b0) * dim : nullptr,
+        mode, n, dim, vf, codes, ilv, scales, rows_idx, bb, qf ? qf + size_t(b0) * dim : nullptr,
         qc ? qc + size_t(b0) * dim : nullptr, o, ld);
     MOLR_LAUNCHED(ctx);
   }
@@ -310,7 +312,7 @@ int molr_int8_matvec(molr_ctx* ctx, int64_t n, int dim, const int8_t* codes, con
   MOLR_TRY(qq.stage(q, size_t(dim), s));
   MOLR_TRY(o.stage(out, size_t(n) * 4, s));
   // raw mode over an ad-hoc view: scales unused
-  MOLR_TRY(scan_scores(ctx, MOLR_S1_INT8_RAW, n, dim, nullptr, c.as<int8_t>(), nullptr, nullptr, 1, nullptr,
+  MOLR_TRY(scan_scores(ctx, MOLR_S1_INT8_RAW, n, dim, nullptr, c.as<int8_t>(), false, nullptr, nullptr, 1, nullptr,
                        qq.as<int8_t>(), o.dptr, n, s));
   return finish_outputs(s, {&o});
 }
@@ -332,7 +334,7 @@ int molr_stage1_scores(molr_ctx* ctx, const molr_cache* c, int mode, int B, cons
     MOLR_TRY(qs.alloc(size_t(B) * 4, s));
     MOLR_TRY(prepare_queries(ctx, mode, B, c->d1, qi.as<float>(), qc.as<int8_t>(), qs.as<float>(), s));
   }
-  MOLR_TRY(scan_scores(ctx, mode, c->X, c->d1, c->s1_f32, c->s1_codes, c->s1_scales, nullptr, B, qi.as<float>(),
+  MOLR_TRY(scan_scores(ctx, mode, c->X, c->d1, c->s1_f32, c->s1_codes, s1_interleaved(c->d1), c->s1_scales, nullptr, B, qi.as<float>(),
                        qc.as<int8_t>(), o.dptr, c->X, s));
   return finish_outputs(s, {&o});
 }
@@ -362,7 +364,7 @@ int molr_h_indexer(molr_ctx* ctx, const molr_cache* c, int mode, int B, const fl
     MOLR_TRY(qs.alloc(size_t(B) * 4, s));
     MOLR_TRY(prepare_queries(ctx, mode, B, c->d1, qi.as<float>(), qc.as<int8_t>(), qs.as<float>(), s));
   }
-  MOLR_TRY(scan_scores(ctx, mode, c->X, c->d1, c->s1_f32, c->s1_codes, c->s1_scales, nullptr, B, qi.as<float>(),
+  MOLR_TRY(scan_scores(ctx, mode, c->X, c->d1, c->s1_f32, c->s1_codes, s1_interleaved(c->d1), c->s1_scales, nullptr, B, qi.as<float>(),
                        qc.as<int8_t>(), scores.p, c->X, s));
   // 2. threshold = n-th largest of the SAME score array at the sampled rows (hindexer.py:156-158)
   Scratch tkey;

@@ -4,7 +4,7 @@
 
 namespace molr {
 
-int scan_scores(molr_ctx* ctx, int mode, int64_t n, int dim, const float* vf, const int8_t* codes,
+int scan_scores(molr_ctx* ctx, int mode, int64_t n, int dim, const float* vf, const int8_t* codes, bool ilv,
                 const float* scales, const int64_t* rows_idx, int B, const float* qf, const int8_t* qc, void* out,
                 int64_t ld, cudaStream_t s);
 int compact_passers(molr_ctx* ctx, int B, int64_t n, const void* sc, int is_int, int64_t ld, const uint32_t* tkey,
@@ -13,6 +13,11 @@ int gather_rows(molr_ctx* ctx, int64_t m, int64_t dim_bytes, const void* src, co
                 cudaStream_t s);
 int prepare_queries(molr_ctx* ctx, int mode, int B, int dim, const float* q, int8_t* qc, float* qs, cudaStream_t s);
 int check_view(const molr_cache* c, int mode);
+bool s1_tc_supported(const molr_cache* c, int mode);
+int s1_tc_scan(molr_ctx* ctx, int mode, const int8_t* codes, const float* scales, const float2* mm, int64_t n, int B,
+               const int8_t* qcodes, const uint32_t* tkeys, int strict, int64_t cap, int32_t* cand, int64_t* counts,
+               void* out, int64_t ld, cudaStream_t s);
+int s1_update_chunk_mm(molr_cache* c, int64_t row0, int64_t n, cudaStream_t s);
 int int_to_float_inplace(molr_ctx* ctx, int32_t* p, int64_t n, cudaStream_t s);
 
 }  // namespace molr

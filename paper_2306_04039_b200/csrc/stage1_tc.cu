@@ -1,0 +1,372 @@
+// Stage-1 corpus scan on the tensor cores: tcgen05 kind::i8 (s8 x s8 -> s32, exact) over
+// [B queries x 64] x [items x 64]^T, with the h-indexer threshold filter fused into the TMEM
+// epilogue (hindexer.py:94-112, 155-163; quant.py:83-90).  The B x X score matrix never exists:
+// each (query, 256-item) tile of int32 accumulators is tested in registers and only passers are
+// appended to the query's candidate list.  A second epilogue variant writes the scores (used for
+// the lambda-row threshold sample, where the scores feed the n-th-largest selection).
+//
+// Layout: queries (B <= 1024, padded to blocks of 128) stay resident in shared memory for the
+// whole launch (64 KB); item tiles of 256 rows (16 KB of codes in the cache's interleaved
+// layout + 1 KB of scales + per-32-row scale min/max) stream through a 4-stage ring by bulk copy.
+// Per tile, MMA (M=128 queries, N=256 items, K=64 as 2 x K=32) per query block into one of two
+// 256-column TMEM accumulators; two epilogue warpgroups alternate blocks.
+//
+// Exactness (int8 view, hindexer.py:111): score = fl(float(acc) * scale_row), compared with the
+// threshold t in fp32 exactly like NumPy.  The fast path compares acc against an integer bound L
+// that is necessary for passing anywhere in the 32-row chunk (from the chunk's scale min/max),
+// then re-checks the few survivors exactly.  Raw mode (raw_int_ordering) compares acc directly.
+#include <algorithm>
+
+#include "kernels.cuh"
+#include "stage1.cuh"
+
+namespace molr {
+namespace s1tc {
+
+constexpr int NT = 256;    // items per tile (MMA N)
+constexpr int QB = 128;    // queries per block (MMA M)
+constexpr int MAXQB = 8;   // queries per launch <= 1024
+constexpr int NSTAGE = 4;
+constexpr int SZ_CODES = NT * 64;                 // 16 KB
+constexpr int SZ_STAGE = SZ_CODES + NT * 4 + 1024;  // codes + scales + chunk min/max, 1 KB aligned: 18 KB
+constexpr int OFF_A = 0;                          // MAXQB x 8 KB query codes (interleave)
+constexpr int OFF_RING = OFF_A + MAXQB * 8192;
+constexpr int OFF_T = OFF_RING + NSTAGE * SZ_STAGE;  // per-query threshold (f32 or s32), 4 KB
+constexpr int OFF_BAR = OFF_T + MAXQB * QB * 4;
+constexpr int NBAR = 2 * NSTAGE + 4;
+constexpr int OFF_TMEM = OFF_BAR + NBAR * 8;
+constexpr int SMEM_BYTES = OFF_TMEM + 16;
+
+enum Mode { FILTER_SCALED = 0, FILTER_RAW = 1, WRITE_SCALED = 2, WRITE_RAW = 3 };
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(bar),
+      "r"(parity), "r"(0x989680)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ uint64_t desc_ilv(uint32_t addr) {  // interleave K-major: LBO 128 B (K), SBO 512 B (rows)
+  return uint64_t((addr >> 4) & 0x3FFF) | (uint64_t(128 >> 4) << 16) | (uint64_t(512 >> 4) << 32) | (1ull << 46);
+}
+// kind::i8: A = B = signed 8-bit, D = s32, K-major, M = 128, N = 256
+constexpr uint32_t IDESC_I8 = (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(NT >> 3) << 17) | (uint32_t(QB >> 4) << 24);
+__device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(IDESC_I8), "r"(accum)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+#define TMEM_LD32(taddr, r)                                                                                         \
+  asm volatile(                                                                                                     \
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19," \
+      "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                                                   \
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),  \
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),       \
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),      \
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])                    \
+      : "r"(taddr))
+
+struct Params {
+  const int8_t* codes;    // interleaved rows, padded to NT
+  const float* scales;    // padded
+  const float2* chunk_mm; // per 32 rows (min, max) scale
+  int64_t n;              // valid rows
+  int B;                  // queries in this launch (<= 1024)
+  const int8_t* qcodes;   // (B, 64) linear
+  const uint32_t* tkeys;  // (B,) ascending-order threshold keys (filter modes)
+  int strict;
+  int64_t cap;
+  int32_t* cand;          // (B, cap)
+  unsigned long long* counts;  // (B,)
+  void* out;              // write modes: (B, ld) f32 / s32
+  int64_t ld;
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(64 + 256, 1) s1_tc_kernel(Params P) {
+  constexpr bool WRITE = MODE >= WRITE_SCALED;
+  constexpr bool RAW = (MODE == FILTER_RAW || MODE == WRITE_RAW);
+  extern __shared__ __align__(1024) uint8_t sm[];
+  const uint32_t sbase = smem_u32(sm);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nqb = (P.B + QB - 1) / QB;
+  const int64_t ntiles = (P.n + NT - 1) / NT;
+  auto bar = [&](int i) { return sbase + OFF_BAR + 8 * i; };
+  auto full_bar = [&](int s) { return bar(s); };
+  auto empty_bar = [&](int s) { return bar(NSTAGE + s); };
+  auto tfull = [&](int e) { return bar(2 * NSTAGE + e); };
+  auto tempty = [&](int e) { return bar(2 * NSTAGE + 2 + e); };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + OFF_TMEM);
+
+  // ---- setup: query codes -> interleave operand blocks (zero padded), thresholds, barriers ----
+  for (int i = threadIdx.x; i < nqb * QB * 4; i += blockDim.x) {
+    const int q = i >> 2, c = i & 3;
+    int4 v = make_int4(0, 0, 0, 0);
+    if (q < P.B) v = __ldg(reinterpret_cast<const int4*>(P.qcodes + int64_t(q) * 64) + c);
+    const int qb = q / QB, m = q % QB;
+    *reinterpret_cast<int4*>(sm + OFF_A + qb * 8192 + (m >> 3) * 512 + c * 128 + (m & 7) * 16) = v;
+  }
+  if (!WRITE)
+    for (int q = threadIdx.x; q < nqb * QB; q += blockDim.x) {
+      uint32_t t = 0;
+      if (q < P.B) t = RAW ? uint32_t(key_i32(__ldg(P.tkeys + q))) : __float_as_uint(key_f32(__ldg(P.tkeys + q)));
+      reinterpret_cast<uint32_t*>(sm + OFF_T)[q] = t;
+    }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NSTAGE; ++s) {
+      mbar_init(full_bar(s), 1);
+      mbar_init(empty_bar(s), 1 + 256);
+    }
+    for (int e = 0; e < 2; ++e) {
+      mbar_init(tfull(e), 1);
+      mbar_init(tempty(e), 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)), "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ================= producer =================
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        mbar_wait(empty_bar(stage), phase ^ 1);
+        const uint32_t st = sbase + OFF_RING + stage * SZ_STAGE;
+        mbar_arrive_expect_tx(full_bar(stage), SZ_CODES + NT * 4 + (WRITE ? 0 : 64));
+        bulk_g2s(st, P.codes + tile * SZ_CODES, SZ_CODES, full_bar(stage));
+        bulk_g2s(st + SZ_CODES, P.scales + tile * NT, NT * 4, full_bar(stage));
+        if (!WRITE) bulk_g2s(st + SZ_CODES + NT * 4, P.chunk_mm + tile * (NT / 32), 64, full_bar(stage));
+        if (++stage == NSTAGE) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ================= MMA issuer =================
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      uint32_t eph[2] = {0, 0};
+      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        mbar_wait(full_bar(stage), phase);
+        tc_fence_after();
+        const uint32_t bt = sbase + OFF_RING + stage * SZ_STAGE;
+        for (int qb = 0; qb < nqb; ++qb) {
+          const int e = qb & 1;
+          mbar_wait(tempty(e), eph[e] ^ 1);
+          eph[e] ^= 1;
+          tc_fence_after();
+          const uint32_t at = sbase + OFF_A + qb * 8192;
+          mma_i8(tmem_base + e * 256, desc_ilv(at), desc_ilv(bt), 0);
+          mma_i8(tmem_base + e * 256, desc_ilv(at + 256), desc_ilv(bt + 256), 1);
+          mma_commit(tfull(e));
+        }
+        mma_commit(empty_bar(stage));
+        if (++stage == NSTAGE) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    // ================= epilogue warpgroups =================
+    const int e = (warp - 2) >> 2;
+    const int quarter = warp & 3;
+    const int p = quarter * 32 + lane;
+    const uint32_t tm = tmem_base + e * 256 + ((uint32_t)(quarter * 32) << 16);
+    int stage = 0;
+    uint32_t phase = 0, tph = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      mbar_wait(full_bar(stage), phase);  // scales / chunk min-max of this tile are in smem
+      const uint8_t* st = sm + OFF_RING + stage * SZ_STAGE;
+      const float* sc = reinterpret_cast<const float*>(st + SZ_CODES);
+      const float2* mm = reinterpret_cast<const float2*>(st + SZ_CODES + NT * 4);
+      const int64_t row0 = tile * NT;
+      const int nvalid = (int)imin64(NT, P.n - row0);
+      for (int qb = e; qb < nqb; qb += 2) {
+        const int q = qb * QB + p;
+        mbar_wait(tfull(e), tph);
+        tph ^= 1;
+        tc_fence_after();
+        if (WRITE) {
+#pragma unroll 1
+          for (int cc = 0; cc < NT / 32; ++cc) {
+            uint32_t a[32];
+            TMEM_LD32(tm + cc * 32, a);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            if (q < P.B) {
+              const int j0 = cc * 32;
+              if (RAW) {
+                int32_t* o = reinterpret_cast<int32_t*>(P.out) + int64_t(q) * P.ld + row0 + j0;
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                  if (j0 + j < nvalid) o[j] = int32_t(a[j]);
+              } else {
+                float* o = reinterpret_cast<float*>(P.out) + int64_t(q) * P.ld + row0 + j0;
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                  if (j0 + j < nvalid) o[j] = __fmul_rn((float)int32_t(a[j]), sc[j0 + j]);
+              }
+            }
+          }
+        } else {
+          const uint32_t traw = reinterpret_cast<const uint32_t*>(sm + OFF_T)[q];
+          const float tf = __uint_as_float(traw);
+          const int32_t ti = int32_t(traw);
+          uint32_t mask[NT / 32];
+          int total = 0;
+#pragma unroll
+          for (int cc = 0; cc < NT / 32; ++cc) {
+            uint32_t a[32];
+            TMEM_LD32(tm + cc * 32, a);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            int32_t L;
+            if (RAW) {
+              L = P.strict ? ti + 1 : ti;  // exact
+            } else {
+              const float2 m2 = mm[cc];
+              if (!(m2.y > 0.f)) {
+                L = 0x7fffffff;  // chunk of padding rows only
+              } else {
+                const float l = fminf(tf * (1.0f - 1e-6f) / m2.y, tf * (1.0f + 1e-6f) / m2.x);
+                L = l <= -1073741824.f ? -1073741824 : (l >= 1073741824.f ? 1073741824 : int32_t(floorf(l)) - 1);
+              }
+            }
+            uint32_t m = 0;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) m |= uint32_t(int32_t(a[j]) >= L) << j;
+            const int j0 = cc * 32;
+            if (nvalid - j0 < 32) m &= (nvalid - j0 <= 0) ? 0u : ((1u << (nvalid - j0)) - 1u);
+            if (!RAW) {
+              uint32_t mm2 = m;
+              while (mm2) {  // exact re-check of the few survivors: fl(acc * scale) vs t
+                const int j = __ffs(mm2) - 1;
+                mm2 &= mm2 - 1;
+                uint32_t aj = a[0];
+#pragma unroll
+                for (int k = 1; k < 32; ++k) aj = (k == j) ? a[k] : aj;
+                const float s = __fmul_rn((float)int32_t(aj), sc[j0 + j]);
+                const bool ok = P.strict ? (s > tf) : (s >= tf);
+                if (!ok) m &= ~(1u << j);
+              }
+            }
+            mask[cc] = m;
+            total += __popc(m);
+          }
+          if (total && q < P.B) {
+            unsigned long long pos = atomicAdd(P.counts + q, (unsigned long long)total);
+#pragma unroll
+            for (int cc = 0; cc < NT / 32; ++cc) {
+              uint32_t m = mask[cc];
+              while (m) {
+                const int j = __ffs(m) - 1;
+                m &= m - 1;
+                if ((int64_t)pos < P.cap) P.cand[int64_t(q) * P.cap + (int64_t)pos] = int32_t(row0 + cc * 32 + j);
+                ++pos;
+              }
+            }
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(tempty(e));
+      }
+      mbar_arrive(empty_bar(stage));
+      if (++stage == NSTAGE) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+    // the other warpgroup's arrivals on empty barriers: WG 1 also walks all tiles (above)
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
+}
+
+}  // namespace s1tc
+
+bool s1_tc_supported(const molr_cache* c, int mode) {
+  return c && mode != MOLR_S1_FLOAT && c->d1 == 64 && c->s1_codes && c->s1_chunk_mm && !getenv("MOLR_DISABLE_TC");
+}
+
+// Scan rows [0, n) of an interleaved code matrix against B queries (chunks of 1024 per launch).
+// filter: tkeys != nullptr -> append passers to cand / counts; else write scores to out (B, ld).
+int s1_tc_scan(molr_ctx* ctx, int mode, const int8_t* codes, const float* scales, const float2* mm, int64_t n, int B,
+               const int8_t* qcodes, const uint32_t* tkeys, int strict, int64_t cap, int32_t* cand, int64_t* counts,
+               void* out, int64_t ld, cudaStream_t s) {
+  using namespace s1tc;
+  if (n <= 0 || B <= 0) return MOLR_OK;
+  const bool raw = mode == MOLR_S1_INT8_RAW;
+  const int m = tkeys ? (raw ? FILTER_RAW : FILTER_SCALED) : (raw ? WRITE_RAW : WRITE_SCALED);
+  const int64_t ntiles = (n + NT - 1) / NT;
+  const int grid = (int)std::min<int64_t>(ntiles, ctx->num_sms);
+  for (int b0 = 0; b0 < B; b0 += MAXQB * QB) {
+    Params P;
+    P.codes = codes;
+    P.scales = scales;
+    P.chunk_mm = mm;
+    P.n = n;
+    P.B = std::min(B - b0, MAXQB * QB);
+    P.qcodes = qcodes + int64_t(b0) * 64;
+    P.tkeys = tkeys ? tkeys + b0 : nullptr;
+    P.strict = strict;
+    P.cap = cap;
+    P.cand = cand ? cand + int64_t(b0) * cap : nullptr;
+    P.counts = reinterpret_cast<unsigned long long*>(counts ? counts + b0 : nullptr);
+    P.out = out ? reinterpret_cast<char*>(out) + int64_t(b0) * ld * 4 : nullptr;
+    P.ld = ld;
+    auto launch = [&](auto kern) -> int {
+      MOLR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+      kern<<<grid, 64 + 256, SMEM_BYTES, s>>>(P);
+      MOLR_LAUNCHED(ctx);
+      return MOLR_OK;
+    };
+    switch (m) {
+      case FILTER_SCALED: MOLR_TRY(launch(s1_tc_kernel<FILTER_SCALED>)); break;
+      case FILTER_RAW: MOLR_TRY(launch(s1_tc_kernel<FILTER_RAW>)); break;
+      case WRITE_SCALED: MOLR_TRY(launch(s1_tc_kernel<WRITE_SCALED>)); break;
+      default: MOLR_TRY(launch(s1_tc_kernel<WRITE_RAW>)); break;
+    }
+  }
+  return MOLR_OK;
+}
+
+}  // namespace molr

@@ -446,21 +446,20 @@ def test_launch_counter_moves():
 
 
 # ---------------------------------------------------------------------------------- tcgen05 path
-def _synthetic_prod_cache(n_items, seed=0, gate_scale=1.0):
+def _synthetic_prod_cache(n_items, seed=0, gate_scale=1.0, n_users=32):
     """Production-shape synthetic corpus (bf16-representable) through the oracle generator."""
     from paper_2306_04039_b200.mol import ItemCache, MoLConfig
     from paper_2306_04039_b200.quant import quantize_rowwise
 
-    syn = O.init_synthetic(32, n_items, k_u=8, k_x=8, d=64, gating_hidden=128, seed=seed)
+    syn = O.init_synthetic(n_users, n_items, k_u=8, k_x=8, d=64, gating_hidden=128, seed=seed)
     c = O.build_item_cache(syn.item_table, syn.item_proj, syn.gating.item_net, 8, 64, 20.0, 8, quantized=False)
     embs = O.round_bf16(c.item_embs)
     gp = O.round_bf16(c.item_gate_pre * gate_scale)
     s1 = embs.mean(axis=1).astype(np.float32)
     cfg = MoLConfig(k_u=8, k_x=8, d=64, tau=20.0, gating_hidden=128, dropout_p=0.0)
     cache = ItemCache(config=cfg, item_embs=embs, item_gate_pre=gp, stage1_embs=s1, stage1_q=quantize_rowwise(s1))
-    ue = O.user_components(syn, np.arange(32), 8, 64).astype(np.float32)
-    g = syn.gating
-    return cache, syn, ue, syn.user_table[:32]
+    ue = O.user_components(syn, np.arange(n_users), 8, 64).astype(np.float32)
+    return cache, syn, ue, syn.user_table[:n_users]
 
 
 def _prod_gating(syn, cross_scale=1.0):
@@ -520,3 +519,47 @@ def test_tc_kernel_candidates_partial_tiles():
         ref_all[lists[u]] = O.score_candidates(oc, og, lists[u], ue[u], feats[u])
         oi, _ = O.mol_top_k(oc, og, lists[u], ue[u], feats[u], 50)
         assert topk_equal_modulo_ties(ids[u], oi, ref_all)
+
+
+@pytest.mark.parametrize("strict,raw", [(False, False), (True, False), (False, True)])
+def test_batched_stage1_tc_counts_exact(strict, raw):
+    """Tensor-core int8 scan + fused filter: with lambda = X the threshold is the exact n-th largest
+    stage-1 score, so every query's passer count must equal the oracle's h_indexer count bit for bit
+    (200k items, 300 queries = 3 query blocks, all comparator / ordering modes)."""
+    from paper_2306_04039_b200.engine import two_stage_top_k
+    from paper_2306_04039_b200.hindexer import HIndexerConfig
+
+    cache, syn, ue, feats = _synthetic_prod_cache(200_000, seed=13, n_users=300)
+    gating, og = _prod_gating(syn)
+    X = cache.num_items
+    kp = 2000
+    hcfg = HIndexerConfig(k_prime=kp, lam=X, quantized=True, comparator="strict" if strict else "inclusive",
+                          raw_int_ordering=raw)
+    uw = gating.user_net(feats)
+    ids, sc, cand = two_stage_top_k(cache, gating, ue, uw, 10, hcfg, seed=1)
+    q = O.Quant(cache.stage1_q.codes, cache.stage1_q.scales)
+    for u in range(ue.shape[0]):
+        c_ids, t, _ = O.h_indexer(q, ue[u].mean(axis=0), kp, O.make_rng(0), lam=X,
+                                  comparator="strict" if strict else "inclusive", raw_int_ordering=raw)
+        assert cand[u] == c_ids.size, (u, cand[u], c_ids.size)
+
+
+def test_batched_two_stage_recall_device_sample():
+    """Device-drawn sample (lambda = 1% of X): candidate counts near K' and top-100 recall vs the
+    oracle's exact MoL top-100 >= 0.99 (north-star bar), 100k items."""
+    from paper_2306_04039_b200.engine import two_stage_top_k
+    from paper_2306_04039_b200.hindexer import HIndexerConfig
+
+    cache, syn, ue, feats = _synthetic_prod_cache(100_000, seed=21, n_users=64)
+    gating, og = _prod_gating(syn)
+    hcfg = HIndexerConfig(k_prime=5000, sample_ratio=0.05, quantized=True)
+    uw = gating.user_net(feats)
+    ids, sc, cand = two_stage_top_k(cache, gating, ue, uw, 100, hcfg, seed=7)
+    assert np.all(np.abs(cand - 5000) < 5000 * 0.25), cand
+    oc = O.Cache(cache.item_embs, cache.item_gate_pre, cache.stage1_embs, None, 20.0, 8)
+    rec = []
+    for u in range(16):
+        ex, _ = O.full_top_k(oc, og, ue[u], feats[u], 100)
+        rec.append(len(set(ex.tolist()) & set(ids[u].tolist())) / 100)
+    print("recall", np.mean(rec))
+    assert np.mean(rec) >= 0.99
