@@ -316,10 +316,12 @@ def main():
     lib = L.load()
     ctx = L.ctx(local)
     X, B, k = cfg["X"], cfg["B"], cfg["k"]
-    lo, hi = rank * X // world, (rank + 1) * X // world
+    from paper_2306_04039_b200.sharding import local_k_prime, local_lambda, shard_range
+
+    lo, hi = shard_range(X, world, rank)
     Xl = hi - lo
-    kp_local = max(1, math.ceil(cfg["k_prime"] / world))
-    lam_local = max(1, round(cfg["ratio"] * Xl))
+    kp_local = local_k_prime(cfg["k_prime"], world)
+    lam_local = local_lambda(Xl, sample_ratio=cfg["ratio"])
 
     model = synthetic_model()
     t_build = time.perf_counter()

@@ -19,7 +19,9 @@
 //   E1: h = silu(D1) -> A2 = [bf16(h) | bf16(h - bf16(h))] written in place over D1 (each
 //       16-column chunk: 8 cols hi + 8 cols lo); keeping h to ~2^-17 keeps the cross-net within
 //       tolerance for sharp gating
-//   L2: A2 (TMEM, K = 256) . [W2^T ; W2^T] -> D2 cols [64,128)
+//   L2: h_hi.W2_hi + h_lo.W2_hi + h_hi.W2_lo (A from TMEM, W2 split hi/lo in smem) -> D2 cols
+//       [64,128): the cross net's second layer is carried to ~2^-16 (W2 rounding dominated the
+//       error budget under sharp gating)
 //   E2: pi = softmax(silu(uw * gate_pre + D2)); score = sum pi * CLT  -> global
 // The G logits and H hidden units never leave the SM.
 #include <algorithm>
@@ -44,7 +46,8 @@ constexpr int SZ_STAGE = GROUP * 1024;                  // 16 KB
 constexpr int OFF_RING = 0;
 constexpr int OFF_W1T = OFF_RING + NSTAGE * SZ_STAGE;   // 128 x 64 bf16, SW128      16 KB
 constexpr int OFF_W2T = OFF_W1T + 16384;                // 2 x (64 x 64) bf16, SW128 16 KB
-constexpr int OFF_W1B = OFF_W2T + 16384;                // 128 x 16 bf16, interleave  4 KB
+constexpr int OFF_W2L = OFF_W2T + 16384;                // W2^T residual bf16(W2 - bf16(W2))     16 KB
+constexpr int OFF_W1B = OFF_W2L + 16384;                // 128 x 16 bf16, interleave  4 KB
 constexpr int OFF_BIASA = OFF_W1B + 4096;               // 128 x 16 bf16, interleave  4 KB
 constexpr int OFF_GRP = OFF_BIASA + 4096;               // per epilogue group:
 constexpr int G_B0 = 0;                                 //   16 x 64 bf16 SW128 (u_hi ; u_lo)  2 KB
@@ -224,7 +227,7 @@ struct Params {
   const __nv_bfloat16* embs;  // (X, 8, 64) pre-swizzled item blocks
   const __nv_bfloat16* gp;    // (X, 64)
   const __nv_bfloat16* w1t;   // SW128 image (16 KB)
-  const __nv_bfloat16* w2t;   // SW128 image (16 KB)
+  const __nv_bfloat16* w2t;   // SW128 image (16 KB), followed by the residual image (16 KB)
   const __nv_bfloat16* w1b;   // interleave image (4 KB)
   const float* user_embs;     // (B, 8, 64)
   const float* uw;            // (B, 64)
@@ -258,6 +261,7 @@ __global__ void __launch_bounds__(64 + NE * 128, 1) mol_tc_kernel(Params P, cons
     for (int i = threadIdx.x; i < 1024; i += blockDim.x) {
       reinterpret_cast<uint4*>(sm + OFF_W1T)[i] = __ldg(src1 + i);
       reinterpret_cast<uint4*>(sm + OFF_W2T)[i] = __ldg(src2 + i);
+      reinterpret_cast<uint4*>(sm + OFF_W2L)[i] = __ldg(src2 + 1024 + i);
     }
     for (int i = threadIdx.x; i < 256; i += blockDim.x) reinterpret_cast<uint4*>(sm + OFF_W1B)[i] = __ldg(src3 + i);
     // bias A operand: K columns 0 and 1 of every row = 1.0 (pairs with the b1 hi / lo rows of W1B)
@@ -387,10 +391,12 @@ __global__ void __launch_bounds__(64 + NE * 128, 1) mol_tc_kernel(Params P, cons
             if (!mbar_test(gbar(g, 4), gphase[g])) continue;
             tc_fence_after();
 #pragma unroll
-            for (int ch = 0; ch < 8; ++ch) {  // hidden chunk ch = K [16ch, 16ch+16): hi then lo
-              const uint64_t bd = desc_sw128(sbase + OFF_W2T + (ch >> 2) * 8192 + (ch & 3) * 32);
-              mma_bf16_ts(tm + 64, tm + 128 + ch * 16, bd, ID64, ch > 0);
-              mma_bf16_ts(tm + 64, tm + 128 + ch * 16 + 8, bd, ID64, 1);
+            for (int ch = 0; ch < 8; ++ch) {  // hidden chunk ch = K [16ch, 16ch+16)
+              const uint32_t bo = (ch >> 2) * 8192 + (ch & 3) * 32;
+              const uint64_t bhi = desc_sw128(sbase + OFF_W2T + bo), blo = desc_sw128(sbase + OFF_W2L + bo);
+              mma_bf16_ts(tm + 64, tm + 128 + ch * 16, bhi, ID64, ch > 0);  // h_hi . W2_hi
+              mma_bf16_ts(tm + 64, tm + 128 + ch * 16 + 8, bhi, ID64, 1);   // h_lo . W2_hi
+              mma_bf16_ts(tm + 64, tm + 128 + ch * 16, blo, ID64, 1);       // h_hi . W2_lo
             }
             mma_commit(gbar(g, 5));
             gstate[g] = 0;
@@ -622,7 +628,7 @@ extern "C" int molr_gating_tc_prepare(molr_gating* g) {
   MOLR_CUDA(cudaMemcpy(w1.data(), g->w1, w1.size() * 4, cudaMemcpyDefault));
   MOLR_CUDA(cudaMemcpy(b1.data(), g->b1, b1.size() * 4, cudaMemcpyDefault));
   MOLR_CUDA(cudaMemcpy(w2.data(), g->w2, w2.size() * 4, cudaMemcpyDefault));
-  std::vector<__nv_bfloat16> img(8192 + 2048 + 8192, __float2bfloat16(0.0f));
+  std::vector<__nv_bfloat16> img(8192 + 2048 + 8192 + 8192, __float2bfloat16(0.0f));
   auto sw = [](int r, int k) {  // element offset in an SW128 K-major [rows x 64] region
     return (r >> 3) * 512 + (r & 7) * 64 + ((((k >> 3) ^ (r & 7))) << 3) + (k & 7);
   };
@@ -636,9 +642,14 @@ extern "C" int molr_gating_tc_prepare(molr_gating* g) {
     img[base + 1] = lo;
   }
   for (int gg = 0; gg < 64; ++gg)
-    for (int j = 0; j < 128; ++j) img[8192 + 2048 + (j >> 6) * 4096 + sw(gg, j & 63)] = __float2bfloat16(w2[size_t(j) * 64 + gg]);
-  // layout in device memory: [W1T 8192][W1B 2048][W2T 8192] -> w1t_bf16 points at the start,
-  // w2t_bf16 at +10240
+    for (int j = 0; j < 128; ++j) {
+      const float v = w2[size_t(j) * 64 + gg];
+      const __nv_bfloat16 hi = __float2bfloat16(v);
+      img[8192 + 2048 + (j >> 6) * 4096 + sw(gg, j & 63)] = hi;
+      img[8192 + 2048 + 8192 + (j >> 6) * 4096 + sw(gg, j & 63)] = __float2bfloat16(v - __bfloat162float(hi));
+    }
+  // layout in device memory: [W1T 8192][W1B 2048][W2T 8192][W2L 8192] -> w1t_bf16 points at the
+  // start, w2t_bf16 at +10240
   MOLR_CUDA(cudaMalloc(&g->w1t_bf16, img.size() * 2));
   MOLR_CUDA(cudaMemcpy(g->w1t_bf16, img.data(), img.size() * 2, cudaMemcpyHostToDevice));
   g->w2t_bf16 = g->w1t_bf16 + 10240;
