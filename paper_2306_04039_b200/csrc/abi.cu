@@ -2,6 +2,7 @@
 #include <mutex>
 
 #include "common.cuh"
+#include "stage1.cuh"
 
 namespace molr {
 
@@ -63,6 +64,73 @@ __global__ void embs_to_bf16_kernel(const float* __restrict__ x, int64_t rows, i
   if (local_bad) atomicOr(bad, 1);
 }
 
+__global__ void iota_kernel(int32_t* p, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = int32_t(i);
+}
+
+// Sort the rows of each 256-row tile by scale (ascending; padding rows, scale 0, last) and
+// permute codes / scales / perm accordingly.  One CTA per tile.
+__global__ void __launch_bounds__(256) seal_sort_kernel(int8_t* __restrict__ codes, float* __restrict__ scales,
+                                                        int32_t* __restrict__ perm) {
+  __shared__ uint64_t key[256];
+  __shared__ int4 tcodes[256 * 4];
+  __shared__ float tsc[256];
+  __shared__ int32_t tperm[256];
+  const int t = threadIdx.x;
+  const int64_t r0 = int64_t(blockIdx.x) * 256;
+  const float sc = scales[r0 + t];
+  tsc[t] = sc;
+  tperm[t] = perm[r0 + t];
+  for (int c = 0; c < 4; ++c) tcodes[t * 4 + c] = *reinterpret_cast<const int4*>(codes + s1_chunk_offset(r0 + t, c, 64));
+  const uint32_t k = sc > 0.f ? __float_as_uint(sc) : 0xffffffffu;  // positive floats order as uints
+  key[t] = (uint64_t(k) << 32) | uint32_t(t);
+  __syncthreads();
+  for (int size = 2; size <= 256; size <<= 1)
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      if (t < 128) {
+        const int lo = 2 * t - (t & (stride - 1)), hi = lo + stride;
+        const bool up = (lo & size) == 0;
+        const uint64_t x = key[lo], y = key[hi];
+        if ((x > y) == up) {
+          key[lo] = y;
+          key[hi] = x;
+        }
+      }
+      __syncthreads();
+    }
+  const int src = int(key[t] & 0xffffffffu);
+  scales[r0 + t] = tsc[src];
+  perm[r0 + t] = tperm[src];
+  for (int c = 0; c < 4; ++c) *reinterpret_cast<int4*>(codes + s1_chunk_offset(r0 + t, c, 64)) = tcodes[src * 4 + c];
+}
+
+__global__ void inv_perm_kernel(const int32_t* __restrict__ perm, int64_t n_rows, int64_t X, int32_t* __restrict__ inv) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_rows; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t r = perm[i];
+    if (r < X) inv[r] = int32_t(i);
+  }
+}
+
+// Seal the int8 view of a cache: sort tiles by scale, rebuild inv and the chunk min/max.
+// Idempotent and thread-safe; called by every stage-1 entry point before reading the view.
+int s1_seal(molr_cache* c, cudaStream_t s) {
+  if (!c->s1_perm || c->s1_sealed.load(std::memory_order_acquire)) return MOLR_OK;
+  std::lock_guard<std::mutex> g(c->seal_mu);
+  if (c->s1_sealed.load()) return MOLR_OK;
+  const int64_t xr = s1_rows_alloc(c->X, c->d1);
+  if (xr > 0) {
+    seal_sort_kernel<<<(unsigned)(xr / 256), 256, 0, s>>>(c->s1_codes, c->s1_scales, c->s1_perm);
+    MOLR_LAUNCHED(c->ctx);
+    inv_perm_kernel<<<div_up(xr, 256), 256, 0, s>>>(c->s1_perm, xr, c->X, c->s1_inv);
+    MOLR_LAUNCHED(c->ctx);
+    MOLR_TRY(s1_update_chunk_mm(c, 0, xr, s));
+    MOLR_CUDA(cudaStreamSynchronize(s));
+  }
+  c->s1_sealed.store(1, std::memory_order_release);
+  return MOLR_OK;
+}
+
 // linear (m, 64) int8 rows -> interleaved cache layout starting at row r0
 __global__ void codes_to_ilv_kernel(const int8_t* __restrict__ src, int64_t m, int64_t r0, int8_t* __restrict__ dst) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m * 4; i += (int64_t)gridDim.x * blockDim.x) {
@@ -88,6 +156,7 @@ __global__ void chunk_mm_kernel(const float* __restrict__ scales, int64_t c0, in
 
 int s1_update_chunk_mm(molr_cache* c, int64_t row0, int64_t n, cudaStream_t s) {
   const int64_t c0 = row0 / 32, c1 = (row0 + n + 31) / 32;
+  if (c1 <= c0) return MOLR_OK;
   chunk_mm_kernel<<<div_up(c1 - c0, 256), 256, 0, s>>>(c->s1_scales, c0, c1, c->s1_chunk_mm);
   MOLR_LAUNCHED(c->ctx);
   return MOLR_OK;
@@ -178,8 +247,16 @@ int molr_cache_alloc(molr_ctx* ctx, int64_t X, int k_x, int d, int G, int d1, in
   const int64_t xr = s1_rows_alloc(X, d1);
   if (!st && (storage & MOLR_STORE_S1_INT8)) st = grab((void**)&c->s1_codes, size_t(xr) * d1);
   if (!st && (storage & MOLR_STORE_S1_INT8)) st = grab((void**)&c->s1_scales, size_t(xr) * 4);
-  if (!st && (storage & MOLR_STORE_S1_INT8) && s1_interleaved(d1))
+  if (!st && (storage & MOLR_STORE_S1_INT8) && s1_interleaved(d1)) {
     st = grab((void**)&c->s1_chunk_mm, size_t(xr / 32) * sizeof(float2));
+    if (!st) st = grab((void**)&c->s1_perm, size_t(xr) * 4);
+    if (!st) st = grab((void**)&c->s1_inv, size_t(xr) * 4);
+    if (!st && xr > 0) {
+      iota_kernel<<<div_up(xr, 256), 256>>>(c->s1_perm, xr);
+      iota_kernel<<<div_up(xr, 256), 256>>>(c->s1_inv, xr);
+      if (cudaGetLastError() != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) st = MOLR_ERR_CUDA;
+    }
+  }
   if (!st && (storage & MOLR_STORE_S1_INT8)) {  // zero the padding rows
     if (cudaMemset(c->s1_codes, 0, size_t(xr) * d1) != cudaSuccess || cudaMemset(c->s1_scales, 0, size_t(xr) * 4) != cudaSuccess)
       st = MOLR_ERR_CUDA;
@@ -197,6 +274,8 @@ int molr_cache_fill(molr_cache* c, int64_t row0, int64_t n, const float* embs, c
   if (!c) MOLR_FAIL(MOLR_ERR_INVALID, "null cache");
   if (row0 < 0 || n < 0 || row0 + n > c->X) MOLR_FAIL(MOLR_ERR_OUT_OF_RANGE, "fill rows out of range");
   if (n == 0) return MOLR_OK;
+  if (c->s1_sealed.load() && (codes || scales))
+    MOLR_FAIL(MOLR_ERR_INVALID, "stage-1 view is sealed (the cache is immutable once queried)");
   molr_ctx* ctx = c->ctx;
   MOLR_CUDA(cudaSetDevice(ctx->device));
   cudaStream_t s = pick_stream(ctx, stream);
@@ -318,6 +397,8 @@ int molr_cache_destroy(molr_cache* c) {
   cudaFree(c->s1_codes);
   cudaFree(c->s1_scales);
   cudaFree(c->s1_chunk_mm);
+  cudaFree(c->s1_perm);
+  cudaFree(c->s1_inv);
   delete c;
   return MOLR_OK;
 }

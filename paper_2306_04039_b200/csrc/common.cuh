@@ -137,6 +137,14 @@ struct molr_cache {
   int8_t* s1_codes = nullptr;          // (X, d1)
   float* s1_scales = nullptr;          // (X,) (padded like the codes)
   float2* s1_chunk_mm = nullptr;       // per 32-row chunk (min, max) of s1_scales (d1 = 64)
+  // d1 = 64 int8 view: within every 256-row tile the rows are stored sorted by scale (the cache
+  // is "sealed" on first stage-1 use), so each 32-row chunk has a narrow scale range and the
+  // tensor-core filter's integer pre-test is tight.  perm: stored position -> item id;
+  // inv: item id -> stored position.
+  int32_t* s1_perm = nullptr;
+  int32_t* s1_inv = nullptr;
+  std::atomic<int> s1_sealed{0};
+  std::mutex seal_mu;
   int64_t bytes = 0;
 };
 
@@ -156,7 +164,10 @@ struct molr_gating {
 
 namespace molr {
 
+// Every entry point resolves its stream first; clearing any stale non-sticky launch error here
+// keeps it from being attributed to this call's launches.
 inline cudaStream_t pick_stream(molr_ctx* ctx, void* s) {
+  cudaGetLastError();
   return s ? reinterpret_cast<cudaStream_t>(s) : ctx->stream;
 }
 

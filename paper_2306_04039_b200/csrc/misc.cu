@@ -75,11 +75,15 @@ __global__ void embs_to_f32_kernel(const __nv_bfloat16* __restrict__ a, int64_t 
 }
 
 // interleaved cache codes rows [r0, r0+n) -> linear (n, 64)
-__global__ void codes_from_ilv_kernel(const int8_t* __restrict__ src, int64_t r0, int64_t n, int8_t* __restrict__ dst) {
+__global__ void codes_from_ilv_kernel(const int8_t* __restrict__ src, const int32_t* __restrict__ inv,
+                                      const float* __restrict__ scales, int64_t r0, int64_t n, int8_t* __restrict__ dst,
+                                      float* __restrict__ dsc) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * 4; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = i >> 2;
     const int c = int(i & 3);
-    *reinterpret_cast<int4*>(dst + r * 64 + c * 16) = *reinterpret_cast<const int4*>(src + s1_chunk_offset(r0 + r, c, 64));
+    const int64_t pos = inv ? inv[r0 + r] : r0 + r;
+    if (dst) *reinterpret_cast<int4*>(dst + r * 64 + c * 16) = *reinterpret_cast<const int4*>(src + s1_chunk_offset(pos, c, 64));
+    if (dsc && c == 0) dsc[r] = scales[pos];
   }
 }
 
@@ -173,19 +177,20 @@ int molr_cache_read(const molr_cache* c, int64_t row0, int64_t n, float* embs, f
     }
   }
   if (s1 && c->s1_f32) MOLR_CUDA(cudaMemcpyAsync(s1, c->s1_f32 + row0 * c->d1, size_t(n) * c->d1 * 4, cudaMemcpyDefault, s));
-  Out ocodes;
-  if (codes && c->s1_codes) {
+  Out ocodes, oscales;
+  if ((codes || scales) && c->s1_codes) {
     if (s1_interleaved(c->d1)) {
-      MOLR_TRY(ocodes.stage(codes, size_t(n) * c->d1, s));
-      codes_from_ilv_kernel<<<grid_for(ctx, n * 4), 256, 0, s>>>(c->s1_codes, row0, n, ocodes.as<int8_t>());
+      MOLR_TRY(ocodes.stage(codes, codes ? size_t(n) * c->d1 : 0, s));
+      MOLR_TRY(oscales.stage(scales, scales ? size_t(n) * 4 : 0, s));
+      codes_from_ilv_kernel<<<grid_for(ctx, n * 4), 256, 0, s>>>(c->s1_codes, c->s1_inv, c->s1_scales, row0, n,
+                                                                 ocodes.as<int8_t>(), oscales.as<float>());
       MOLR_LAUNCHED(ctx);
     } else {
-      MOLR_CUDA(cudaMemcpyAsync(codes, c->s1_codes + row0 * c->d1, size_t(n) * c->d1, cudaMemcpyDefault, s));
+      if (codes) MOLR_CUDA(cudaMemcpyAsync(codes, c->s1_codes + row0 * c->d1, size_t(n) * c->d1, cudaMemcpyDefault, s));
+      if (scales) MOLR_CUDA(cudaMemcpyAsync(scales, c->s1_scales + row0, size_t(n) * 4, cudaMemcpyDefault, s));
     }
   }
-  if (scales && c->s1_scales)
-    MOLR_CUDA(cudaMemcpyAsync(scales, c->s1_scales + row0, size_t(n) * 4, cudaMemcpyDefault, s));
-  MOLR_TRY(finish_outputs(s, {&oe, &og, &ocodes}));
+  MOLR_TRY(finish_outputs(s, {&oe, &og, &ocodes, &oscales}));
   MOLR_CUDA(cudaStreamSynchronize(s));
   return MOLR_OK;
 }
@@ -213,7 +218,7 @@ int molr_estimate_threshold(molr_ctx* ctx, const molr_cache* c, int mode, int B,
   MOLR_TRY(ss.alloc(size_t(B) * lam * 4, s));
   MOLR_TRY(tk.alloc(size_t(B) * 4, s));
   for (int b = 0; b < B; ++b) {  // each query has its own sample rows
-    MOLR_TRY(scan_scores(ctx, mode, lam, c->d1, c->s1_f32, c->s1_codes, s1_interleaved(c->d1), c->s1_scales, si.as<int64_t>() + size_t(b) * lam,
+    MOLR_TRY(scan_scores(ctx, mode, lam, c->d1, c->s1_f32, c->s1_codes, s1_interleaved(c->d1), c->s1_inv, c->s1_scales, si.as<int64_t>() + size_t(b) * lam,
                          1, qi.as<float>() + size_t(b) * c->d1, qc.as<int8_t>() ? qc.as<int8_t>() + size_t(b) * c->d1 : nullptr,
                          ss.as<float>() + size_t(b) * lam, lam, s));
   }

@@ -78,7 +78,7 @@ __global__ void feistel_sample_kernel(int64_t X, int64_t lam, uint64_t seed, int
 template <int MODE>
 __global__ void __launch_bounds__(256)
 filter_scan_kernel(int64_t n, int dim, const float* __restrict__ vf, const int8_t* __restrict__ codes,
-                   const float* __restrict__ scales, int B, const float* __restrict__ qf,
+                   const int32_t* __restrict__ inv, const float* __restrict__ scales, int B, const float* __restrict__ qf,
                    const int8_t* __restrict__ qc, const uint32_t* __restrict__ tkey, int strict, int64_t cap,
                    int32_t* __restrict__ cand, int64_t* __restrict__ counts) {
   extern __shared__ __align__(16) unsigned char sq[];
@@ -100,15 +100,16 @@ filter_scan_kernel(int64_t n, int dim, const float* __restrict__ vf, const int8_
         key = f32_key(acc);
       } else {
         int32_t acc = 0;
+        const int64_t pos = inv ? inv[r] : r;
         const int4* qq = reinterpret_cast<const int4*>(qs + b * dim);
         for (int k = 0; k < dim / 16; ++k) {
-          int4 x = *reinterpret_cast<const int4*>(codes + s1_chunk_offset(r, k, dim)), y = qq[k];
+          int4 x = *reinterpret_cast<const int4*>(codes + s1_chunk_offset(pos, k, dim)), y = qq[k];
           acc = __dp4a(x.x, y.x, acc);
           acc = __dp4a(x.y, y.y, acc);
           acc = __dp4a(x.z, y.z, acc);
           acc = __dp4a(x.w, y.w, acc);
         }
-        key = MODE == MOLR_S1_INT8_RAW ? i32_key(acc) : f32_key(__fmul_rn((float)acc, scales[r]));
+        key = MODE == MOLR_S1_INT8_RAW ? i32_key(acc) : f32_key(__fmul_rn((float)acc, scales[pos]));
       }
       bool pass = strict ? key > tk[b] : key >= tk[b];
       if (pass) {
@@ -129,24 +130,27 @@ __global__ void cap_segs_kernel(int B, int64_t cap, const int64_t* __restrict__ 
 
 // gather sampled stage-1 rows (codes interleaved + scales) into a contiguous padded operand
 __global__ void gather_sample_kernel(const int8_t* __restrict__ codes, const float* __restrict__ scales,
-                                     const int64_t* __restrict__ idx, int64_t n, int8_t* __restrict__ dcodes,
-                                     float* __restrict__ dscales) {
+                                     const int32_t* __restrict__ inv, const int64_t* __restrict__ idx, int64_t n,
+                                     int8_t* __restrict__ dcodes, float* __restrict__ dscales) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * 4; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = i >> 2;
     const int c = int(i & 3);
-    const int64_t src = idx[r];
+    const int64_t src = inv ? inv[idx[r]] : idx[r];
     *reinterpret_cast<int4*>(dcodes + s1_chunk_offset(r, c, 64)) = *reinterpret_cast<const int4*>(codes + s1_chunk_offset(src, c, 64));
     if (c == 0) dscales[r] = scales[src];
   }
 }
 
 // gather interleaved stage-1 code rows (index_select)
-__global__ void gather_codes_kernel(const int8_t* __restrict__ src, const int64_t* __restrict__ idx, int64_t n,
-                                    int8_t* __restrict__ dst) {
+__global__ void gather_codes_kernel(const int8_t* __restrict__ src, const float* __restrict__ ssc,
+                                    const int32_t* __restrict__ inv, const int64_t* __restrict__ idx, int64_t n,
+                                    int8_t* __restrict__ dst, float* __restrict__ dsc) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * 4; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = i >> 2;
     const int c = int(i & 3);
-    *reinterpret_cast<int4*>(dst + s1_chunk_offset(r, c, 64)) = *reinterpret_cast<const int4*>(src + s1_chunk_offset(idx[r], c, 64));
+    const int64_t pos = inv ? inv[idx[r]] : idx[r];
+    *reinterpret_cast<int4*>(dst + s1_chunk_offset(r, c, 64)) = *reinterpret_cast<const int4*>(src + s1_chunk_offset(pos, c, 64));
+    if (c == 0) dsc[r] = ssc[pos];
   }
 }
 
@@ -266,6 +270,7 @@ int molr_index_select(molr_ctx* ctx, const molr_cache* c, int64_t n, const int64
   if (!ctx || !c || !out) MOLR_FAIL(MOLR_ERR_INVALID, "null argument");
   MOLR_CUDA(cudaSetDevice(ctx->device));
   cudaStream_t s = ctx->stream;
+  if (c->s1_codes) MOLR_TRY(s1_seal(const_cast<molr_cache*>(c), s));
   molr_cache* r = nullptr;
   MOLR_TRY(molr_cache_alloc(ctx, n, c->k_x, c->d, c->G, c->d1, c->storage, &r));
   if (n > 0) {
@@ -281,15 +286,15 @@ int molr_index_select(molr_ctx* ctx, const molr_cache* c, int64_t n, const int64
     g(c->s1_f32, r->s1_f32, int64_t(c->d1) * 4);
     if (st == MOLR_OK && c->s1_codes) {
       if (s1_interleaved(c->d1)) {
-        gather_codes_kernel<<<std::min(div_up(n * 4, 256), ctx->num_sms * 8), 256, 0, s>>>(c->s1_codes, ii.as<int64_t>(),
-                                                                                         n, r->s1_codes);
+        gather_codes_kernel<<<std::min(div_up(n * 4, 256), ctx->num_sms * 8), 256, 0, s>>>(
+            c->s1_codes, c->s1_scales, c->s1_inv, ii.as<int64_t>(), n, r->s1_codes, r->s1_scales);
         if (cudaGetLastError() != cudaSuccess) st = MOLR_ERR_CUDA;
         ctx->launches++;
       } else {
         g(c->s1_codes, r->s1_codes, int64_t(c->d1));
+        g(c->s1_scales, r->s1_scales, 4);
       }
     }
-    g(c->s1_scales, r->s1_scales, 4);
     if (st == MOLR_OK && r->s1_chunk_mm) st = s1_update_chunk_mm(r, 0, n, s);
     if (st == MOLR_OK && cudaStreamSynchronize(s) != cudaSuccess) st = MOLR_ERR_CUDA;
     if (st) {
@@ -378,14 +383,14 @@ int molr_two_stage_top_k(molr_ctx* ctx, const molr_cache* c, const molr_gating* 
       MOLR_CUDA(cudaMemsetAsync(scodes.p, 0, size_t(lp) * 64, s));
       MOLR_CUDA(cudaMemsetAsync(sscales.p, 0, size_t(lp) * 4, s));
       gather_sample_kernel<<<std::min(div_up(lam * 4, 256), ctx->num_sms * 8), 256, 0, s>>>(
-          c->s1_codes, c->s1_scales, samp.as<int64_t>(), lam, scodes.as<int8_t>(), sscales.as<float>());
+          c->s1_codes, c->s1_scales, c->s1_inv, samp.as<int64_t>(), lam, scodes.as<int8_t>(), sscales.as<float>());
       MOLR_LAUNCHED(ctx);
       KTimer t(ctx, "stage1_sample_scan_tc", s, double(B) * lam);
-      MOLR_TRY(s1_tc_scan(ctx, mode, scodes.as<int8_t>(), sscales.as<float>(), nullptr, lam, B, qc.as<int8_t>(), nullptr,
+      MOLR_TRY(s1_tc_scan(ctx, mode, scodes.as<int8_t>(), sscales.as<float>(), nullptr, nullptr, lam, B, qc.as<int8_t>(), nullptr,
                           0, 0, nullptr, nullptr, ss.p, lam, s));
     } else {
       KTimer t(ctx, "stage1_sample_scan", s, double(B) * lam);
-      MOLR_TRY(scan_scores(ctx, mode, lam, c->d1, c->s1_f32, c->s1_codes, s1_interleaved(c->d1), c->s1_scales,
+      MOLR_TRY(scan_scores(ctx, mode, lam, c->d1, c->s1_f32, c->s1_codes, s1_interleaved(c->d1), c->s1_inv, c->s1_scales,
                            samp.as<int64_t>(), B, q.as<float>(), qc.as<int8_t>(), ss.p, lam, s));
     }
     {
@@ -405,7 +410,7 @@ int molr_two_stage_top_k(molr_ctx* ctx, const molr_cache* c, const molr_gating* 
       auto launch = [&](auto kern) -> int {
         MOLR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int blocks = std::min(div_up(X, 256), ctx->num_sms * std::max(1, int((220 * 1024) / (smem + 1024))));
-        kern<<<blocks, 256, smem, s>>>(X, c->d1, c->s1_f32, c->s1_codes, c->s1_scales, B, q.as<float>(),
+        kern<<<blocks, 256, smem, s>>>(X, c->d1, c->s1_f32, c->s1_codes, c->s1_inv, c->s1_scales, B, q.as<float>(),
                                        qc.as<int8_t>(), tkey.as<uint32_t>(), comparator == MOLR_STRICT, cap,
                                        cand.as<int32_t>(), counts.as<int64_t>());
         MOLR_LAUNCHED(ctx);
@@ -413,7 +418,7 @@ int molr_two_stage_top_k(molr_ctx* ctx, const molr_cache* c, const molr_gating* 
       };
       if (use_tc) {
         KTimer t(ctx, "stage1_filter_tc", s, double(B) * X);
-        MOLR_TRY(s1_tc_scan(ctx, mode, c->s1_codes, c->s1_scales, c->s1_chunk_mm, X, B, qc.as<int8_t>(),
+        MOLR_TRY(s1_tc_scan(ctx, mode, c->s1_codes, c->s1_scales, c->s1_chunk_mm, c->s1_perm, X, B, qc.as<int8_t>(),
                             tkey.as<uint32_t>(), comparator == MOLR_STRICT, cap, cand.as<int32_t>(), counts.as<int64_t>(),
                             nullptr, 0, s));
       } else {

@@ -66,7 +66,8 @@ __device__ __forceinline__ int32_t dot_row_i8(const int8_t* __restrict__ codes, 
 
 // mode: MOLR_S1_FLOAT (f32 out), MOLR_S1_INT8 (f32 out = acc.f32 * scale), MOLR_S1_INT8_RAW (i32 out)
 __global__ void scan_scores_kernel(int mode, int64_t n, int dim, const float* __restrict__ vf,
-                                   const int8_t* __restrict__ codes, bool ilv, const float* __restrict__ scales,
+                                   const int8_t* __restrict__ codes, bool ilv, const int32_t* __restrict__ inv,
+                                   const float* __restrict__ scales,
                                    const int64_t* __restrict__ rows_idx, int B, const float* __restrict__ qf,
                                    const int8_t* __restrict__ qc, void* __restrict__ out, int64_t ld) {
   extern __shared__ __align__(16) unsigned char sq[];
@@ -86,9 +87,10 @@ __global__ void scan_scores_kernel(int mode, int64_t n, int dim, const float* __
         reinterpret_cast<float*>(out)[b * ld + i] = acc;
       }
     } else {
-      const float scale = mode == MOLR_S1_INT8 ? scales[r] : 0.f;
+      const int64_t pos = inv ? inv[r] : r;  // stored position of item r (sealed, scale-sorted tiles)
+      const float scale = mode == MOLR_S1_INT8 ? scales[pos] : 0.f;
       for (int b = 0; b < B; ++b) {
-        int32_t acc = dot_row_i8(codes, r, reinterpret_cast<const int8_t*>(sq) + b * dim, dim, ilv);
+        int32_t acc = dot_row_i8(codes, pos, reinterpret_cast<const int8_t*>(sq) + b * dim, dim, ilv);
         if (mode == MOLR_S1_INT8_RAW) reinterpret_cast<int32_t*>(out)[b * ld + i] = acc;
         else reinterpret_cast<float*>(out)[b * ld + i] = __fmul_rn((float)acc, scale);
       }
@@ -97,7 +99,7 @@ __global__ void scan_scores_kernel(int mode, int64_t n, int dim, const float* __
 }
 
 int scan_scores(molr_ctx* ctx, int mode, int64_t n, int dim, const float* vf, const int8_t* codes, bool ilv,
-                const float* scales, const int64_t* rows_idx, int B, const float* qf, const int8_t* qc, void* out,
+                const int32_t* inv, const float* scales, const int64_t* rows_idx, int B, const float* qf, const int8_t* qc, void* out,
                 int64_t ld, cudaStream_t s) {
   if (n <= 0 || B <= 0) return MOLR_OK;
   // shared memory holds up to 48 KB of queries per launch; chunk the batch otherwise
@@ -110,7 +112,7 @@ int scan_scores(molr_ctx* ctx, int mode, int64_t n, int dim, const float* vf, co
     size_t esz = mode == MOLR_S1_INT8_RAW ? 4 : 4;
     void* o = reinterpret_cast<char*>(out) + size_t(b0) * ld * esz;
     scan_scores_kernel<<<blocks, 256, size_t(bb) * per_q, s>>>(
-        mode, n, dim, vf, codes, ilv, scales, rows_idx, bb, qf ? qf + size_t(b0) * dim : nullptr,
+        mode, n, dim, vf, codes, ilv, inv, scales, rows_idx, bb, qf ? qf + size_t(b0) * dim : nullptr,
         qc ? qc + size_t(b0) * dim : nullptr, o, ld);
     MOLR_LAUNCHED(ctx);
   }
@@ -269,6 +271,7 @@ int prepare_queries(molr_ctx* ctx, int mode, int B, int dim, const float* q, int
 }
 
 int check_view(const molr_cache* c, int mode) {
+  if (mode != MOLR_S1_FLOAT && c->s1_codes) MOLR_TRY(s1_seal(const_cast<molr_cache*>(c), c->ctx->stream));
   if (mode == MOLR_S1_FLOAT && !c->s1_f32) MOLR_FAIL(MOLR_ERR_INVALID, "cache has no float stage-1 view");
   if (mode != MOLR_S1_FLOAT && !c->s1_codes)
     MOLR_FAIL(MOLR_ERR_INVALID, "cache was built without quantized stage-1 embeddings");
@@ -312,7 +315,7 @@ int molr_int8_matvec(molr_ctx* ctx, int64_t n, int dim, const int8_t* codes, con
   MOLR_TRY(qq.stage(q, size_t(dim), s));
   MOLR_TRY(o.stage(out, size_t(n) * 4, s));
   // raw mode over an ad-hoc view: scales unused
-  MOLR_TRY(scan_scores(ctx, MOLR_S1_INT8_RAW, n, dim, nullptr, c.as<int8_t>(), false, nullptr, nullptr, 1, nullptr,
+  MOLR_TRY(scan_scores(ctx, MOLR_S1_INT8_RAW, n, dim, nullptr, c.as<int8_t>(), false, nullptr, nullptr, nullptr, 1, nullptr,
                        qq.as<int8_t>(), o.dptr, n, s));
   return finish_outputs(s, {&o});
 }
@@ -334,7 +337,7 @@ int molr_stage1_scores(molr_ctx* ctx, const molr_cache* c, int mode, int B, cons
     MOLR_TRY(qs.alloc(size_t(B) * 4, s));
     MOLR_TRY(prepare_queries(ctx, mode, B, c->d1, qi.as<float>(), qc.as<int8_t>(), qs.as<float>(), s));
   }
-  MOLR_TRY(scan_scores(ctx, mode, c->X, c->d1, c->s1_f32, c->s1_codes, s1_interleaved(c->d1), c->s1_scales, nullptr, B, qi.as<float>(),
+  MOLR_TRY(scan_scores(ctx, mode, c->X, c->d1, c->s1_f32, c->s1_codes, s1_interleaved(c->d1), c->s1_inv, c->s1_scales, nullptr, B, qi.as<float>(),
                        qc.as<int8_t>(), o.dptr, c->X, s));
   return finish_outputs(s, {&o});
 }
@@ -364,7 +367,7 @@ int molr_h_indexer(molr_ctx* ctx, const molr_cache* c, int mode, int B, const fl
     MOLR_TRY(qs.alloc(size_t(B) * 4, s));
     MOLR_TRY(prepare_queries(ctx, mode, B, c->d1, qi.as<float>(), qc.as<int8_t>(), qs.as<float>(), s));
   }
-  MOLR_TRY(scan_scores(ctx, mode, c->X, c->d1, c->s1_f32, c->s1_codes, s1_interleaved(c->d1), c->s1_scales, nullptr, B, qi.as<float>(),
+  MOLR_TRY(scan_scores(ctx, mode, c->X, c->d1, c->s1_f32, c->s1_codes, s1_interleaved(c->d1), c->s1_inv, c->s1_scales, nullptr, B, qi.as<float>(),
                        qc.as<int8_t>(), scores.p, c->X, s));
   // 2. threshold = n-th largest of the SAME score array at the sampled rows (hindexer.py:156-158)
   Scratch tkey;

@@ -5,7 +5,7 @@
 namespace molr {
 
 int scan_scores(molr_ctx* ctx, int mode, int64_t n, int dim, const float* vf, const int8_t* codes, bool ilv,
-                const float* scales, const int64_t* rows_idx, int B, const float* qf, const int8_t* qc, void* out,
+                const int32_t* inv, const float* scales, const int64_t* rows_idx, int B, const float* qf, const int8_t* qc, void* out,
                 int64_t ld, cudaStream_t s);
 int compact_passers(molr_ctx* ctx, int B, int64_t n, const void* sc, int is_int, int64_t ld, const uint32_t* tkey,
                     int strict, int64_t cap, int64_t id_base, int64_t* out_ids, int64_t* totals, cudaStream_t s);
@@ -14,10 +14,12 @@ int gather_rows(molr_ctx* ctx, int64_t m, int64_t dim_bytes, const void* src, co
 int prepare_queries(molr_ctx* ctx, int mode, int B, int dim, const float* q, int8_t* qc, float* qs, cudaStream_t s);
 int check_view(const molr_cache* c, int mode);
 bool s1_tc_supported(const molr_cache* c, int mode);
-int s1_tc_scan(molr_ctx* ctx, int mode, const int8_t* codes, const float* scales, const float2* mm, int64_t n, int B,
+int s1_tc_scan(molr_ctx* ctx, int mode, const int8_t* codes, const float* scales, const float2* mm,
+               const int32_t* perm, int64_t n, int B,
                const int8_t* qcodes, const uint32_t* tkeys, int strict, int64_t cap, int32_t* cand, int64_t* counts,
                void* out, int64_t ld, cudaStream_t s);
 int s1_update_chunk_mm(molr_cache* c, int64_t row0, int64_t n, cudaStream_t s);
+int s1_seal(molr_cache* c, cudaStream_t s);
 int int_to_float_inplace(molr_ctx* ctx, int32_t* p, int64_t n, cudaStream_t s);
 
 }  // namespace molr

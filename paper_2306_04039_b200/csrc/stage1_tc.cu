@@ -28,11 +28,14 @@ constexpr int QB = 128;    // queries per block (MMA M)
 constexpr int MAXQB = 8;   // queries per launch <= 1024
 constexpr int NSTAGE = 4;
 constexpr int SZ_CODES = NT * 64;                 // 16 KB
-constexpr int SZ_STAGE = SZ_CODES + NT * 4 + 1024;  // codes + scales + chunk min/max, 1 KB aligned: 18 KB
+// stage: codes 16 KB | scales 1 KB | perm 1 KB | chunk min/max 64 B  (1 KB aligned: 19 KB)
+constexpr int ST_SC = SZ_CODES, ST_PERM = SZ_CODES + NT * 4, ST_MM = SZ_CODES + NT * 8;
+constexpr int SZ_STAGE = SZ_CODES + NT * 8 + 1024;
 constexpr int OFF_A = 0;                          // MAXQB x 8 KB query codes (interleave)
 constexpr int OFF_RING = OFF_A + MAXQB * 8192;
 constexpr int OFF_T = OFF_RING + NSTAGE * SZ_STAGE;  // per-query threshold (f32 or s32), 4 KB
-constexpr int OFF_BAR = OFF_T + MAXQB * QB * 4;
+constexpr int OFF_SCR = OFF_T + MAXQB * QB * 4;     // per epilogue thread: 32 accumulators (dynamic indexing)
+constexpr int OFF_BAR = OFF_SCR + 256 * 32 * 4;
 constexpr int NBAR = 2 * NSTAGE + 4;
 constexpr int OFF_TMEM = OFF_BAR + NBAR * 8;
 constexpr int SMEM_BYTES = OFF_TMEM + 16;
@@ -96,6 +99,7 @@ struct Params {
   const int8_t* codes;    // interleaved rows, padded to NT
   const float* scales;    // padded
   const float2* chunk_mm; // per 32 rows (min, max) scale
+  const int32_t* perm;    // stored row -> item id (filter modes)
   int64_t n;              // valid rows
   int B;                  // queries in this launch (<= 1024)
   const int8_t* qcodes;   // (B, 64) linear
@@ -167,10 +171,13 @@ __global__ void __launch_bounds__(64 + 256, 1) s1_tc_kernel(Params P) {
       for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         mbar_wait(empty_bar(stage), phase ^ 1);
         const uint32_t st = sbase + OFF_RING + stage * SZ_STAGE;
-        mbar_arrive_expect_tx(full_bar(stage), SZ_CODES + NT * 4 + (WRITE ? 0 : 64));
+        mbar_arrive_expect_tx(full_bar(stage), SZ_CODES + NT * 4 + (WRITE ? 0 : NT * 4 + 64));
         bulk_g2s(st, P.codes + tile * SZ_CODES, SZ_CODES, full_bar(stage));
-        bulk_g2s(st + SZ_CODES, P.scales + tile * NT, NT * 4, full_bar(stage));
-        if (!WRITE) bulk_g2s(st + SZ_CODES + NT * 4, P.chunk_mm + tile * (NT / 32), 64, full_bar(stage));
+        bulk_g2s(st + ST_SC, P.scales + tile * NT, NT * 4, full_bar(stage));
+        if (!WRITE) {
+          bulk_g2s(st + ST_PERM, P.perm + tile * NT, NT * 4, full_bar(stage));
+          bulk_g2s(st + ST_MM, P.chunk_mm + tile * (NT / 32), 64, full_bar(stage));
+        }
         if (++stage == NSTAGE) {
           stage = 0;
           phase ^= 1;
@@ -216,8 +223,10 @@ __global__ void __launch_bounds__(64 + 256, 1) s1_tc_kernel(Params P) {
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       mbar_wait(full_bar(stage), phase);  // scales / chunk min-max of this tile are in smem
       const uint8_t* st = sm + OFF_RING + stage * SZ_STAGE;
-      const float* sc = reinterpret_cast<const float*>(st + SZ_CODES);
-      const float2* mm = reinterpret_cast<const float2*>(st + SZ_CODES + NT * 4);
+      const float* sc = reinterpret_cast<const float*>(st + ST_SC);
+      const int32_t* pm = reinterpret_cast<const int32_t*>(st + ST_PERM);
+      const float2* mm = reinterpret_cast<const float2*>(st + ST_MM);
+      int32_t* scr = reinterpret_cast<int32_t*>(sm + OFF_SCR) + (threadIdx.x - 64) * 32;
       const int64_t row0 = tile * NT;
       const int nvalid = (int)imin64(NT, P.n - row0);
       for (int qb = e; qb < nqb; qb += 2) {
@@ -269,22 +278,29 @@ __global__ void __launch_bounds__(64 + 256, 1) s1_tc_kernel(Params P) {
                 L = l <= -1073741824.f ? -1073741824 : (l >= 1073741824.f ? 1073741824 : int32_t(floorf(l)) - 1);
               }
             }
+            // any accumulator of the chunk at or above the bound? (3-input max: 16 ops / 32 values)
+            int32_t mx = int32_t(a[0]);
+#pragma unroll
+            for (int j = 1; j < 31; j += 2) mx = __vimax3_s32(mx, int32_t(a[j]), int32_t(a[j + 1]));
+            mx = max(mx, int32_t(a[31]));
             uint32_t m = 0;
-#pragma unroll
-            for (int j = 0; j < 32; ++j) m |= uint32_t(int32_t(a[j]) >= L) << j;
             const int j0 = cc * 32;
-            if (nvalid - j0 < 32) m &= (nvalid - j0 <= 0) ? 0u : ((1u << (nvalid - j0)) - 1u);
-            if (!RAW) {
-              uint32_t mm2 = m;
-              while (mm2) {  // exact re-check of the few survivors: fl(acc * scale) vs t
-                const int j = __ffs(mm2) - 1;
-                mm2 &= mm2 - 1;
-                uint32_t aj = a[0];
+            if (mx >= L) {
 #pragma unroll
-                for (int k = 1; k < 32; ++k) aj = (k == j) ? a[k] : aj;
-                const float s = __fmul_rn((float)int32_t(aj), sc[j0 + j]);
-                const bool ok = P.strict ? (s > tf) : (s >= tf);
-                if (!ok) m &= ~(1u << j);
+              for (int j = 0; j < 32; j += 4)
+                *reinterpret_cast<int4*>(scr + j) = make_int4(int32_t(a[j]), int32_t(a[j + 1]), int32_t(a[j + 2]), int32_t(a[j + 3]));
+#pragma unroll
+              for (int j = 0; j < 32; ++j) m |= uint32_t(int32_t(a[j]) >= L) << j;
+              if (nvalid - j0 < 32) m &= (nvalid - j0 <= 0) ? 0u : ((1u << (nvalid - j0)) - 1u);
+              if (!RAW) {
+                uint32_t mm2 = m;
+                while (mm2) {  // exact re-check of the survivors: fl(acc * scale) vs t (hindexer.py:111)
+                  const int j = __ffs(mm2) - 1;
+                  mm2 &= mm2 - 1;
+                  const float s = __fmul_rn((float)scr[j], sc[j0 + j]);
+                  const bool ok = P.strict ? (s > tf) : (s >= tf);
+                  if (!ok) m &= ~(1u << j);
+                }
               }
             }
             mask[cc] = m;
@@ -298,7 +314,7 @@ __global__ void __launch_bounds__(64 + 256, 1) s1_tc_kernel(Params P) {
               while (m) {
                 const int j = __ffs(m) - 1;
                 m &= m - 1;
-                if ((int64_t)pos < P.cap) P.cand[int64_t(q) * P.cap + (int64_t)pos] = int32_t(row0 + cc * 32 + j);
+                if ((int64_t)pos < P.cap) P.cand[int64_t(q) * P.cap + (int64_t)pos] = pm[cc * 32 + j];
                 ++pos;
               }
             }
@@ -329,7 +345,8 @@ bool s1_tc_supported(const molr_cache* c, int mode) {
 
 // Scan rows [0, n) of an interleaved code matrix against B queries (chunks of 1024 per launch).
 // filter: tkeys != nullptr -> append passers to cand / counts; else write scores to out (B, ld).
-int s1_tc_scan(molr_ctx* ctx, int mode, const int8_t* codes, const float* scales, const float2* mm, int64_t n, int B,
+int s1_tc_scan(molr_ctx* ctx, int mode, const int8_t* codes, const float* scales, const float2* mm,
+               const int32_t* perm, int64_t n, int B,
                const int8_t* qcodes, const uint32_t* tkeys, int strict, int64_t cap, int32_t* cand, int64_t* counts,
                void* out, int64_t ld, cudaStream_t s) {
   using namespace s1tc;
@@ -343,6 +360,7 @@ int s1_tc_scan(molr_ctx* ctx, int mode, const int8_t* codes, const float* scales
     P.codes = codes;
     P.scales = scales;
     P.chunk_mm = mm;
+    P.perm = perm;
     P.n = n;
     P.B = std::min(B - b0, MAXQB * QB);
     P.qcodes = qcodes + int64_t(b0) * 64;
