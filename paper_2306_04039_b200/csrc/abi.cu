@@ -150,7 +150,9 @@ __global__ void chunk_mm_kernel(const float* __restrict__ scales, int64_t c0, in
         hi = fmaxf(hi, v);
       }
     }
-    mm[c] = make_float2(lo, hi);
+    // stored as reciprocals (1/min, 1/max) for the filter's integer bound; (0, -1) marks a chunk
+    // of padding rows only
+    mm[c] = hi > 0.f ? make_float2(float(1.0 / double(lo)), float(1.0 / double(hi))) : make_float2(0.f, -1.f);
   }
 }
 

@@ -136,7 +136,7 @@ struct molr_cache {
   float* s1_f32 = nullptr;             // (X, d1)
   int8_t* s1_codes = nullptr;          // (X, d1)
   float* s1_scales = nullptr;          // (X,) (padded like the codes)
-  float2* s1_chunk_mm = nullptr;       // per 32-row chunk (min, max) of s1_scales (d1 = 64)
+  float2* s1_chunk_mm = nullptr;       // per 32-row chunk (1/min, 1/max) of s1_scales (d1 = 64)
   // d1 = 64 int8 view: within every 256-row tile the rows are stored sorted by scale (the cache
   // is "sealed" on first stage-1 use), so each 32-row chunk has a narrow scale range and the
   // tensor-core filter's integer pre-test is tight.  perm: stored position -> item id;

@@ -174,14 +174,18 @@ __device__ __forceinline__ float rcp(float x) {
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-// SiLU with one MUFU (tanh.approx, ~5e-4 relative): kept for experiments; the production path
-// uses silu_acc because the hidden units are carried at ~2^-17 (hi/lo split) into layer 2
-__device__ __forceinline__ float silu_fast(float x) {
-  float h = 0.5f * x;
-  return fmaf(h, fast_tanh(h), h);
-}
-// SiLU as x * rcp(1 + 2^(-x log2 e)) with ex2 + rcp (~1e-7 relative)
+// SiLU, one MUFU: x * sigmoid(x) = h + h * tanh(h), h = x / 2.  tanh.approx has ~2^-11 relative
+// error, so for |x| >= 2 (where 1 + tanh(h) cancels) the exact-ish two-MUFU form is used instead.
+// (Measured slower than silu_acc in round 1 — the kernel is issue/latency bound, not MUFU
+// bound — so the production epilogues use silu_acc.)
 __device__ __forceinline__ float silu_acc(float x) { return x * rcp(1.0f + ex2(-1.4426950408889634f * x)); }
+__device__ __forceinline__ float silu_fast(float x) {
+  if (fabsf(x) < 2.0f) {
+    const float h = 0.5f * x;
+    return fmaf(h, fast_tanh(h), h);
+  }
+  return silu_acc(x);
+}
 
 // SW128 K-major byte offset of 16-byte chunk `c` of row `r` within a [rows x 128 B] region.
 __device__ __forceinline__ uint32_t sw128(int r, int c) { return (r >> 3) * 1024 + (r & 7) * 128 + ((c ^ (r & 7)) << 4); }

@@ -34,8 +34,9 @@ constexpr int SZ_STAGE = SZ_CODES + NT * 8 + 1024;
 constexpr int OFF_A = 0;                          // MAXQB x 8 KB query codes (interleave)
 constexpr int OFF_RING = OFF_A + MAXQB * 8192;
 constexpr int OFF_T = OFF_RING + NSTAGE * SZ_STAGE;  // per-query threshold (f32 or s32), 4 KB
-constexpr int OFF_SCR = OFF_T + MAXQB * QB * 4;     // per epilogue thread: 32 accumulators (dynamic indexing)
-constexpr int OFF_BAR = OFF_SCR + 256 * 32 * 4;
+constexpr int NEPI = 4;    // epilogue warpgroups: (TMEM buffer e = wg & 1) x (column half = wg >> 1)
+constexpr int NTHREADS = 64 + NEPI * 128;
+constexpr int OFF_BAR = OFF_T + MAXQB * QB * 4;
 constexpr int NBAR = 2 * NSTAGE + 4;
 constexpr int OFF_TMEM = OFF_BAR + NBAR * 8;
 constexpr int SMEM_BYTES = OFF_TMEM + 16;
@@ -113,7 +114,7 @@ struct Params {
 };
 
 template <int MODE>
-__global__ void __launch_bounds__(64 + 256, 1) s1_tc_kernel(Params P) {
+__global__ void __launch_bounds__(NTHREADS, 1) s1_tc_kernel(Params P) {
   constexpr bool WRITE = MODE >= WRITE_SCALED;
   constexpr bool RAW = (MODE == FILTER_RAW || MODE == WRITE_RAW);
   extern __shared__ __align__(1024) uint8_t sm[];
@@ -145,11 +146,11 @@ __global__ void __launch_bounds__(64 + 256, 1) s1_tc_kernel(Params P) {
   if (threadIdx.x == 0) {
     for (int s = 0; s < NSTAGE; ++s) {
       mbar_init(full_bar(s), 1);
-      mbar_init(empty_bar(s), 1 + 256);
+      mbar_init(empty_bar(s), 1 + NEPI * 128);
     }
     for (int e = 0; e < 2; ++e) {
       mbar_init(tfull(e), 1);
-      mbar_init(tempty(e), 128);
+      mbar_init(tempty(e), 256);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -214,21 +215,23 @@ __global__ void __launch_bounds__(64 + 256, 1) s1_tc_kernel(Params P) {
     __syncwarp();
   } else {
     // ================= epilogue warpgroups =================
-    const int e = (warp - 2) >> 2;
+    // WG w reads TMEM buffer e = w & 1 (query blocks qb = e, e+2, ...) and column half w >> 1.
+    const int wg = (warp - 2) >> 2;
+    const int e = wg & 1, half = wg >> 1;
     const int quarter = warp & 3;
     const int p = quarter * 32 + lane;
-    const uint32_t tm = tmem_base + e * 256 + ((uint32_t)(quarter * 32) << 16);
+    const uint32_t lanebit = 1u << lane;
+    const uint32_t tm = tmem_base + e * 256 + half * 128 + ((uint32_t)(quarter * 32) << 16);
     int stage = 0;
     uint32_t phase = 0, tph = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      mbar_wait(full_bar(stage), phase);  // scales / chunk min-max of this tile are in smem
+      mbar_wait(full_bar(stage), phase);  // scales / perm / chunk bounds of this tile are in smem
       const uint8_t* st = sm + OFF_RING + stage * SZ_STAGE;
-      const float* sc = reinterpret_cast<const float*>(st + ST_SC);
-      const int32_t* pm = reinterpret_cast<const int32_t*>(st + ST_PERM);
-      const float2* mm = reinterpret_cast<const float2*>(st + ST_MM);
-      int32_t* scr = reinterpret_cast<int32_t*>(sm + OFF_SCR) + (threadIdx.x - 64) * 32;
-      const int64_t row0 = tile * NT;
-      const int nvalid = (int)imin64(NT, P.n - row0);
+      const float* sc = reinterpret_cast<const float*>(st + ST_SC) + half * 128;
+      const int32_t* pm = reinterpret_cast<const int32_t*>(st + ST_PERM) + half * 128;
+      const float2* mm = reinterpret_cast<const float2*>(st + ST_MM) + half * 4;
+      const int64_t row0 = tile * NT + half * 128;
+      const int nvalid = (int)imax64(0, imin64(128, P.n - row0));
       for (int qb = e; qb < nqb; qb += 2) {
         const int q = qb * QB + p;
         mbar_wait(tfull(e), tph);
@@ -236,22 +239,36 @@ __global__ void __launch_bounds__(64 + 256, 1) s1_tc_kernel(Params P) {
         tc_fence_after();
         if (WRITE) {
 #pragma unroll 1
-          for (int cc = 0; cc < NT / 32; ++cc) {
+          for (int cc = 0; cc < 4; ++cc) {
             uint32_t a[32];
             TMEM_LD32(tm + cc * 32, a);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            if (q < P.B) {
-              const int j0 = cc * 32;
+            const int j0 = cc * 32;
+            if (q < P.B && j0 < nvalid) {
               if (RAW) {
                 int32_t* o = reinterpret_cast<int32_t*>(P.out) + int64_t(q) * P.ld + row0 + j0;
+                if (nvalid - j0 >= 32 && ((reinterpret_cast<uintptr_t>(o) & 15) == 0)) {
 #pragma unroll
-                for (int j = 0; j < 32; ++j)
-                  if (j0 + j < nvalid) o[j] = int32_t(a[j]);
+                  for (int j = 0; j < 32; j += 4)
+                    *reinterpret_cast<int4*>(o + j) = make_int4(int32_t(a[j]), int32_t(a[j + 1]), int32_t(a[j + 2]), int32_t(a[j + 3]));
+                } else {
+#pragma unroll
+                  for (int j = 0; j < 32; ++j)
+                    if (j0 + j < nvalid) o[j] = int32_t(a[j]);
+                }
               } else {
                 float* o = reinterpret_cast<float*>(P.out) + int64_t(q) * P.ld + row0 + j0;
+                float v[32];
 #pragma unroll
-                for (int j = 0; j < 32; ++j)
-                  if (j0 + j < nvalid) o[j] = __fmul_rn((float)int32_t(a[j]), sc[j0 + j]);
+                for (int j = 0; j < 32; ++j) v[j] = __fmul_rn((float)int32_t(a[j]), sc[j0 + j]);
+                if (nvalid - j0 >= 32 && ((reinterpret_cast<uintptr_t>(o) & 15) == 0)) {
+#pragma unroll
+                  for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4*>(o + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                } else {
+#pragma unroll
+                  for (int j = 0; j < 32; ++j)
+                    if (j0 + j < nvalid) o[j] = v[j];
+                }
               }
             }
           }
@@ -259,47 +276,54 @@ __global__ void __launch_bounds__(64 + 256, 1) s1_tc_kernel(Params P) {
           const uint32_t traw = reinterpret_cast<const uint32_t*>(sm + OFF_T)[q];
           const float tf = __uint_as_float(traw);
           const int32_t ti = int32_t(traw);
-          uint32_t mask[NT / 32];
+          uint32_t mask[4];
           int total = 0;
 #pragma unroll
-          for (int cc = 0; cc < NT / 32; ++cc) {
+          for (int cc = 0; cc < 4; ++cc) {
             uint32_t a[32];
             TMEM_LD32(tm + cc * 32, a);
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            // integer bound L: acc >= L is necessary to pass anywhere in this 32-row chunk
+            // (computed while the TMEM load is in flight)
             int32_t L;
             if (RAW) {
               L = P.strict ? ti + 1 : ti;  // exact
             } else {
-              const float2 m2 = mm[cc];
-              if (!(m2.y > 0.f)) {
-                L = 0x7fffffff;  // chunk of padding rows only
+              const float2 inv = mm[cc];  // (1/min scale, 1/max scale) of the chunk
+              if (inv.y < 0.f) {
+                L = 0x7fffffff;  // padding rows only
               } else {
-                const float l = fminf(tf * (1.0f - 1e-6f) / m2.y, tf * (1.0f + 1e-6f) / m2.x);
-                L = l <= -1073741824.f ? -1073741824 : (l >= 1073741824.f ? 1073741824 : int32_t(floorf(l)) - 1);
+                const float l = fminf(tf * inv.y * (1.0f - 4e-6f), tf * inv.x * (1.0f + 4e-6f));
+                L = l <= -1073741824.f ? -1073741824 : (l >= 1073741824.f ? 1073741824 : __float2int_rd(l) - 1);
               }
             }
-            // any accumulator of the chunk at or above the bound? (3-input max: 16 ops / 32 values)
-            int32_t mx = int32_t(a[0]);
-#pragma unroll
-            for (int j = 1; j < 31; j += 2) mx = __vimax3_s32(mx, int32_t(a[j]), int32_t(a[j + 1]));
-            mx = max(mx, int32_t(a[31]));
-            uint32_t m = 0;
             const int j0 = cc * 32;
-            if (mx >= L) {
+            const int lim = nvalid - j0;  // valid columns in this chunk
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            // per 8-column group: max as a shallow tree of 3-input maxes (ILP, not a serial chain)
+            int32_t gm[4];
 #pragma unroll
-              for (int j = 0; j < 32; j += 4)
-                *reinterpret_cast<int4*>(scr + j) = make_int4(int32_t(a[j]), int32_t(a[j + 1]), int32_t(a[j + 2]), int32_t(a[j + 3]));
+            for (int g8 = 0; g8 < 4; ++g8) {
+              const int32_t* v = reinterpret_cast<const int32_t*>(a) + g8 * 8;
+              gm[g8] = max(__vimax3_s32(v[0], v[1], v[2]), __vimax3_s32(v[3], v[4], max(v[5], max(v[6], v[7]))));
+            }
+            uint32_t m = 0;
 #pragma unroll
-              for (int j = 0; j < 32; ++j) m |= uint32_t(int32_t(a[j]) >= L) << j;
-              if (nvalid - j0 < 32) m &= (nvalid - j0 <= 0) ? 0u : ((1u << (nvalid - j0)) - 1u);
-              if (!RAW) {
-                uint32_t mm2 = m;
-                while (mm2) {  // exact re-check of the survivors: fl(acc * scale) vs t (hindexer.py:111)
-                  const int j = __ffs(mm2) - 1;
-                  mm2 &= mm2 - 1;
-                  const float s = __fmul_rn((float)scr[j], sc[j0 + j]);
-                  const bool ok = P.strict ? (s > tf) : (s >= tf);
-                  if (!ok) m &= ~(1u << j);
+            for (int g8 = 0; g8 < 4; ++g8) {
+              // a group is examined by the warp only if some lane may have a passer in it
+              if (__any_sync(0xffffffffu, gm[g8] >= L && g8 * 8 < lim)) {
+                if (gm[g8] >= L) {
+#pragma unroll
+                  for (int jj = 0; jj < 8; ++jj) {
+                    const int j = g8 * 8 + jj;
+                    bool ok;
+                    if (RAW) {
+                      ok = int32_t(a[j]) >= L;
+                    } else {  // exact fp32 test: fl(acc * scale) vs t  (hindexer.py:111)
+                      const float s = __fmul_rn((float)int32_t(a[j]), sc[j0 + j]);
+                      ok = P.strict ? (s > tf) : (s >= tf);
+                    }
+                    m |= uint32_t(ok && j < lim) << j;
+                  }
                 }
               }
             }
@@ -309,7 +333,7 @@ __global__ void __launch_bounds__(64 + 256, 1) s1_tc_kernel(Params P) {
           if (total && q < P.B) {
             unsigned long long pos = atomicAdd(P.counts + q, (unsigned long long)total);
 #pragma unroll
-            for (int cc = 0; cc < NT / 32; ++cc) {
+            for (int cc = 0; cc < 4; ++cc) {
               uint32_t m = mask[cc];
               while (m) {
                 const int j = __ffs(m) - 1;
@@ -329,7 +353,6 @@ __global__ void __launch_bounds__(64 + 256, 1) s1_tc_kernel(Params P) {
         phase ^= 1;
       }
     }
-    // the other warpgroup's arrivals on empty barriers: WG 1 also walks all tiles (above)
   }
   tc_fence_before();
   __syncthreads();
@@ -373,7 +396,7 @@ int s1_tc_scan(molr_ctx* ctx, int mode, const int8_t* codes, const float* scales
     P.ld = ld;
     auto launch = [&](auto kern) -> int {
       MOLR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
-      kern<<<grid, 64 + 256, SMEM_BYTES, s>>>(P);
+      kern<<<grid, NTHREADS, SMEM_BYTES, s>>>(P);
       MOLR_LAUNCHED(ctx);
       return MOLR_OK;
     };
