@@ -156,6 +156,13 @@ __global__ void chunk_mm_kernel(const float* __restrict__ scales, int64_t c0, in
   }
 }
 
+int chunk_minmax(molr_ctx* ctx, const float* scales, int64_t c0, int64_t c1, float2* mm, cudaStream_t s) {
+  if (c1 <= c0) return MOLR_OK;
+  chunk_mm_kernel<<<div_up(c1 - c0, 256), 256, 0, s>>>(scales, c0, c1, mm);
+  MOLR_LAUNCHED(ctx);
+  return MOLR_OK;
+}
+
 int s1_update_chunk_mm(molr_cache* c, int64_t row0, int64_t n, cudaStream_t s) {
   const int64_t c0 = row0 / 32, c1 = (row0 + n + 31) / 32;
   if (c1 <= c0) return MOLR_OK;

@@ -39,6 +39,11 @@ int nth_largest_rows(molr_ctx* ctx, int B, int64_t n_values, const void* values,
                      int64_t ld, const int64_t* gather, int64_t gather_ld, int64_t n,
                      uint32_t* out_keys, cudaStream_t s);
 
+// n-th largest of rows of pre-computed ascending keys (row b: keys[b*cap, b*cap + counts[b])).
+// Rows holding fewer than n keys set *short_rows (left untouched otherwise) and get no key.
+int nth_largest_keys(molr_ctx* ctx, int B, int64_t cap, const uint32_t* keys, const int64_t* counts, int64_t n,
+                     uint32_t* out_keys, int* short_rows, cudaStream_t s);
+
 int quantize_rows(molr_ctx* ctx, int64_t rows, int dim, const float* x, int8_t* codes, float* scales,
                   cudaStream_t s);
 

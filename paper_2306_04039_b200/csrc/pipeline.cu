@@ -120,6 +120,12 @@ filter_scan_kernel(int64_t n, int dim, const float* __restrict__ vf, const int8_
   }
 }
 
+// flag |= 1 if any query's passer count overflowed its capacity
+__global__ void max_count_kernel(int B, const int64_t* __restrict__ counts, int64_t cap, int* __restrict__ flag) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (__syncthreads_or(b < B && counts[b] > cap) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
 __global__ void cap_segs_kernel(int B, int64_t cap, const int64_t* __restrict__ counts, int64_t* __restrict__ beg,
                                 int64_t* __restrict__ end) {
   for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < B; b += gridDim.x * blockDim.x) {
@@ -152,6 +158,70 @@ __global__ void gather_codes_kernel(const int8_t* __restrict__ src, const float*
     *reinterpret_cast<int4*>(dst + s1_chunk_offset(r, c, 64)) = *reinterpret_cast<const int4*>(src + s1_chunk_offset(pos, c, 64));
     if (c == 0) dsc[r] = ssc[pos];
   }
+}
+
+// Threshold of the lam-row sample (the n_rank-th largest sampled score per query,
+// hindexer.py:115-132) without materialising the B x lam score matrix:
+//   1. pilot: score the first lam0 sample rows (a uniform subsample: the Feistel prefix is a
+//      uniform random order) and take their n0-th largest t0, with n0 set ~6 sigma above the
+//      expected count of rows above the true threshold, so t0 <= t with overwhelming probability
+//   2. scan the whole sample with the fused filter (>= t0), appending only the passers' score keys
+//   3. the n_rank-th largest passer key IS the n_rank-th largest sampled score whenever at least
+//      n_rank rows passed (every row >= t passes); otherwise (or on capacity overflow) fall back to
+//      scoring the full sample.  Exact in every case.
+int sample_threshold_tc(molr_ctx* ctx, int mode, const int8_t* scodes, const float* sscales, int64_t lam, int B,
+                        const int8_t* qc, int64_t n_rank, Scratch& ss, uint32_t* tkey, cudaStream_t s) {
+  const bool raw = mode == MOLR_S1_INT8_RAW;
+  const double p = double(n_rank) / double(lam);
+  int64_t lam0 = (int64_t)std::ceil(48.0 / p);
+  lam0 = (lam0 + 255) / 256 * 256;
+  if (!getenv("MOLR_NO_PILOT") && lam0 * 4 <= lam) {
+    const double mu = double(lam0) * p;
+    int64_t n0 = std::min<int64_t>(lam0, (int64_t)std::ceil(mu + 6.0 * std::sqrt(mu) + 16.0));
+    if (const char* e = getenv("MOLR_PILOT_N0")) n0 = std::max<int64_t>(1, std::min<int64_t>(lam0, atoll(e)));  // tests
+    const double expect = double(lam) * double(n0) / double(lam0);
+    const int64_t cap = (int64_t)(2.0 * expect) + 2048;
+    Scratch pilot, t0, keys, counts, flag;
+    MOLR_TRY(pilot.alloc(size_t(B) * lam0 * 4, s));
+    MOLR_TRY(t0.alloc(size_t(B) * 4, s));
+    MOLR_TRY(keys.alloc(size_t(B) * cap * 4, s));
+    MOLR_TRY(counts.alloc(size_t(B) * 8, s));
+    MOLR_TRY(flag.alloc(sizeof(int) * 2, s));
+    Scratch mm;
+    const int64_t lp = (lam + 255) / 256 * 256;
+    MOLR_TRY(mm.alloc(size_t(lp / 32) * sizeof(float2), s));
+    {
+      KTimer t(ctx, "stage1_sample_scan_tc", s, double(B) * lam);
+      MOLR_TRY(s1_tc_scan(ctx, mode, scodes, sscales, nullptr, nullptr, lam0, B, qc, nullptr, 0, 0, nullptr, nullptr,
+                          pilot.p, lam0, s));
+      MOLR_TRY(nth_largest_rows(ctx, B, lam0, pilot.p, raw, lam0, nullptr, 0, n0, t0.as<uint32_t>(), s));
+      MOLR_TRY(chunk_minmax(ctx, sscales, 0, lp / 32, mm.as<float2>(), s));
+      MOLR_CUDA(cudaMemsetAsync(counts.p, 0, size_t(B) * 8, s));
+      MOLR_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int) * 2, s));
+      MOLR_TRY(s1_tc_scan(ctx, mode, scodes, sscales, mm.as<float2>(), nullptr, lam, B, qc, t0.as<uint32_t>(), 0, cap,
+                          keys.as<int32_t>(), counts.as<int64_t>(), nullptr, 0, s, /*emit_keys=*/true));
+    }
+    {
+      KTimer t(ctx, "select_nth", s, double(B) * expect);
+      MOLR_TRY(nth_largest_keys(ctx, B, cap, keys.as<uint32_t>(), counts.as<int64_t>(), n_rank, tkey,
+                                flag.as<int>(), s));
+      max_count_kernel<<<div_up(B, 256), 256, 0, s>>>(B, counts.as<int64_t>(), cap, flag.as<int>());
+      MOLR_LAUNCHED(ctx);
+    }
+    int hf = 0;
+    MOLR_CUDA(cudaMemcpyAsync(&hf, flag.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    MOLR_CUDA(cudaStreamSynchronize(s));
+    if (!hf) return MOLR_OK;
+  }
+  // full sample: write every score, then select
+  MOLR_TRY(ss.alloc(size_t(B) * lam * 4, s));
+  {
+    KTimer t(ctx, "stage1_sample_scan_tc", s, double(B) * lam);
+    MOLR_TRY(s1_tc_scan(ctx, mode, scodes, sscales, nullptr, nullptr, lam, B, qc, nullptr, 0, 0, nullptr, nullptr,
+                        ss.p, lam, s));
+  }
+  KTimer t(ctx, "select_nth", s, double(B) * lam);
+  return nth_largest_rows(ctx, B, lam, ss.p, raw, lam, nullptr, 0, n_rank, tkey, s);
 }
 
 }  // namespace molr
@@ -371,7 +441,6 @@ int molr_two_stage_top_k(molr_ctx* ctx, const molr_cache* c, const molr_gating* 
     const double nr = std::nearbyint(double(k_prime * lam) / double(X));  // Python round(): half-even
     const int64_t n_rank = std::max<int64_t>(1, (int64_t)nr);
     Scratch ss, tkey;
-    MOLR_TRY(ss.alloc(size_t(B) * lam * 4, s));
     MOLR_TRY(tkey.alloc(size_t(B) * 4, s));
     const bool use_tc = s1_tc_supported(c, mode);
     if (use_tc) {
@@ -385,15 +454,15 @@ int molr_two_stage_top_k(molr_ctx* ctx, const molr_cache* c, const molr_gating* 
       gather_sample_kernel<<<std::min(div_up(lam * 4, 256), ctx->num_sms * 8), 256, 0, s>>>(
           c->s1_codes, c->s1_scales, c->s1_inv, samp.as<int64_t>(), lam, scodes.as<int8_t>(), sscales.as<float>());
       MOLR_LAUNCHED(ctx);
-      KTimer t(ctx, "stage1_sample_scan_tc", s, double(B) * lam);
-      MOLR_TRY(s1_tc_scan(ctx, mode, scodes.as<int8_t>(), sscales.as<float>(), nullptr, nullptr, lam, B, qc.as<int8_t>(), nullptr,
-                          0, 0, nullptr, nullptr, ss.p, lam, s));
+      MOLR_TRY(sample_threshold_tc(ctx, mode, scodes.as<int8_t>(), sscales.as<float>(), lam, B, qc.as<int8_t>(),
+                                   n_rank, ss, tkey.as<uint32_t>(), s));
     } else {
+      MOLR_TRY(ss.alloc(size_t(B) * lam * 4, s));
       KTimer t(ctx, "stage1_sample_scan", s, double(B) * lam);
       MOLR_TRY(scan_scores(ctx, mode, lam, c->d1, c->s1_f32, c->s1_codes, s1_interleaved(c->d1), c->s1_inv, c->s1_scales,
                            samp.as<int64_t>(), B, q.as<float>(), qc.as<int8_t>(), ss.p, lam, s));
     }
-    {
+    if (!use_tc) {
       KTimer t(ctx, "select_nth", s, double(B) * lam);
       MOLR_TRY(nth_largest_rows(ctx, B, lam, ss.p, mode == MOLR_S1_INT8_RAW, lam, nullptr, 0, n_rank,
                                 tkey.as<uint32_t>(), s));

@@ -207,12 +207,21 @@ __device__ __forceinline__ double key_f64(uint64_t k) {
 
 // nth_largest over B rows: value keys (f32 / i32 / f64 / i64), optional gather through sample
 // indices.  Writes the ascending-order key of the n-th largest value.
+// DT: 0 f32, 1 i32, 2 f64, 3 i64, 4 pre-computed ascending uint32 keys (f32_key / i32_key).
+// row_n (optional): row b holds only min(row_n[b], n) values; a row with fewer than rank_n values
+// sets *short_rows and writes no key.
 template <class K, int DT>
 __global__ void __launch_bounds__(kSelThreads)
 nth_largest_kernel(int64_t n, const void* __restrict__ values, int64_t ld, const int64_t* __restrict__ gather,
-                   int64_t gather_ld, int64_t rank_n, K* __restrict__ out_keys) {
+                   int64_t gather_ld, int64_t rank_n, K* __restrict__ out_keys, const int64_t* __restrict__ row_n,
+                   int* __restrict__ short_rows) {
   __shared__ uint32_t hist[256];
   const int b = blockIdx.x;
+  const int64_t nb = row_n ? imin64(row_n[b], n) : n;
+  if (nb < rank_n) {
+    if (threadIdx.x == 0 && short_rows) atomicOr(short_rows, 1);
+    return;
+  }
   const int64_t* gi = gather ? gather + int64_t(b) * gather_ld : nullptr;
   auto key_of = [&](int64_t i, K* k) -> bool {
     int64_t j = int64_t(b) * ld + (gi ? gi[i] : i);
@@ -220,21 +229,30 @@ nth_largest_kernel(int64_t n, const void* __restrict__ values, int64_t ld, const
     if (DT == 0) v = (K)f32_key(reinterpret_cast<const float*>(values)[j]);
     else if (DT == 1) v = (K)i32_key(reinterpret_cast<const int32_t*>(values)[j]);
     else if (DT == 2) v = (K)f64_key(reinterpret_cast<const double*>(values)[j]);
+    else if (DT == 4) v = (K)reinterpret_cast<const uint32_t*>(values)[j];
     else v = (K)(uint64_t(reinterpret_cast<const int64_t*>(values)[j]) ^ 0x8000000000000000ull);
     *k = ~v;
     return true;
   };
   K kstar;
   int64_t less;
-  block_radix_select<K>(key_of, n, rank_n, hist, &kstar, &less);
+  block_radix_select<K>(key_of, nb, rank_n, hist, &kstar, &less);
   if (threadIdx.x == 0) out_keys[b] = ~kstar;
 }
 
 int nth_largest_rows(molr_ctx* ctx, int B, int64_t n_values, const void* values, int is_int, int64_t ld,
                      const int64_t* gather, int64_t gather_ld, int64_t n, uint32_t* out_keys, cudaStream_t s) {
   if (B <= 0) return MOLR_OK;
-  if (is_int) nth_largest_kernel<uint32_t, 1><<<B, kSelThreads, 0, s>>>(n_values, values, ld, gather, gather_ld, n, out_keys);
-  else nth_largest_kernel<uint32_t, 0><<<B, kSelThreads, 0, s>>>(n_values, values, ld, gather, gather_ld, n, out_keys);
+  if (is_int) nth_largest_kernel<uint32_t, 1><<<B, kSelThreads, 0, s>>>(n_values, values, ld, gather, gather_ld, n, out_keys, nullptr, nullptr);
+  else nth_largest_kernel<uint32_t, 0><<<B, kSelThreads, 0, s>>>(n_values, values, ld, gather, gather_ld, n, out_keys, nullptr, nullptr);
+  MOLR_LAUNCHED(ctx);
+  return MOLR_OK;
+}
+
+int nth_largest_keys(molr_ctx* ctx, int B, int64_t cap, const uint32_t* keys, const int64_t* counts, int64_t n,
+                     uint32_t* out_keys, int* short_rows, cudaStream_t s) {
+  if (B <= 0) return MOLR_OK;
+  nth_largest_kernel<uint32_t, 4><<<B, kSelThreads, 0, s>>>(cap, keys, cap, nullptr, 0, n, out_keys, counts, short_rows);
   MOLR_LAUNCHED(ctx);
   return MOLR_OK;
 }
@@ -288,10 +306,10 @@ int molr_nth_largest(molr_ctx* ctx, int B, int64_t n_values, const void* values,
   uint64_t* k64 = keys.as<uint64_t>();
   uint32_t* k32 = keys.as<uint32_t>();
   switch (dtype) {
-    case 0: nth_largest_kernel<uint32_t, 0><<<B, kSelThreads, 0, s>>>(n_values, v.dptr, n_values, nullptr, 0, n, k32); break;
-    case 1: nth_largest_kernel<uint32_t, 1><<<B, kSelThreads, 0, s>>>(n_values, v.dptr, n_values, nullptr, 0, n, k32); break;
-    case 2: nth_largest_kernel<uint64_t, 2><<<B, kSelThreads, 0, s>>>(n_values, v.dptr, n_values, nullptr, 0, n, k64); break;
-    default: nth_largest_kernel<uint64_t, 3><<<B, kSelThreads, 0, s>>>(n_values, v.dptr, n_values, nullptr, 0, n, k64); break;
+    case 0: nth_largest_kernel<uint32_t, 0><<<B, kSelThreads, 0, s>>>(n_values, v.dptr, n_values, nullptr, 0, n, k32, nullptr, nullptr); break;
+    case 1: nth_largest_kernel<uint32_t, 1><<<B, kSelThreads, 0, s>>>(n_values, v.dptr, n_values, nullptr, 0, n, k32, nullptr, nullptr); break;
+    case 2: nth_largest_kernel<uint64_t, 2><<<B, kSelThreads, 0, s>>>(n_values, v.dptr, n_values, nullptr, 0, n, k64, nullptr, nullptr); break;
+    default: nth_largest_kernel<uint64_t, 3><<<B, kSelThreads, 0, s>>>(n_values, v.dptr, n_values, nullptr, 0, n, k64, nullptr, nullptr); break;
   }
   MOLR_LAUNCHED(ctx);
   std::vector<uint64_t> hk(B);

@@ -41,7 +41,10 @@ constexpr int NBAR = 2 * NSTAGE + 4;
 constexpr int OFF_TMEM = OFF_BAR + NBAR * 8;
 constexpr int SMEM_BYTES = OFF_TMEM + 16;
 
-enum Mode { FILTER_SCALED = 0, FILTER_RAW = 1, WRITE_SCALED = 2, WRITE_RAW = 3 };
+// FILTER_*: append passers' item ids (perm) per query; WRITE_*: write every score;
+// KEYS_*: filter, but append the passers' ascending score keys (f32_key / i32_key) instead of ids
+// (the threshold-estimation sample: only the order statistics of the passers are needed)
+enum Mode { FILTER_SCALED = 0, FILTER_RAW = 1, WRITE_SCALED = 2, WRITE_RAW = 3, KEYS_SCALED = 4, KEYS_RAW = 5 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
@@ -96,6 +99,18 @@ __device__ __forceinline__ void mma_commit(uint32_t bar) {
         "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])                    \
       : "r"(taddr))
 
+// wait for outstanding tcgen05.ld; the registers are in/out operands so no use of them can be
+// scheduled above the wait
+#define TMEM_WAIT32(r)                                                                                              \
+  asm volatile("tcgen05.wait::ld.sync.aligned;"                                                                     \
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),    \
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15]), \
+                 "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]), "+r"(r[22]),            \
+                 "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]), "+r"(r[29]),            \
+                 "+r"(r[30]), "+r"(r[31])                                                                           \
+               :                                                                                                    \
+               : "memory")
+
 struct Params {
   const int8_t* codes;    // interleaved rows, padded to NT
   const float* scales;    // padded
@@ -115,8 +130,9 @@ struct Params {
 
 template <int MODE>
 __global__ void __launch_bounds__(NTHREADS, 1) s1_tc_kernel(Params P) {
-  constexpr bool WRITE = MODE >= WRITE_SCALED;
-  constexpr bool RAW = (MODE == FILTER_RAW || MODE == WRITE_RAW);
+  constexpr bool WRITE = MODE == WRITE_SCALED || MODE == WRITE_RAW;
+  constexpr bool KEYS = MODE == KEYS_SCALED || MODE == KEYS_RAW;
+  constexpr bool RAW = (MODE == FILTER_RAW || MODE == WRITE_RAW || MODE == KEYS_RAW);
   extern __shared__ __align__(1024) uint8_t sm[];
   const uint32_t sbase = smem_u32(sm);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -172,13 +188,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) s1_tc_kernel(Params P) {
       for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         mbar_wait(empty_bar(stage), phase ^ 1);
         const uint32_t st = sbase + OFF_RING + stage * SZ_STAGE;
-        mbar_arrive_expect_tx(full_bar(stage), SZ_CODES + NT * 4 + (WRITE ? 0 : NT * 4 + 64));
+        mbar_arrive_expect_tx(full_bar(stage), SZ_CODES + NT * 4 + (WRITE ? 0 : 64) + ((WRITE || KEYS) ? 0 : NT * 4));
         bulk_g2s(st, P.codes + tile * SZ_CODES, SZ_CODES, full_bar(stage));
         bulk_g2s(st + ST_SC, P.scales + tile * NT, NT * 4, full_bar(stage));
-        if (!WRITE) {
-          bulk_g2s(st + ST_PERM, P.perm + tile * NT, NT * 4, full_bar(stage));
-          bulk_g2s(st + ST_MM, P.chunk_mm + tile * (NT / 32), 64, full_bar(stage));
-        }
+        if (!WRITE) bulk_g2s(st + ST_MM, P.chunk_mm + tile * (NT / 32), 64, full_bar(stage));
+        if (!WRITE && !KEYS) bulk_g2s(st + ST_PERM, P.perm + tile * NT, NT * 4, full_bar(stage));
         if (++stage == NSTAGE) {
           stage = 0;
           phase ^= 1;
@@ -273,20 +287,27 @@ __global__ void __launch_bounds__(NTHREADS, 1) s1_tc_kernel(Params P) {
             }
           }
         } else {
+          // per thread: one query (TMEM lane), 128 item columns as 4 chunks of 32 rows
           const uint32_t traw = reinterpret_cast<const uint32_t*>(sm + OFF_T)[q];
           const float tf = __uint_as_float(traw);
-          const int32_t ti = int32_t(traw);
+          // strict (s > t) as s >= the next float above t (thresholds are finite scores);
+          // raw: acc >= t (+1 when strict)
+          const float tfe = P.strict ? __uint_as_float(tf >= 0.f ? (tf == 0.f ? 1u : traw + 1u) : traw - 1u) : tf;
+          const int32_t ti = int32_t(traw) + (P.strict ? 1 : 0);
+          const float4* sc4 = reinterpret_cast<const float4*>(sc);
           uint32_t mask[4];
           int total = 0;
+          uint32_t ra[32], rb[32];
+          TMEM_LD32(tm, ra);
 #pragma unroll
           for (int cc = 0; cc < 4; ++cc) {
-            uint32_t a[32];
-            TMEM_LD32(tm + cc * 32, a);
+            uint32_t* a = (cc & 1) ? rb : ra;
+            uint32_t* nx = (cc & 1) ? ra : rb;
             // integer bound L: acc >= L is necessary to pass anywhere in this 32-row chunk
             // (computed while the TMEM load is in flight)
             int32_t L;
             if (RAW) {
-              L = P.strict ? ti + 1 : ti;  // exact
+              L = ti;  // exact
             } else {
               const float2 inv = mm[cc];  // (1/min scale, 1/max scale) of the chunk
               if (inv.y < 0.f) {
@@ -296,10 +317,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) s1_tc_kernel(Params P) {
                 L = l <= -1073741824.f ? -1073741824 : (l >= 1073741824.f ? 1073741824 : __float2int_rd(l) - 1);
               }
             }
+            TMEM_WAIT32(a);
+            if (cc < 3) TMEM_LD32(tm + (cc + 1) * 32, nx);  // next chunk loads under this chunk's test
             const int j0 = cc * 32;
-            const int lim = nvalid - j0;  // valid columns in this chunk
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            // per 8-column group: max as a shallow tree of 3-input maxes (ILP, not a serial chain)
+            // per 8-column group: max as a shallow tree of 3-input maxes
             int32_t gm[4];
 #pragma unroll
             for (int g8 = 0; g8 < 4; ++g8) {
@@ -310,27 +331,43 @@ __global__ void __launch_bounds__(NTHREADS, 1) s1_tc_kernel(Params P) {
 #pragma unroll
             for (int g8 = 0; g8 < 4; ++g8) {
               // a group is examined by the warp only if some lane may have a passer in it
-              if (__any_sync(0xffffffffu, gm[g8] >= L && g8 * 8 < lim)) {
+              if (__any_sync(0xffffffffu, gm[g8] >= L)) {
                 if (gm[g8] >= L) {
+                  const int32_t* v = reinterpret_cast<const int32_t*>(a) + g8 * 8;
+                  uint32_t bits = 0;
+                  if (RAW) {
 #pragma unroll
-                  for (int jj = 0; jj < 8; ++jj) {
-                    const int j = g8 * 8 + jj;
-                    bool ok;
-                    if (RAW) {
-                      ok = int32_t(a[j]) >= L;
-                    } else {  // exact fp32 test: fl(acc * scale) vs t  (hindexer.py:111)
-                      const float s = __fmul_rn((float)int32_t(a[j]), sc[j0 + j]);
-                      ok = P.strict ? (s > tf) : (s >= tf);
-                    }
-                    m |= uint32_t(ok && j < lim) << j;
+                    for (int jj = 0; jj < 8; ++jj) bits |= uint32_t(v[jj] >= L) << jj;
+                  } else {  // exact fp32 test: fl(acc * scale) >= t  (hindexer.py:111)
+                    const float4 s0 = sc4[(j0 + g8 * 8) >> 2], s1 = sc4[((j0 + g8 * 8) >> 2) + 1];
+                    const float sv[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+#pragma unroll
+                    for (int jj = 0; jj < 8; ++jj) bits |= uint32_t(__fmul_rn((float)v[jj], sv[jj]) >= tfe) << jj;
                   }
+                  m |= bits << (g8 * 8);
                 }
               }
             }
+            const int lim = nvalid - j0;  // valid columns in this chunk
+            if (lim < 32) m &= lim <= 0 ? 0u : ((1u << lim) - 1u);
             mask[cc] = m;
             total += __popc(m);
+            if (KEYS && m && q < P.B) {  // append the passers' ascending score keys now (a[] is live)
+              unsigned long long pos = atomicAdd(P.counts + q, (unsigned long long)__popc(m));
+              while (m) {
+                const int j = __ffs(m) - 1;
+                m &= m - 1;
+                uint32_t accv = 0;
+#pragma unroll
+                for (int jj = 0; jj < 32; ++jj) accv = (jj == j) ? a[jj] : accv;  // static register select
+                const int32_t acc = int32_t(accv);
+                const uint32_t key = RAW ? i32_key(acc) : f32_key(__fmul_rn((float)acc, sc[j0 + j]));
+                if ((int64_t)pos < P.cap) P.cand[int64_t(q) * P.cap + (int64_t)pos] = int32_t(key);
+                ++pos;
+              }
+            }
           }
-          if (total && q < P.B) {
+          if (!KEYS && total && q < P.B) {
             unsigned long long pos = atomicAdd(P.counts + q, (unsigned long long)total);
 #pragma unroll
             for (int cc = 0; cc < 4; ++cc) {
@@ -371,11 +408,12 @@ bool s1_tc_supported(const molr_cache* c, int mode) {
 int s1_tc_scan(molr_ctx* ctx, int mode, const int8_t* codes, const float* scales, const float2* mm,
                const int32_t* perm, int64_t n, int B,
                const int8_t* qcodes, const uint32_t* tkeys, int strict, int64_t cap, int32_t* cand, int64_t* counts,
-               void* out, int64_t ld, cudaStream_t s) {
+               void* out, int64_t ld, cudaStream_t s, bool emit_keys) {
   using namespace s1tc;
   if (n <= 0 || B <= 0) return MOLR_OK;
   const bool raw = mode == MOLR_S1_INT8_RAW;
-  const int m = tkeys ? (raw ? FILTER_RAW : FILTER_SCALED) : (raw ? WRITE_RAW : WRITE_SCALED);
+  const int m = tkeys ? (emit_keys ? (raw ? KEYS_RAW : KEYS_SCALED) : (raw ? FILTER_RAW : FILTER_SCALED))
+                      : (raw ? WRITE_RAW : WRITE_SCALED);
   const int64_t ntiles = (n + NT - 1) / NT;
   const int grid = (int)std::min<int64_t>(ntiles, ctx->num_sms);
   for (int b0 = 0; b0 < B; b0 += MAXQB * QB) {
@@ -404,7 +442,9 @@ int s1_tc_scan(molr_ctx* ctx, int mode, const int8_t* codes, const float* scales
       case FILTER_SCALED: MOLR_TRY(launch(s1_tc_kernel<FILTER_SCALED>)); break;
       case FILTER_RAW: MOLR_TRY(launch(s1_tc_kernel<FILTER_RAW>)); break;
       case WRITE_SCALED: MOLR_TRY(launch(s1_tc_kernel<WRITE_SCALED>)); break;
-      default: MOLR_TRY(launch(s1_tc_kernel<WRITE_RAW>)); break;
+      case WRITE_RAW: MOLR_TRY(launch(s1_tc_kernel<WRITE_RAW>)); break;
+      case KEYS_SCALED: MOLR_TRY(launch(s1_tc_kernel<KEYS_SCALED>)); break;
+      default: MOLR_TRY(launch(s1_tc_kernel<KEYS_RAW>)); break;
     }
   }
   return MOLR_OK;

@@ -563,3 +563,31 @@ def test_batched_two_stage_recall_device_sample():
         rec.append(len(set(ex.tolist()) & set(ids[u].tolist())) / 100)
     print("recall", np.mean(rec))
     assert np.mean(rec) >= 0.99
+
+
+@pytest.mark.parametrize("strict,raw", [(False, False), (True, False), (False, True)])
+def test_sample_threshold_pilot_exact(strict, raw, monkeypatch):
+    """The pilot-filtered sample threshold (score a subsample, keep only sample rows above a low
+    pilot threshold, select among them) must give the SAME threshold as scoring the whole sample:
+    identical candidate counts and top-k for pilot / no pilot / forced fallback (pilot threshold
+    too high -> full sample)."""
+    from paper_2306_04039_b200.engine import two_stage_top_k
+    from paper_2306_04039_b200.hindexer import HIndexerConfig
+
+    cache, syn, ue, feats = _synthetic_prod_cache(300_000, seed=17, n_users=200)
+    gating, og = _prod_gating(syn)
+    hcfg = HIndexerConfig(k_prime=3000, sample_ratio=0.2, quantized=True,
+                          comparator="strict" if strict else "inclusive", raw_int_ordering=raw)
+    uw = gating.user_net(feats)
+    runs = {}
+    for tag, env in (("pilot", {}), ("full", {"MOLR_NO_PILOT": "1"}), ("fallback", {"MOLR_PILOT_N0": "1"})):
+        for k2 in ("MOLR_NO_PILOT", "MOLR_PILOT_N0"):
+            monkeypatch.delenv(k2, raising=False)
+        for k2, v in env.items():
+            monkeypatch.setenv(k2, v)
+        runs[tag] = two_stage_top_k(cache, gating, ue, uw, 50, hcfg, seed=11)
+    for tag in ("full", "fallback"):
+        np.testing.assert_array_equal(runs["pilot"][2], runs[tag][2])
+        np.testing.assert_array_equal(runs["pilot"][0], runs[tag][0])
+        np.testing.assert_array_equal(runs["pilot"][1], runs[tag][1])
+    assert np.all(np.abs(runs["pilot"][2] - 3000) < 3000 * 0.3)
