@@ -21,7 +21,6 @@ import argparse
 import json
 import math
 import os
-import subprocess
 import sys
 import threading
 import time
@@ -137,66 +136,64 @@ def make_queries(model, B, seed, dev):
 # clocks sampled during the timed region
 # ------------------------------------------------------------------------------------------
 class Clocks:
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    """Samples SM clock + throttle reasons through NVML (in-process, every 100 ms) while active."""
 
     def __init__(self, dev_index):
         self.dev = dev_index
-        self.p = None
-        self.lines = []
-        self.first = threading.Event()
+        self.samples = []
+        self.stop = threading.Event()
+        self.ok = False
 
-    def _reader(self):
-        for line in self.p.stdout:
-            self.lines.append(line)
-            self.first.set()
-        self.first.set()
+    def _run(self):
+        import pynvml as N
+
+        while not self.stop.is_set():
+            try:
+                sm = N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM)
+                r = N.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.samples.append((sm, r))
+            except Exception:
+                pass
+            self.stop.wait(0.1)
 
     def __enter__(self):
+        if os.environ.get("MOLR_NO_CLOCKS") == "1":
+            self.err = "disabled (MOLR_NO_CLOCKS)"
+            return self
         try:
-            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
-                                       "--format=csv,noheader,nounits", "-lms", "200"],
-                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._reader, daemon=True)
+            import pynvml as N
+
+            N.nvmlInit()
+            self.h = None
+            try:  # NVML and CUDA may order devices differently: match by UUID
+                import torch
+
+                self.h = N.nvmlDeviceGetHandleByUUID("GPU-" + str(torch.cuda.get_device_properties(self.dev).uuid))
+            except Exception:
+                self.h = N.nvmlDeviceGetHandleByIndex(self.dev)
+            self.max_sm = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
+            self.bits = {"hw_slowdown": N.nvmlClocksEventReasonHwSlowdown,
+                         "hw_thermal_slowdown": N.nvmlClocksEventReasonHwThermalSlowdown,
+                         "sw_thermal_slowdown": N.nvmlClocksEventReasonSwThermalSlowdown,
+                         "sw_power_cap": N.nvmlClocksEventReasonSwPowerCap}
+            self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
-            # nvidia-smi's start-up (driver attach) stalls the GPU for a while: wait for its first
-            # sample, then let it settle before any timed work
-            self.first.wait(15.0)
-            time.sleep(1.0)
-        except Exception:
-            self.p = None
+            self.ok = True
+        except Exception as e:
+            self.err = repr(e)
         return self
 
     def __exit__(self, *a):
-        if self.p:
-            self.p.terminate()
-            try:
-                self.p.wait(timeout=5)
-                self.t.join(timeout=5)
-            except Exception:
-                pass
-        self.out = "".join(self.lines)
+        self.stop.set()
+        if self.ok:
+            self.t.join(timeout=2)
 
     def summary(self):
-        if not self.p:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in (self.out or "").strip().splitlines():
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) < 7:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx.append(float(parts[1]))
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[3:7]):
-                if v.lower() == "active":
-                    reasons.add(nm)
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "samples": len(sm), "reasons": sorted(reasons)}
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable: " + getattr(self, "err", "")]}
+        reasons = sorted({k for _, r in self.samples for k, b in self.bits.items() if r & b})
+        return {"sm_mhz": float(np.median([s for s, _ in self.samples])), "sm_max_mhz": float(self.max_sm),
+                "samples": len(self.samples), "reasons": reasons, "source": "nvml"}
 
 
 # ------------------------------------------------------------------------------------------
@@ -397,9 +394,21 @@ def main():
             torch.cuda.profiler.start()
         barrier()
         evs[0].record(stream)
+        trace = os.environ.get("MOLR_STEP_TRACE") == "1"  # diagnostics: per-step kernel times (syncs)
+        last = {}
+        host_ms = []
         for i in range(args.steps):
+            t_host = time.perf_counter()
             step(args.warmup + i, ue_d.data_ptr(), feats_d.data_ptr())
             evs[i + 1].record(stream)
+            host_ms.append(round(1e3 * (time.perf_counter() - t_host), 2))
+            if trace:
+                torch.cuda.synchronize()
+                cur = L.prof_read(local)
+                d = {n: round(v[1] - last.get(n, (0, 0.0))[1], 2) for n, v in cur.items()}
+                last = cur
+                print(f"step {i}: host {1e3 * (time.perf_counter() - t_host):.1f} ms, gpu {evs[i].elapsed_time(evs[i + 1]):.1f} ms,"
+                      f" {d}", file=sys.stderr, flush=True)
         barrier()
         if prof_range:
             torch.cuda.profiler.stop()
@@ -526,7 +535,7 @@ def main():
                    "k_prime": cfg["k_prime"], "k_prime_per_gpu": kp_local, "sample_ratio": cfg["ratio"],
                    "lambda_per_gpu": lam_local, "stage1": "int8 (bit-exact)", "parallelism": f"item-shard x{world}",
                    "l2": "inputs larger than L2 (corpus shard >= 12.5M items x 1.2 KB)"},
-        "p50_batch_latency_ms": float(np.median(step_ms)), "step_ms": [round(x, 3) for x in step_ms], "p50_single_query_latency_ms": float(np.median(lat)),
+        "p50_batch_latency_ms": float(np.median(step_ms)), "step_ms": [round(x, 3) for x in step_ms], "step_host_ms": host_ms, "p50_single_query_latency_ms": float(np.median(lat)),
         "recall_at_k_vs_exact_mol": recall, "recall_queries": R,
         "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "step_ms": [round(x, 3) for x in e2e_step_ms]},

@@ -5,6 +5,7 @@
 #include "stage1.cuh"
 
 namespace molr {
+thread_local molr_arena* tl_arena = nullptr;
 
 static thread_local std::string g_last_error;
 void set_error(const std::string& msg) { g_last_error = msg; }
@@ -207,6 +208,11 @@ int molr_ctx_create(int device, molr_ctx** out) {
 int molr_ctx_destroy(molr_ctx* ctx) {
   if (!ctx) return MOLR_OK;
   cudaSetDevice(ctx->device);
+  cudaDeviceSynchronize();
+  for (molr_arena* a : ctx->ws_all) {
+    if (a->base) cudaFree(a->base);
+    delete a;
+  }
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
   return MOLR_OK;

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <atomic>
 #include <mutex>
 #include <utility>
@@ -76,6 +77,14 @@ struct molr_prof_sum {
   double ms = 0, work = 0;
 };
 
+// Grow-only device workspace for one synchronous entry-point call (see WorkspaceScope).
+struct molr_arena {
+  char* base = nullptr;
+  size_t cap = 0;
+  size_t off = 0;
+  size_t need = 0;  // high-water mark of this call (including what did not fit)
+};
+
 struct molr_ctx {
   int device = 0;
   int num_sms = 148;
@@ -87,6 +96,10 @@ struct molr_ctx {
   std::vector<molr_prof_rec> prof_pending;
   std::vector<cudaEvent_t> prof_free;
   std::vector<std::pair<std::string, molr_prof_sum>> prof_sums;
+  // workspace arenas: one per concurrently running synchronous call
+  std::mutex ws_mu;
+  std::vector<molr_arena*> ws_free;
+  std::vector<molr_arena*> ws_all;
 };
 
 namespace molr {
@@ -174,19 +187,34 @@ inline cudaStream_t pick_stream(molr_ctx* ctx, void* s) {
 // True if the kernel can dereference p directly (device or managed memory).
 bool is_device_ptr(const void* p);
 
-// Stream-ordered scratch that frees itself.
+// The calling thread's active workspace arena (set by WorkspaceScope), or null.
+extern thread_local molr_arena* tl_arena;
+
+// Stream-ordered scratch that frees itself.  Inside a WorkspaceScope it is bump-allocated from
+// the call's arena (no allocator traffic on the hot path); otherwise cudaMallocAsync.
 struct Scratch {
   void* p = nullptr;
   cudaStream_t s = nullptr;
+  bool arena = false;
   Scratch() = default;
   Scratch(const Scratch&) = delete;
   Scratch& operator=(const Scratch&) = delete;
-  ~Scratch() {
-    if (p) cudaFreeAsync(p, s);
-  }
+  ~Scratch() { reset(); }
   int alloc(size_t bytes, cudaStream_t stream) {
+    reset();
     s = stream;
     if (bytes == 0) bytes = 16;
+    const size_t rb = (bytes + 255) & ~size_t(255);
+    if (molr_arena* a = tl_arena) {
+      a->need = std::max(a->need, a->off + rb);
+      if (a->off + rb <= a->cap) {
+        p = a->base + a->off;
+        a->off += rb;
+        arena = true;
+        return MOLR_OK;
+      }
+      a->off += rb;  // account for it so the arena grows to the high-water mark
+    }
     cudaError_t e = cudaMallocAsync(&p, bytes, stream);
     if (e != cudaSuccess) {
       p = nullptr;
@@ -196,11 +224,54 @@ struct Scratch {
     return MOLR_OK;
   }
   void reset() {
-    if (p) cudaFreeAsync(p, s);
+    if (p && !arena) cudaFreeAsync(p, s);
     p = nullptr;
+    arena = false;
   }
   template <class T>
   T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+// RAII: gives the calling thread an arena of `ctx` for the duration of a call that synchronises
+// its stream before returning (the arena is recycled at scope exit).  An arena that overflowed is
+// regrown at exit to the call's high-water mark, so steady-state calls do no allocation at all.
+struct WorkspaceScope {
+  molr_ctx* ctx;
+  cudaStream_t s;
+  molr_arena* a = nullptr;
+  molr_arena* prev;
+  WorkspaceScope(molr_ctx* c, cudaStream_t st) : ctx(c), s(st), prev(tl_arena) {
+    {
+      std::lock_guard<std::mutex> g(ctx->ws_mu);
+      if (!ctx->ws_free.empty()) {
+        a = ctx->ws_free.back();
+        ctx->ws_free.pop_back();
+      } else {
+        a = new molr_arena();
+        ctx->ws_all.push_back(a);
+      }
+    }
+    a->off = 0;
+    a->need = 0;
+    tl_arena = a;
+  }
+  ~WorkspaceScope() {
+    tl_arena = prev;
+    cudaStreamSynchronize(s);  // no-op on the normal path; covers early error returns
+    if (a->need > a->cap) {  // every user of the old block has completed (the call synchronised)
+      if (a->base) cudaFree(a->base);
+      const size_t cap = a->need + a->need / 8;
+      if (cudaMalloc(&a->base, cap) == cudaSuccess) {
+        a->cap = cap;
+      } else {
+        a->base = nullptr;
+        a->cap = 0;
+        cudaGetLastError();
+      }
+    }
+    std::lock_guard<std::mutex> g(ctx->ws_mu);
+    ctx->ws_free.push_back(a);
+  }
 };
 
 // Input view: device pointer to `bytes` of data from a host-or-device pointer.

@@ -401,6 +401,7 @@ int molr_two_stage_top_k(molr_ctx* ctx, const molr_cache* c, const molr_gating* 
   MOLR_CUDA(cudaSetDevice(ctx->device));
   cudaStream_t s = pick_stream(ctx, stream);
   if (B <= 0) return MOLR_OK;
+  WorkspaceScope ws(ctx, s);  // this call synchronises its stream before returning
   const int64_t X = c->X;
   const int kk = (int)imin64(k, X);
   In iue, iuw;

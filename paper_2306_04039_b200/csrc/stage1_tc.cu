@@ -8,13 +8,14 @@
 // Layout: queries (B <= 1024, padded to blocks of 128) stay resident in shared memory for the
 // whole launch (64 KB); item tiles of 256 rows (16 KB of codes in the cache's interleaved
 // layout + 1 KB of scales + per-32-row scale min/max) stream through a 4-stage ring by bulk copy.
-// Per tile, MMA (M=128 queries, N=256 items, K=64 as 2 x K=32) per query block into one of two
-// 256-column TMEM accumulators; two epilogue warpgroups alternate blocks.
+// Per (tile, query block) the single MMA thread issues four M=128 x N=64 x K=64 MMAs, one per
+// 64-item quarter of the tile, into eight 64-column TMEM buffers: epilogue warpgroup w owns
+// quarter w and double-buffers it (buffers 2w, 2w+1), so an epilogue never waits on an MMA that
+// is queued behind another warpgroup's buffer.
 //
-// Exactness (int8 view, hindexer.py:111): score = fl(float(acc) * scale_row), compared with the
-// threshold t in fp32 exactly like NumPy.  The fast path compares acc against an integer bound L
-// that is necessary for passing anywhere in the 32-row chunk (from the chunk's scale min/max),
-// then re-checks the few survivors exactly.  Raw mode (raw_int_ordering) compares acc directly.
+// Passers go to per-CTA private segments of each query's candidate list with shared-memory
+// counters (no global atomics on the hot path); a compaction kernel concatenates the segments.
+//
 #include <algorithm>
 
 #include "kernels.cuh"
@@ -34,10 +35,12 @@ constexpr int SZ_STAGE = SZ_CODES + NT * 8 + 1024;
 constexpr int OFF_A = 0;                          // MAXQB x 8 KB query codes (interleave)
 constexpr int OFF_RING = OFF_A + MAXQB * 8192;
 constexpr int OFF_T = OFF_RING + NSTAGE * SZ_STAGE;  // per-query threshold (f32 or s32), 4 KB
-constexpr int NEPI = 4;    // epilogue warpgroups: (TMEM buffer e = wg & 1) x (column half = wg >> 1)
+constexpr int OFF_CNT = OFF_T + MAXQB * QB * 4;      // per-query passer counters of this CTA, 4 KB
+constexpr int NEPI = 4;    // epilogue warpgroups: warpgroup w owns tile columns [64w, 64w + 64)
+constexpr int NBUF = 2 * NEPI;  // 64-column TMEM accumulators
 constexpr int NTHREADS = 64 + NEPI * 128;
-constexpr int OFF_BAR = OFF_T + MAXQB * QB * 4;
-constexpr int NBAR = 2 * NSTAGE + 4;
+constexpr int OFF_BAR = OFF_CNT + MAXQB * QB * 4;
+constexpr int NBAR = 2 * NSTAGE + 2 * NBUF;
 constexpr int OFF_TMEM = OFF_BAR + NBAR * 8;
 constexpr int SMEM_BYTES = OFF_TMEM + 16;
 
@@ -65,19 +68,31 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       "r"(parity), "r"(0x989680)
       : "memory");
 }
+__device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.b32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
                "l"(src), "r"(bytes), "r"(bar)
                : "memory");
 }
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ uint64_t desc_ilv(uint32_t addr) {  // interleave K-major: LBO 128 B (K), SBO 512 B (rows)
   return uint64_t((addr >> 4) & 0x3FFF) | (uint64_t(128 >> 4) << 16) | (uint64_t(512 >> 4) << 32) | (1ull << 46);
 }
-// kind::i8: A = B = signed 8-bit, D = s32, K-major, M = 128, N = 256
-constexpr uint32_t IDESC_I8 = (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(NT >> 3) << 17) | (uint32_t(QB >> 4) << 24);
+// kind::i8: A = B = signed 8-bit, D = s32, K-major, M = 128, N = 64
+constexpr uint32_t IDESC_I8 = (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(64 >> 3) << 17) | (uint32_t(QB >> 4) << 24);
 __device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t accum) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
@@ -121,9 +136,10 @@ struct Params {
   const int8_t* qcodes;   // (B, 64) linear
   const uint32_t* tkeys;  // (B,) ascending-order threshold keys (filter modes)
   int strict;
-  int64_t cap;
+  int64_t cap;            // per query: gridDim.x private segments of `seg` entries
+  int64_t seg;
   int32_t* cand;          // (B, cap)
-  unsigned long long* counts;  // (B,)
+  int32_t* cta_counts;    // (B, gridDim.x) passers per (query, CTA) (may exceed seg: overflow)
   void* out;              // write modes: (B, ld) f32 / s32
   int64_t ld;
 };
@@ -138,12 +154,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) s1_tc_kernel(Params P) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nqb = (P.B + QB - 1) / QB;
   const int64_t ntiles = (P.n + NT - 1) / NT;
+  // each CTA scans one contiguous block of tiles, so its private candidate segments are in
+  // ascending item order and the concatenated per-query lists are (nearly) id-sorted: stage 2
+  // then walks every query's candidates through the same item window at the same time (L2 reuse)
+  const int64_t tile_lo = (int64_t(blockIdx.x) * ntiles) / gridDim.x;
+  const int64_t tile_hi = (int64_t(blockIdx.x + 1) * ntiles) / gridDim.x;
   auto bar = [&](int i) { return sbase + OFF_BAR + 8 * i; };
   auto full_bar = [&](int s) { return bar(s); };
   auto empty_bar = [&](int s) { return bar(NSTAGE + s); };
   auto tfull = [&](int e) { return bar(2 * NSTAGE + e); };
-  auto tempty = [&](int e) { return bar(2 * NSTAGE + 2 + e); };
+  auto tempty = [&](int e) { return bar(2 * NSTAGE + NBUF + e); };
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + OFF_TMEM);
+  uint32_t* scnt = reinterpret_cast<uint32_t*>(sm + OFF_CNT);
 
   // ---- setup: query codes -> interleave operand blocks (zero padded), thresholds, barriers ----
   for (int i = threadIdx.x; i < nqb * QB * 4; i += blockDim.x) {
@@ -158,15 +180,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) s1_tc_kernel(Params P) {
       uint32_t t = 0;
       if (q < P.B) t = RAW ? uint32_t(key_i32(__ldg(P.tkeys + q))) : __float_as_uint(key_f32(__ldg(P.tkeys + q)));
       reinterpret_cast<uint32_t*>(sm + OFF_T)[q] = t;
+      scnt[q] = 0;
     }
   if (threadIdx.x == 0) {
     for (int s = 0; s < NSTAGE; ++s) {
       mbar_init(full_bar(s), 1);
       mbar_init(empty_bar(s), 1 + NEPI * 128);
     }
-    for (int e = 0; e < 2; ++e) {
+    for (int e = 0; e < NBUF; ++e) {
       mbar_init(tfull(e), 1);
-      mbar_init(tempty(e), 256);
+      mbar_init(tempty(e), 128);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -185,7 +208,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) s1_tc_kernel(Params P) {
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      for (int64_t tile = tile_lo; tile < tile_hi; ++tile) {
         mbar_wait(empty_bar(stage), phase ^ 1);
         const uint32_t st = sbase + OFF_RING + stage * SZ_STAGE;
         mbar_arrive_expect_tx(full_bar(stage), SZ_CODES + NT * 4 + (WRITE ? 0 : 64) + ((WRITE || KEYS) ? 0 : NT * 4));
@@ -201,23 +224,27 @@ __global__ void __launch_bounds__(NTHREADS, 1) s1_tc_kernel(Params P) {
     }
   } else if (warp == 1) {
     // ================= MMA issuer =================
+    // per (tile, query block): four M=128 x N=64 x K=64 MMAs, one per tile quarter, each into
+    // its warpgroup's next buffer (blocking waits: the hardware sleeps the thread)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      uint32_t eph[2] = {0, 0};
-      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      uint32_t jc = 0;  // (tile, query block) jobs issued: buffer parity = jc & 1, use = jc >> 1
+      for (int64_t tile = tile_lo; tile < tile_hi; ++tile) {
         mbar_wait(full_bar(stage), phase);
         tc_fence_after();
         const uint32_t bt = sbase + OFF_RING + stage * SZ_STAGE;
-        for (int qb = 0; qb < nqb; ++qb) {
-          const int e = qb & 1;
-          mbar_wait(tempty(e), eph[e] ^ 1);
-          eph[e] ^= 1;
-          tc_fence_after();
+        for (int qb = 0; qb < nqb; ++qb, ++jc) {
           const uint32_t at = sbase + OFF_A + qb * 8192;
-          mma_i8(tmem_base + e * 256, desc_ilv(at), desc_ilv(bt), 0);
-          mma_i8(tmem_base + e * 256, desc_ilv(at + 256), desc_ilv(bt + 256), 1);
-          mma_commit(tfull(e));
+#pragma unroll
+          for (int qt = 0; qt < NEPI; ++qt) {
+            const int buf = qt * 2 + int(jc & 1);
+            mbar_wait(tempty(buf), ((jc >> 1) & 1) ^ 1);
+            tc_fence_after();
+            mma_i8(tmem_base + buf * 64, desc_ilv(at), desc_ilv(bt + qt * 4096), 0);
+            mma_i8(tmem_base + buf * 64, desc_ilv(at + 256), desc_ilv(bt + qt * 4096 + 256), 1);
+            mma_commit(tfull(buf));
+          }
         }
         mma_commit(empty_bar(stage));
         if (++stage == NSTAGE) {
@@ -229,34 +256,36 @@ __global__ void __launch_bounds__(NTHREADS, 1) s1_tc_kernel(Params P) {
     __syncwarp();
   } else {
     // ================= epilogue warpgroups =================
-    // WG w reads TMEM buffer e = w & 1 (query blocks qb = e, e+2, ...) and column half w >> 1.
-    const int wg = (warp - 2) >> 2;
-    const int e = wg & 1, half = wg >> 1;
-    const int quarter = warp & 3;
+    // WG w owns tile columns [64w, 64w+64) of every (tile, query block) job and TMEM buffers
+    // 2w / 2w+1 (double-buffered: the MMA of job j+1 runs under job j's epilogue).
+    const int w = (warp - 2) >> 2;
+    const int quarter = warp & 3;  // TMEM lane quarter this warp may access
     const int p = quarter * 32 + lane;
-    const uint32_t lanebit = 1u << lane;
-    const uint32_t tm = tmem_base + e * 256 + half * 128 + ((uint32_t)(quarter * 32) << 16);
+    const uint32_t tlane = (uint32_t)(quarter * 32) << 16;
     int stage = 0;
-    uint32_t phase = 0, tph = 0;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    uint32_t phase = 0;
+    int64_t jc = 0;
+    int32_t* cand_cta = P.cand ? P.cand + int64_t(blockIdx.x) * P.seg : nullptr;
+    for (int64_t tile = tile_lo; tile < tile_hi; ++tile) {
       mbar_wait(full_bar(stage), phase);  // scales / perm / chunk bounds of this tile are in smem
       const uint8_t* st = sm + OFF_RING + stage * SZ_STAGE;
-      const float* sc = reinterpret_cast<const float*>(st + ST_SC) + half * 128;
-      const int32_t* pm = reinterpret_cast<const int32_t*>(st + ST_PERM) + half * 128;
-      const float2* mm = reinterpret_cast<const float2*>(st + ST_MM) + half * 4;
-      const int64_t row0 = tile * NT + half * 128;
-      const int nvalid = (int)imax64(0, imin64(128, P.n - row0));
-      for (int qb = e; qb < nqb; qb += 2) {
+      const float* sc = reinterpret_cast<const float*>(st + ST_SC) + w * 64;
+      const int32_t* pm = reinterpret_cast<const int32_t*>(st + ST_PERM) + w * 64;
+      const float2* mm = reinterpret_cast<const float2*>(st + ST_MM) + w * 2;
+      const int64_t row0 = tile * NT + w * 64;
+      const int nvalid = (int)imax64(0, imin64(64, P.n - row0));
+      for (int qb = 0; qb < nqb; ++qb, ++jc) {
         const int q = qb * QB + p;
-        mbar_wait(tfull(e), tph);
-        tph ^= 1;
+        const int buf = w * 2 + int(jc & 1);
+        const uint32_t tm = tmem_base + buf * 64 + tlane;
+        mbar_wait(tfull(buf), uint32_t((jc >> 1) & 1));
         tc_fence_after();
         if (WRITE) {
 #pragma unroll 1
-          for (int cc = 0; cc < 4; ++cc) {
+          for (int cc = 0; cc < 2; ++cc) {
             uint32_t a[32];
             TMEM_LD32(tm + cc * 32, a);
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            TMEM_WAIT32(a);
             const int j0 = cc * 32;
             if (q < P.B && j0 < nvalid) {
               if (RAW) {
@@ -287,7 +316,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) s1_tc_kernel(Params P) {
             }
           }
         } else {
-          // per thread: one query (TMEM lane), 128 item columns as 4 chunks of 32 rows
+          // per thread: one query (TMEM lane), 64 item columns as 2 chunks of 32 rows
           const uint32_t traw = reinterpret_cast<const uint32_t*>(sm + OFF_T)[q];
           const float tf = __uint_as_float(traw);
           // strict (s > t) as s >= the next float above t (thresholds are finite scores);
@@ -295,65 +324,59 @@ __global__ void __launch_bounds__(NTHREADS, 1) s1_tc_kernel(Params P) {
           const float tfe = P.strict ? __uint_as_float(tf >= 0.f ? (tf == 0.f ? 1u : traw + 1u) : traw - 1u) : tf;
           const int32_t ti = int32_t(traw) + (P.strict ? 1 : 0);
           const float4* sc4 = reinterpret_cast<const float4*>(sc);
-          uint32_t mask[4];
-          int total = 0;
+          const float tlo = tf * (1.0f - 4e-6f), thi = tf * (1.0f + 4e-6f);
+          uint32_t mask[2];
           uint32_t ra[32], rb[32];
           TMEM_LD32(tm, ra);
 #pragma unroll
-          for (int cc = 0; cc < 4; ++cc) {
-            uint32_t* a = (cc & 1) ? rb : ra;
-            uint32_t* nx = (cc & 1) ? ra : rb;
+          for (int cc = 0; cc < 2; ++cc) {
+            uint32_t* a = cc ? rb : ra;
             // integer bound L: acc >= L is necessary to pass anywhere in this 32-row chunk
-            // (computed while the TMEM load is in flight)
+            // (from the chunk's (1/min, 1/max) scale with a relative margin; computed while the
+            // TMEM load is in flight).  Padding rows are masked below, so their bound is moot.
             int32_t L;
             if (RAW) {
               L = ti;  // exact
             } else {
-              const float2 inv = mm[cc];  // (1/min scale, 1/max scale) of the chunk
-              if (inv.y < 0.f) {
-                L = 0x7fffffff;  // padding rows only
-              } else {
-                const float l = fminf(tf * inv.y * (1.0f - 4e-6f), tf * inv.x * (1.0f + 4e-6f));
-                L = l <= -1073741824.f ? -1073741824 : (l >= 1073741824.f ? 1073741824 : __float2int_rd(l) - 1);
-              }
+              const float2 inv = mm[cc];
+              L = max(__float2int_rd(fminf(tlo * inv.y, thi * inv.x)), -1073741824) - 1;
             }
             TMEM_WAIT32(a);
-            if (cc < 3) TMEM_LD32(tm + (cc + 1) * 32, nx);  // next chunk loads under this chunk's test
+            if (cc == 0) TMEM_LD32(tm + 32, rb);  // next chunk loads under this chunk's test
             const int j0 = cc * 32;
-            // per 8-column group: max as a shallow tree of 3-input maxes
-            int32_t gm[4];
+            // per 8-column group: max as a shallow tree of 3-input maxes; the warp-wide OR of the
+            // per-lane group hits makes the group branches warp-uniform
+            uint32_t h = 0;
 #pragma unroll
             for (int g8 = 0; g8 < 4; ++g8) {
               const int32_t* v = reinterpret_cast<const int32_t*>(a) + g8 * 8;
-              gm[g8] = max(__vimax3_s32(v[0], v[1], v[2]), __vimax3_s32(v[3], v[4], max(v[5], max(v[6], v[7]))));
+              const int32_t gm = max(__vimax3_s32(v[0], v[1], v[2]), __vimax3_s32(v[3], v[4], max(v[5], max(v[6], v[7]))));
+              h |= uint32_t(gm >= L) << g8;
             }
+            h = __reduce_or_sync(0xffffffffu, h);
             uint32_t m = 0;
 #pragma unroll
             for (int g8 = 0; g8 < 4; ++g8) {
-              // a group is examined by the warp only if some lane may have a passer in it
-              if (__any_sync(0xffffffffu, gm[g8] >= L)) {
-                if (gm[g8] >= L) {
-                  const int32_t* v = reinterpret_cast<const int32_t*>(a) + g8 * 8;
-                  uint32_t bits = 0;
-                  if (RAW) {
+              if (h & (1u << g8)) {  // some lane may have a passer in this group: test all 8 exactly
+                const int32_t* v = reinterpret_cast<const int32_t*>(a) + g8 * 8;
+                uint32_t bits = 0;
+                if (RAW) {
 #pragma unroll
-                    for (int jj = 0; jj < 8; ++jj) bits |= uint32_t(v[jj] >= L) << jj;
-                  } else {  // exact fp32 test: fl(acc * scale) >= t  (hindexer.py:111)
-                    const float4 s0 = sc4[(j0 + g8 * 8) >> 2], s1 = sc4[((j0 + g8 * 8) >> 2) + 1];
-                    const float sv[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+                  for (int jj = 0; jj < 8; ++jj) bits |= uint32_t(v[jj] >= L) << jj;
+                } else {  // exact fp32 test: fl(acc * scale) >= t  (hindexer.py:111)
+                  const float4 s0 = sc4[(j0 + g8 * 8) >> 2], s1 = sc4[((j0 + g8 * 8) >> 2) + 1];
+                  const float sv[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
 #pragma unroll
-                    for (int jj = 0; jj < 8; ++jj) bits |= uint32_t(__fmul_rn((float)v[jj], sv[jj]) >= tfe) << jj;
-                  }
-                  m |= bits << (g8 * 8);
+                  for (int jj = 0; jj < 8; ++jj) bits |= uint32_t(__fmul_rn((float)v[jj], sv[jj]) >= tfe) << jj;
                 }
+                m |= bits << (g8 * 8);
               }
             }
             const int lim = nvalid - j0;  // valid columns in this chunk
             if (lim < 32) m &= lim <= 0 ? 0u : ((1u << lim) - 1u);
             mask[cc] = m;
-            total += __popc(m);
             if (KEYS && m && q < P.B) {  // append the passers' ascending score keys now (a[] is live)
-              unsigned long long pos = atomicAdd(P.counts + q, (unsigned long long)__popc(m));
+              uint32_t pos = atomicAdd(scnt + q, (uint32_t)__popc(m));
               while (m) {
                 const int j = __ffs(m) - 1;
                 m &= m - 1;
@@ -362,27 +385,28 @@ __global__ void __launch_bounds__(NTHREADS, 1) s1_tc_kernel(Params P) {
                 for (int jj = 0; jj < 32; ++jj) accv = (jj == j) ? a[jj] : accv;  // static register select
                 const int32_t acc = int32_t(accv);
                 const uint32_t key = RAW ? i32_key(acc) : f32_key(__fmul_rn((float)acc, sc[j0 + j]));
-                if ((int64_t)pos < P.cap) P.cand[int64_t(q) * P.cap + (int64_t)pos] = int32_t(key);
+                if ((int64_t)pos < P.seg) cand_cta[int64_t(q) * P.cap + pos] = int32_t(key);
                 ++pos;
               }
             }
           }
+          const int total = __popc(mask[0]) + __popc(mask[1]);
           if (!KEYS && total && q < P.B) {
-            unsigned long long pos = atomicAdd(P.counts + q, (unsigned long long)total);
+            uint32_t pos = atomicAdd(scnt + q, (uint32_t)total);  // shared-memory counter
 #pragma unroll
-            for (int cc = 0; cc < 4; ++cc) {
+            for (int cc = 0; cc < 2; ++cc) {
               uint32_t m = mask[cc];
               while (m) {
                 const int j = __ffs(m) - 1;
                 m &= m - 1;
-                if ((int64_t)pos < P.cap) P.cand[int64_t(q) * P.cap + (int64_t)pos] = pm[cc * 32 + j];
+                if ((int64_t)pos < P.seg) cand_cta[int64_t(q) * P.cap + pos] = pm[cc * 32 + j];
                 ++pos;
               }
             }
           }
         }
         tc_fence_before();
-        mbar_arrive(tempty(e));
+        mbar_arrive(tempty(buf));
       }
       mbar_arrive(empty_bar(stage));
       if (++stage == NSTAGE) {
@@ -394,7 +418,41 @@ __global__ void __launch_bounds__(NTHREADS, 1) s1_tc_kernel(Params P) {
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (!WRITE)
+    for (int q = threadIdx.x; q < P.B; q += blockDim.x) P.cta_counts[int64_t(q) * gridDim.x + blockIdx.x] = int32_t(scnt[q]);
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
+}
+
+// Concatenate the per-CTA segments of each query's candidate list (row b: G segments of `seg`
+// entries at src + b*cap_in + g*seg, counts cnt[b*G + g]) into dst + b*cap_out; counts[b] = the
+// true total (may exceed cap_out); *max_cta = the largest per-CTA count (overflow if > seg).
+__global__ void __launch_bounds__(256) compact_segments_kernel(int G, int64_t seg, int64_t cap_in, const int32_t* __restrict__ src,
+                                                               const int32_t* __restrict__ cnt, int64_t cap_out,
+                                                               int32_t* __restrict__ dst, int64_t* __restrict__ counts,
+                                                               int* __restrict__ max_cta) {
+  __shared__ int64_t pre[1025];
+  const int b = blockIdx.x;
+  if (threadIdx.x == 0) {
+    int64_t acc = 0;
+    int mx = 0;
+    for (int g = 0; g < G; ++g) {
+      const int c = cnt[int64_t(b) * G + g];
+      pre[g] = acc;
+      acc += c;
+      mx = max(mx, c);
+    }
+    pre[G] = acc;
+    counts[b] = acc;
+    if (mx > 0) atomicMax(max_cta, mx);
+  }
+  __syncthreads();
+  for (int g = 0; g < G; ++g) {
+    const int64_t n = imin64(pre[g + 1] - pre[g], seg);
+    const int32_t* s = src + int64_t(b) * cap_in + int64_t(g) * seg;
+    int32_t* d = dst + int64_t(b) * cap_out + pre[g];
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x)
+      if (pre[g] + i < cap_out) d[i] = s[i];
+  }
 }
 
 }  // namespace s1tc
@@ -416,35 +474,61 @@ int s1_tc_scan(molr_ctx* ctx, int mode, const int8_t* codes, const float* scales
                       : (raw ? WRITE_RAW : WRITE_SCALED);
   const int64_t ntiles = (n + NT - 1) / NT;
   const int grid = (int)std::min<int64_t>(ntiles, ctx->num_sms);
+  const bool filter = tkeys != nullptr;
+  // per-CTA private segments: expected cap/grid passers each, with headroom; one retry at the
+  // exact maximum if a segment overflowed
+  int64_t seg = filter ? (cap / grid) + (cap / grid) / 3 + 64 : 0;
   for (int b0 = 0; b0 < B; b0 += MAXQB * QB) {
-    Params P;
-    P.codes = codes;
-    P.scales = scales;
-    P.chunk_mm = mm;
-    P.perm = perm;
-    P.n = n;
-    P.B = std::min(B - b0, MAXQB * QB);
-    P.qcodes = qcodes + int64_t(b0) * 64;
-    P.tkeys = tkeys ? tkeys + b0 : nullptr;
-    P.strict = strict;
-    P.cap = cap;
-    P.cand = cand ? cand + int64_t(b0) * cap : nullptr;
-    P.counts = reinterpret_cast<unsigned long long*>(counts ? counts + b0 : nullptr);
-    P.out = out ? reinterpret_cast<char*>(out) + int64_t(b0) * ld * 4 : nullptr;
-    P.ld = ld;
-    auto launch = [&](auto kern) -> int {
-      MOLR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
-      kern<<<grid, NTHREADS, SMEM_BYTES, s>>>(P);
+    const int Bc = std::min(B - b0, MAXQB * QB);
+    for (int attempt = 0; attempt < 2; ++attempt) {
+      Scratch priv, ccount, mx;
+      Params P;
+      P.codes = codes;
+      P.scales = scales;
+      P.chunk_mm = mm;
+      P.perm = perm;
+      P.n = n;
+      P.B = Bc;
+      P.qcodes = qcodes + int64_t(b0) * 64;
+      P.tkeys = tkeys ? tkeys + b0 : nullptr;
+      P.strict = strict;
+      P.seg = seg;
+      P.cap = int64_t(grid) * seg;
+      P.cand = nullptr;
+      P.cta_counts = nullptr;
+      if (filter) {
+        MOLR_TRY(priv.alloc(size_t(Bc) * P.cap * 4, s));
+        MOLR_TRY(ccount.alloc(size_t(Bc) * grid * 4, s));
+        MOLR_TRY(mx.alloc(4, s));
+        MOLR_CUDA(cudaMemsetAsync(mx.p, 0, 4, s));
+        P.cand = priv.as<int32_t>();
+        P.cta_counts = ccount.as<int32_t>();
+      }
+      P.out = out ? reinterpret_cast<char*>(out) + int64_t(b0) * ld * 4 : nullptr;
+      P.ld = ld;
+      auto launch = [&](auto kern) -> int {
+        MOLR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+        kern<<<grid, NTHREADS, SMEM_BYTES, s>>>(P);
+        MOLR_LAUNCHED(ctx);
+        return MOLR_OK;
+      };
+      switch (m) {
+        case FILTER_SCALED: MOLR_TRY(launch(s1_tc_kernel<FILTER_SCALED>)); break;
+        case FILTER_RAW: MOLR_TRY(launch(s1_tc_kernel<FILTER_RAW>)); break;
+        case WRITE_SCALED: MOLR_TRY(launch(s1_tc_kernel<WRITE_SCALED>)); break;
+        case WRITE_RAW: MOLR_TRY(launch(s1_tc_kernel<WRITE_RAW>)); break;
+        case KEYS_SCALED: MOLR_TRY(launch(s1_tc_kernel<KEYS_SCALED>)); break;
+        default: MOLR_TRY(launch(s1_tc_kernel<KEYS_RAW>)); break;
+      }
+      if (!filter) break;
+      compact_segments_kernel<<<Bc, 256, 0, s>>>(grid, seg, P.cap, P.cand, P.cta_counts, cap, cand + int64_t(b0) * cap,
+                                                 counts + b0, mx.as<int>());
       MOLR_LAUNCHED(ctx);
-      return MOLR_OK;
-    };
-    switch (m) {
-      case FILTER_SCALED: MOLR_TRY(launch(s1_tc_kernel<FILTER_SCALED>)); break;
-      case FILTER_RAW: MOLR_TRY(launch(s1_tc_kernel<FILTER_RAW>)); break;
-      case WRITE_SCALED: MOLR_TRY(launch(s1_tc_kernel<WRITE_SCALED>)); break;
-      case WRITE_RAW: MOLR_TRY(launch(s1_tc_kernel<WRITE_RAW>)); break;
-      case KEYS_SCALED: MOLR_TRY(launch(s1_tc_kernel<KEYS_SCALED>)); break;
-      default: MOLR_TRY(launch(s1_tc_kernel<KEYS_RAW>)); break;
+      int hmx = 0;
+      MOLR_CUDA(cudaMemcpyAsync(&hmx, mx.p, 4, cudaMemcpyDeviceToHost, s));
+      MOLR_CUDA(cudaStreamSynchronize(s));
+      if (hmx <= seg) break;
+      seg = hmx;  // a private segment overflowed: rerun with the exact maximum
     }
   }
   return MOLR_OK;
