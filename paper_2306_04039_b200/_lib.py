@@ -16,7 +16,7 @@ import numpy as np
 from paper_2306_04039_b200 import errors as E
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmolr_b200.so")
+LIB_PATH = os.environ.get("MOLR_LIB_PATH") or os.path.join(_HERE, "libmolr_b200.so")
 
 OK, ERR_DIM, ERR_RANGE, ERR_EMPTY, ERR_ZERO, ERR_LEN, ERR_CAP, ERR_CUDA, ERR_INVALID = range(9)
 S1_FLOAT, S1_INT8, S1_INT8_RAW = 0, 1, 2

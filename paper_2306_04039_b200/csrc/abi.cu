@@ -157,6 +157,29 @@ __global__ void chunk_mm_kernel(const float* __restrict__ scales, int64_t c0, in
   }
 }
 
+// 2-D tensor map viewing `rows` x 1 KB as uint32 [rows][256], box = one row (for tile::gather4)
+int encode_rows_tmap(CUtensorMap* tm, const void* base, int64_t rows) {
+  typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                               CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static EncodeFn enc = [] {
+    EncodeFn f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return f;
+  }();
+  if (!enc) return 0;
+  cuuint64_t dims[2] = {256, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {1024};
+  cuuint32_t box[2] = {256, 1};
+  cuuint32_t es[2] = {1, 1};
+  return enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<void*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 int chunk_minmax(molr_ctx* ctx, const float* scales, int64_t c0, int64_t c1, float2* mm, cudaStream_t s) {
   if (c1 <= c0) return MOLR_OK;
   chunk_mm_kernel<<<div_up(c1 - c0, 256), 256, 0, s>>>(scales, c0, c1, mm);
@@ -256,6 +279,7 @@ int molr_cache_alloc(molr_ctx* ctx, int64_t X, int k_x, int d, int G, int d1, in
   };
   size_t ne = size_t(X) * k_x * d;
   int st = (storage & MOLR_STORE_EMBS_F32) ? grab((void**)&c->embs_f32, ne * 4) : grab((void**)&c->embs_bf16, ne * 2);
+  if (!st && c->embs_bf16 && k_x * d == 512 && X > 0) c->embs_tmap_ok = encode_rows_tmap(&c->embs_tmap, c->embs_bf16, X);
   if (!st && (storage & MOLR_STORE_GP_F32)) st = grab((void**)&c->gp_f32, size_t(X) * G * 4);
   if (!st && !(storage & MOLR_STORE_GP_F32)) st = grab((void**)&c->gp_bf16, size_t(X) * G * 2);
   if (!st && (storage & MOLR_STORE_S1_F32)) st = grab((void**)&c->s1_f32, size_t(X) * d1 * 4);

@@ -154,6 +154,9 @@ struct molr_cache {
   // is "sealed" on first stage-1 use), so each 32-row chunk has a narrow scale range and the
   // tensor-core filter's integer pre-test is tight.  perm: stored position -> item id;
   // inv: item id -> stored position.
+  // TMA descriptor over item_embs as (X rows x 1 KB) for tile::gather4 loads (bf16, k_x*d = 512)
+  alignas(64) CUtensorMap embs_tmap{};
+  int embs_tmap_ok = 0;
   int32_t* s1_perm = nullptr;
   int32_t* s1_inv = nullptr;
   std::atomic<int> s1_sealed{0};

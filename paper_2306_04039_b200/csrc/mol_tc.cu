@@ -3,31 +3,36 @@
 // mol_top_k's scoring (mol.py:139-205, 329-386).
 //
 // One persistent CTA per SM, warp-specialised:
-//   warp 0       producer: per candidate, one 1 KB cp.async.bulk of the item's component block
-//                (the cache stores it pre-swizzled, see emb_offset) into a ring of 16-item stages
+//   warp 0       producer: per tile, the query's pre-built B0 operand (2 KB) into a small ring, and
+//                per candidate one 1 KB cp.async.bulk of the item's component block (the cache
+//                stores it pre-swizzled, see emb_offset) into a ring of 16-item stages
 //   warp 1       MMA issuer (one thread, non-blocking state machine) + TMEM owner
-//   warps 2..9   two epilogue warpgroups; tile t belongs to group t % 2, so one group's SIMT
-//                epilogue overlaps the other group's MMAs
-// Per tile of 128 (query, candidate) pairs of ONE query, per group TMEM columns [0, 256):
+//   warps 2..9   two epilogue warpgroups; tile k belongs to group k % 2
+// TMEM (512 columns): D0 = cols [0,128) is ONE buffer shared by both groups: the component
+// GEMM streams through it tile after tile (it only waits for the previous tile's E0 to drain it),
+// so the item ring is consumed continuously and the gather never stalls on an epilogue.
+// Group g owns cols [128 + 192 g, 320 + 192 g): A1/D2 (64) and D1/A2 (128).
+// Per tile of 128 (query, candidate) pairs of ONE query:
 //   C : 8 x [M=128 rows = 16 items x 8 components] x [N=16 = (hi,lo) x 8 user components] x K=64
-//       (SS) -> D0 = cols [0,128).  Query side split u = hi + lo in bf16 (~2^-17 relative), item
-//       side exact bf16, fp32 accumulation.
-//   E0: TMEM -> (hi+lo)/tau -> fp32 logits, transposed to one row per pair through smem (CL)
-//   E0.5: row p -> CLT (fp32, cols [0,64)) for the final gated sum, and A1 = bf16 logits packed
-//       two per column in cols [64,96) (the A operand of layer 1, read straight from TMEM)
-//   L1: A1 (TMEM) . W1^T (smem) + [1 1 0..] . [b1_hi b1_lo 0..]^T (SS, K=16) -> D1 cols [128,256)
+//       (SS) -> D0.  Query side split u = hi + lo in bf16 (~2^-17 relative), item side exact
+//       bf16, fp32 accumulation.
+//   E0: D0 -> (hi+lo)/tau -> fp32 logits, transposed to one row per pair in the group's smem CL
+//       (kept there for the final gated sum); D0 released
+//   E0.5: row p -> A1 = bf16 logits packed two per column (the A operand of layer 1, from TMEM)
+//   L1: A1 (TMEM) . W1^T (smem) + [1 1 0..] . [b1_hi b1_lo 0..]^T (SS, K=16) -> D1
 //   E1: h = silu(D1) -> A2 = [bf16(h) | bf16(h - bf16(h))] written in place over D1 (each
 //       16-column chunk: 8 cols hi + 8 cols lo); keeping h to ~2^-17 keeps the cross-net within
 //       tolerance for sharp gating
-//   L2: h_hi.W2_hi + h_lo.W2_hi + h_hi.W2_lo (A from TMEM, W2 split hi/lo in smem) -> D2 cols
-//       [64,128): the cross net's second layer is carried to ~2^-16 (W2 rounding dominated the
-//       error budget under sharp gating)
-//   E2: pi = softmax(silu(uw * gate_pre + D2)); score = sum pi * CLT  -> global
+//   L2: h_hi.W2_hi + h_lo.W2_hi + h_hi.W2_lo (A from TMEM, W2 split hi/lo in smem) -> D2: the
+//       cross net's second layer is carried to ~2^-16 (W2 rounding dominated the error budget
+//       under sharp gating)
+//   E2: pi = softmax(silu(uw * gate_pre + D2)); score = sum pi * CL  -> global
 // The G logits and H hidden units never leave the SM.
 #include <algorithm>
 #include <cstdlib>
 
 #include "kernels.cuh"
+#include "stage1.cuh"
 
 namespace molr {
 namespace tc {
@@ -39,7 +44,6 @@ constexpr int NGROUPS = TILE / GROUP;
 constexpr int NSTAGE = 6;           // ring stages (16 KB each): ~96 KB of item blocks in flight per SM
 constexpr int NE = 2;               // epilogue groups
 constexpr int CL_LD = 68;           // fp32 row stride of the logit transpose buffer (conflict-free LDS.128)
-constexpr int TMEM_COLS_PER_GROUP = 256;
 
 // ---- shared memory map (bytes; regions holding MMA operands are 1024-aligned) --------------
 constexpr int SZ_STAGE = GROUP * 1024;                  // 16 KB
@@ -49,18 +53,21 @@ constexpr int OFF_W2T = OFF_W1T + 16384;                // 2 x (64 x 64) bf16, S
 constexpr int OFF_W2L = OFF_W2T + 16384;                // W2^T residual bf16(W2 - bf16(W2))     16 KB
 constexpr int OFF_W1B = OFF_W2L + 16384;                // 128 x 16 bf16, interleave  4 KB
 constexpr int OFF_BIASA = OFF_W1B + 4096;               // 128 x 16 bf16, interleave  4 KB
-constexpr int OFF_GRP = OFF_BIASA + 4096;               // per epilogue group:
-constexpr int G_B0 = 0;                                 //   16 x 64 bf16 SW128 (u_hi ; u_lo)  2 KB
-constexpr int G_CL = 2048;                              //   fp32 logits [128 x 68]        34 KB
+constexpr int NB0 = 3;                                  // B0 (query operand) ring slots
+constexpr int OFF_B0 = OFF_BIASA + 4096;                // NB0 x 16 x 64 bf16 SW128 (u_hi ; u_lo), 2 KB each
+constexpr int OFF_GRP = OFF_B0 + NB0 * 2048;            // per epilogue group:
+constexpr int G_CL = 0;                                 //   fp32 logits [128 x 68]        34 KB
 constexpr int G_UW = G_CL + TILE * CL_LD * 4;           //   64 f32
-constexpr int SZ_GRP = 37888;                           //   (rounded to 1 KB)
-static_assert(G_UW + 256 <= SZ_GRP, "group region");
+constexpr int SZ_GRP = G_UW + 256;
 constexpr int OFF_BAR = OFF_GRP + NE * SZ_GRP;
-// barriers: full[NSTAGE], empty[NSTAGE], then per group: b0_ready, d0_full, a1_ready, d1_full, a2_ready, d2_full
-constexpr int NBAR = 2 * NSTAGE + 6 * NE;
+// barriers: full[NSTAGE], empty[NSTAGE], b0full[NB0], b0empty[NB0], d0free,
+//           then per group: d0_full, a1_ready, d1_full, a2_ready, d2_full
+constexpr int NBAR = 2 * NSTAGE + 2 * NB0 + 1 + 5 * NE;
 constexpr int OFF_TMEM = OFF_BAR + NBAR * 8;
 constexpr int SMEM_BYTES = OFF_TMEM + 16;
 static_assert(SMEM_BYTES <= 232448, "shared memory budget");
+constexpr int TM_D0 = 0;                                // shared component-logit accumulator
+__host__ __device__ constexpr int tm_grp(int g) { return 128 + 192 * g; }  // A1/D2 at +0, D1/A2 at +64
 
 // ---- PTX wrappers ---------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -98,6 +105,14 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
                "l"(src), "r"(bytes), "r"(bar)
                : "memory");
+}
+// tile::gather4: rows r0..r3 (1 KB each) of a [rows][256 x u32] tensor map -> 4 KB of smem
+__device__ __forceinline__ void gather4_g2s(uint32_t dst, const CUtensorMap* tm, int r0, int r1, int r2, int r3,
+                                            uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
+      "l"(tm), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(bar)
+      : "memory");
 }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -242,24 +257,29 @@ struct Params {
   const int64_t* end;
   int64_t X;
   const int64_t* tile_pre;
+  const uint8_t* b0img;       // (B, 2048) per-query B0 operand images (b0_image_kernel)
   float* out;
   int64_t out_ld;
   int e1_tanh;  // hidden SiLU via tanh.approx (1 MUFU) instead of ex2 + rcp (2 MUFU)
+  int gather4;  // item fetch by TMA tile::gather4 (4 items per request) instead of 1 KB bulk copies
 };
 
 template <class Id>
-__global__ void __launch_bounds__(64 + NE * 128, 1) mol_tc_kernel(Params P, const Id* __restrict__ ids) {
+__global__ void __launch_bounds__(64 + NE * 128, 1) mol_tc_kernel(Params P, const Id* __restrict__ ids,
+                                                                  const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ __align__(1024) uint8_t sm[];
   const uint32_t sbase = smem_u32(sm);
   if ((sbase & 1023u) != 0u) __trap();  // SW128 operands need 1024-aligned atoms
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + OFF_BAR);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + OFF_TMEM);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   auto bar = [&](int i) { return sbase + OFF_BAR + 8 * i; };
   auto full_bar = [&](int s) { return bar(s); };
   auto empty_bar = [&](int s) { return bar(NSTAGE + s); };
-  // k: 0 b0_ready 1 d0_full 2 a1_ready 3 d1_full 4 a2_ready 5 d2_full
-  auto gbar = [&](int g, int k) { return bar(2 * NSTAGE + 6 * g + k); };
+  auto b0full = [&](int s) { return bar(2 * NSTAGE + s); };
+  auto b0empty = [&](int s) { return bar(2 * NSTAGE + NB0 + s); };
+  const uint32_t d0free = bar(2 * NSTAGE + 2 * NB0);
+  // k: 0 d0_full 1 a1_ready 2 d1_full 3 a2_ready 4 d2_full
+  auto gbar = [&](int g, int k) { return bar(2 * NSTAGE + 2 * NB0 + 1 + 5 * g + k); };
 
   // ---- one-time setup: weight images + constant bias operand, barriers, TMEM ----
   {
@@ -282,19 +302,23 @@ __global__ void __launch_bounds__(64 + NE * 128, 1) mol_tc_kernel(Params P, cons
         mbar_init(full_bar(s), 1);
         mbar_init(empty_bar(s), 1);
       }
+      for (int s = 0; s < NB0; ++s) {
+        mbar_init(b0full(s), 1);
+        mbar_init(b0empty(s), 1);
+      }
+      mbar_init(d0free, 128);
       for (int g = 0; g < NE; ++g) {
-        mbar_init(gbar(g, 0), 128);
-        mbar_init(gbar(g, 1), 1);
-        mbar_init(gbar(g, 2), 128);
-        mbar_init(gbar(g, 3), 1);
-        mbar_init(gbar(g, 4), 128);
-        mbar_init(gbar(g, 5), 1);
+        mbar_init(gbar(g, 0), 1);
+        mbar_init(gbar(g, 1), 128);
+        mbar_init(gbar(g, 2), 1);
+        mbar_init(gbar(g, 3), 128);
+        mbar_init(gbar(g, 4), 1);
       }
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
       asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                   "r"(NE * TMEM_COLS_PER_GROUP));
+                   "r"(512));
       asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     fence_async_smem();
@@ -306,9 +330,9 @@ __global__ void __launch_bounds__(64 + NE * 128, 1) mol_tc_kernel(Params P, cons
   const int64_t T = P.tile_pre[P.B];
 
   if (warp == 0) {
-    // ================= producer: item blocks -> ring =================
-    int stage = 0;
-    uint32_t phase = 0;
+    // ================= producer: B0 image + item blocks -> rings =================
+    int stage = 0, slot = 0;
+    uint32_t phase = 0, bphase = 0;
     TileCursor cur;
     for (int64_t tile = blockIdx.x; tile < T; tile += gridDim.x) {
       const TileInfo t = tile_info(cur, tile, P.B, P.tile_pre, P.begin, P.end, P.X);
@@ -319,14 +343,28 @@ __global__ void __launch_bounds__(64 + NE * 128, 1) mol_tc_kernel(Params P, cons
         const int q = lane + 32 * i;
         xid[i] = cand_id(ids, t, q < t.np ? q : 0);
       }
+      mbar_wait(b0empty(slot), bphase ^ 1);
+      if (lane == 0) {
+        mbar_arrive_expect_tx(b0full(slot), 2048);
+        bulk_g2s(sbase + OFF_B0 + slot * 2048, P.b0img + int64_t(t.b) * 2048, 2048, b0full(slot));
+      }
+      if (++slot == NB0) {
+        slot = 0;
+        bphase ^= 1;
+      }
 #pragma unroll
       for (int g = 0; g < NGROUPS; ++g) {
         const int64_t x = __shfl_sync(0xffffffffu, xid[g >> 1], 16 * (g & 1) + (lane & 15));
         mbar_wait(empty_bar(stage), phase ^ 1);
         if (lane == 0) mbar_arrive_expect_tx(full_bar(stage), SZ_STAGE);
         __syncwarp();
-        if (lane < GROUP)
+        if (P.gather4) {  // 4 items (4 KB) per TMA request: lane l < 4 fetches items 4l .. 4l+3
+          const int r0 = __shfl_sync(0xffffffffu, int(x), (4 * lane) & 15), r1 = __shfl_sync(0xffffffffu, int(x), (4 * lane + 1) & 15);
+          const int r2 = __shfl_sync(0xffffffffu, int(x), (4 * lane + 2) & 15), r3 = __shfl_sync(0xffffffffu, int(x), (4 * lane + 3) & 15);
+          if (lane < 4) gather4_g2s(sbase + OFF_RING + stage * SZ_STAGE + lane * 4096, &tmap, r0, r1, r2, r3, full_bar(stage));
+        } else if (lane < GROUP) {
           bulk_g2s(sbase + OFF_RING + stage * SZ_STAGE + lane * 1024, P.embs + x * (KX * D), 1024, full_bar(stage));
+        }
         __syncwarp();
         if (++stage == NSTAGE) {
           stage = 0;
@@ -338,79 +376,92 @@ __global__ void __launch_bounds__(64 + NE * 128, 1) mol_tc_kernel(Params P, cons
     // ================= MMA issuer (one thread, never blocks on a single barrier) =================
     if (lane == 0) {
       constexpr uint32_t ID16 = idesc_bf16(16), ID128 = idesc_bf16(128), ID64 = idesc_bf16(64);
-      int stage = 0;
-      uint32_t rphase = 0;
-      // per group: 0 wait B0, 1 component MMAs (grp progress), 2 need L1, 3 need L2
-      int64_t gtile[NE];
-      int gstate[NE], ggrp[NE];
-      uint32_t gphase[NE];
+      int stage = 0, slot = 0;
+      uint32_t rphase = 0, bphase = 0;
+      // component stream: local tile kc (ring order), 8 stage groups each
+      int64_t ctile = blockIdx.x;
+      int64_t kc = 0;
+      int cgrp = -1;  // -1: waiting for D0 free + B0
+      // per epilogue group chain: state 0 need L1 (a1_ready), 1 need L2 (a2_ready); use count
+      int gstate[NE];
+      uint32_t guse[NE];
+      int64_t gk[NE];  // local tile index the group is on (its m-th tile: k = 2 m + g)
 #pragma unroll
       for (int g = 0; g < NE; ++g) {
-        gtile[g] = blockIdx.x + (int64_t)g * gridDim.x;
         gstate[g] = 0;
-        ggrp[g] = 0;
-        gphase[g] = 0;
+        guse[g] = 0;
+        gk[g] = g;
       }
-      int64_t next_c = blockIdx.x;  // component MMAs follow ring (= tile) order
-      int live = 0;
-#pragma unroll
-      for (int g = 0; g < NE; ++g) live += gtile[g] < T;
-      while (live > 0) {
-#pragma unroll
-        for (int g = 0; g < NE; ++g) {
-          if (gtile[g] >= T) continue;
-          const uint32_t gb = sbase + OFF_GRP + g * SZ_GRP;
-          const uint32_t tm = tmem_base + g * TMEM_COLS_PER_GROUP;
-          if (gstate[g] == 0) {
-            if (gtile[g] != next_c || !mbar_test(gbar(g, 0), gphase[g])) continue;
-            tc_fence_after();
-            gstate[g] = 1;
+      const int64_t my_tiles = T > blockIdx.x ? (T - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+      while (kc < my_tiles || gk[0] < my_tiles || gk[1] < my_tiles) {
+        // ---- component GEMM stream ----
+        if (kc < my_tiles) {
+          if (cgrp < 0) {
+            // D0 drained by the previous tile's E0, and this tile's query operand landed
+            if ((kc == 0 || mbar_test(d0free, uint32_t((kc - 1) & 1))) && mbar_test(b0full(slot), bphase)) {
+              tc_fence_after();
+              cgrp = 0;
+            }
           }
-          if (gstate[g] == 1) {
-            while (ggrp[g] < NGROUPS && mbar_test(full_bar(stage), rphase)) {
+          if (cgrp >= 0) {
+            const uint32_t b0 = sbase + OFF_B0 + slot * 2048;
+            while (cgrp < NGROUPS && mbar_test(full_bar(stage), rphase)) {
               tc_fence_after();
               const uint32_t a0 = sbase + OFF_RING + stage * SZ_STAGE;
 #pragma unroll
               for (int kk = 0; kk < 4; ++kk)
-                mma_bf16(tm + ggrp[g] * 16, desc_sw128(a0 + kk * 32), desc_sw128(gb + G_B0 + kk * 32), ID16, kk > 0);
+                mma_bf16(tmem_base + TM_D0 + cgrp * 16, desc_sw128(a0 + kk * 32), desc_sw128(b0 + kk * 32), ID16, kk > 0);
               mma_commit(empty_bar(stage));
               if (++stage == NSTAGE) {
                 stage = 0;
                 rphase ^= 1;
               }
-              ++ggrp[g];
+              ++cgrp;
             }
-            if (ggrp[g] < NGROUPS) continue;
-            mma_commit(gbar(g, 1));
-            next_c += gridDim.x;
-            ggrp[g] = 0;
-            gstate[g] = 2;
-          } else if (gstate[g] == 2) {
-            if (!mbar_test(gbar(g, 2), gphase[g])) continue;
+            if (cgrp == NGROUPS) {
+              mma_commit(gbar(int(kc & 1), 0));  // D0 of local tile kc complete -> group kc % 2
+              mma_commit(b0empty(slot));
+              if (++slot == NB0) {
+                slot = 0;
+                bphase ^= 1;
+              }
+              ++kc;
+              ctile += gridDim.x;
+              cgrp = -1;
+            }
+          }
+        }
+        // ---- cross-net layers of each group's current tile ----
+#pragma unroll
+        for (int g = 0; g < NE; ++g) {
+          if (gk[g] >= my_tiles) continue;
+          const uint32_t tg = tmem_base + tm_grp(g);
+          const uint32_t up = guse[g] & 1;
+          if (gstate[g] == 0) {
+            if (!mbar_test(gbar(g, 1), up)) continue;
             tc_fence_after();
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
-              mma_bf16_ts(tm + 128, tm + 64 + kk * 8, desc_sw128(sbase + OFF_W1T + kk * 32), ID128, kk > 0);
-            mma_bf16(tm + 128, desc_interleave(sbase + OFF_BIASA, 128, 256), desc_interleave(sbase + OFF_W1B, 128, 256),
+              mma_bf16_ts(tg + 64, tg + kk * 8, desc_sw128(sbase + OFF_W1T + kk * 32), ID128, kk > 0);
+            mma_bf16(tg + 64, desc_interleave(sbase + OFF_BIASA, 128, 256), desc_interleave(sbase + OFF_W1B, 128, 256),
                      ID128, 1);
-            mma_commit(gbar(g, 3));
-            gstate[g] = 3;
+            mma_commit(gbar(g, 2));
+            gstate[g] = 1;
           } else {
-            if (!mbar_test(gbar(g, 4), gphase[g])) continue;
+            if (!mbar_test(gbar(g, 3), up)) continue;
             tc_fence_after();
 #pragma unroll
             for (int ch = 0; ch < 8; ++ch) {  // hidden chunk ch = K [16ch, 16ch+16)
               const uint32_t bo = (ch >> 2) * 8192 + (ch & 3) * 32;
               const uint64_t bhi = desc_sw128(sbase + OFF_W2T + bo), blo = desc_sw128(sbase + OFF_W2L + bo);
-              mma_bf16_ts(tm + 64, tm + 128 + ch * 16, bhi, ID64, ch > 0);  // h_hi . W2_hi
-              mma_bf16_ts(tm + 64, tm + 128 + ch * 16 + 8, bhi, ID64, 1);   // h_lo . W2_hi
-              mma_bf16_ts(tm + 64, tm + 128 + ch * 16, blo, ID64, 1);       // h_hi . W2_lo
+              mma_bf16_ts(tg, tg + 64 + ch * 16, bhi, ID64, ch > 0);  // h_hi . W2_hi
+              mma_bf16_ts(tg, tg + 64 + ch * 16 + 8, bhi, ID64, 1);   // h_lo . W2_hi
+              mma_bf16_ts(tg, tg + 64 + ch * 16, blo, ID64, 1);       // h_hi . W2_lo
             }
-            mma_commit(gbar(g, 5));
+            mma_commit(gbar(g, 4));
             gstate[g] = 0;
-            gphase[g] ^= 1;
-            gtile[g] += (int64_t)NE * gridDim.x;
-            if (gtile[g] >= T) --live;
+            ++guse[g];
+            gk[g] += NE;
           }
         }
       }
@@ -424,30 +475,15 @@ __global__ void __launch_bounds__(64 + NE * 128, 1) mol_tc_kernel(Params P, cons
     uint8_t* gs = sm + OFF_GRP + eg * SZ_GRP;
     float* CL = reinterpret_cast<float*>(gs + G_CL);
     float* UW = reinterpret_cast<float*>(gs + G_UW);
-    const uint32_t tm = tmem_base + eg * TMEM_COLS_PER_GROUP + ((uint32_t)(quarter * 32) << 16);
+    const uint32_t lq = (uint32_t)(quarter * 32) << 16;
+    const uint32_t td0 = tmem_base + TM_D0 + lq;
+    const uint32_t tg = tmem_base + tm_grp(eg) + lq;
     const int bar_id = 1 + eg;
     uint32_t ph = 0;
     TileCursor cur;
     for (int64_t tile = blockIdx.x + (int64_t)eg * gridDim.x; tile < T; tile += (int64_t)NE * gridDim.x) {
       const TileInfo t = tile_info(cur, tile, P.B, P.tile_pre, P.begin, P.end, P.X);
-      // ---- query operand B0 = [u_hi ; u_lo] (16 x 64 bf16, SW128) and uw ----
-      {
-        const int r = p >> 3, c = p & 7, a = r & 7;  // 128 threads = 16 rows x 8 chunks
-        const float* u = P.user_embs + (int64_t)t.b * (KX * D) + a * D + c * 8;
-        const float4 v0 = __ldg(reinterpret_cast<const float4*>(u)), v1 = __ldg(reinterpret_cast<const float4*>(u) + 1);
-        const float f[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-        uint32_t w[4];
-#pragma unroll
-        for (int m = 0; m < 4; ++m) {
-          const uint32_t hw = pack_bf16(f[2 * m], f[2 * m + 1]);
-          w[m] = (r < 8) ? hw : pack_bf16(f[2 * m] - __uint_as_float(hw << 16), f[2 * m + 1] - __uint_as_float(hw & 0xFFFF0000u));
-        }
-        *reinterpret_cast<uint4*>(gs + G_B0 + sw128(r, c)) = make_uint4(w[0], w[1], w[2], w[3]);
-        if (p < G) UW[p] = __ldg(P.uw + (int64_t)t.b * G + p);
-      }
-      fence_async_smem();
-      tc_fence_before();
-      mbar_arrive(gbar(eg, 0));
+      if (p < G) UW[p] = __ldg(P.uw + (int64_t)t.b * G + p);
       // prefetch this row's gate pre-activations (bf16 x 64 = 128 B)
       uint4 gpr[8];
       {
@@ -456,14 +492,14 @@ __global__ void __launch_bounds__(64 + NE * 128, 1) mol_tc_kernel(Params P, cons
 #pragma unroll
         for (int m = 0; m < 8; ++m) gpr[m] = __ldg(src + m);
       }
-      // ---- E0: component logits -> CL (transpose to one row per pair) ----
-      mbar_wait(gbar(eg, 1), ph);
+      // ---- E0: component logits (shared D0) -> CL (transpose to one row per pair); free D0 ----
+      mbar_wait(gbar(eg, 0), ph);
       tc_fence_after();
 #pragma unroll
       for (int grp = 0; grp < NGROUPS; grp += 2) {
         uint32_t v[16], w[16];
-        TMEM_LD16(tm + grp * 16, v);
-        TMEM_LD16(tm + grp * 16 + 16, w);
+        TMEM_LD16(td0 + grp * 16, v);
+        TMEM_LD16(td0 + grp * 16 + 16, w);
         tmem_wait_ld();
         const int q = grp * GROUP + (p >> 3), bb = p & 7;
 #pragma unroll
@@ -473,38 +509,33 @@ __global__ void __launch_bounds__(64 + NE * 128, 1) mol_tc_kernel(Params P, cons
         }
       }
       tc_fence_before();
+      mbar_arrive(d0free);  // the next tile's component GEMM may overwrite D0
       named_sync(bar_id, 128);
-      tc_fence_after();
-      // ---- E0.5: row p -> CLT (fp32, cols [0,64)) and A1 (bf16 pairs, cols [64,96)) ----
+      // ---- E0.5: row p -> A1 (bf16 pairs, group cols [0,32)) ----
       {
         const float4* row = reinterpret_cast<const float4*>(CL + p * CL_LD);
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
-          uint32_t v[16], a1[8];
+          uint32_t a1[8];
 #pragma unroll
           for (int m = 0; m < 4; ++m) {
             const float4 x = row[h * 4 + m];
-            v[4 * m] = __float_as_uint(x.x);
-            v[4 * m + 1] = __float_as_uint(x.y);
-            v[4 * m + 2] = __float_as_uint(x.z);
-            v[4 * m + 3] = __float_as_uint(x.w);
             a1[2 * m] = pack_bf16(x.x, x.y);
             a1[2 * m + 1] = pack_bf16(x.z, x.w);
           }
-          TMEM_ST16(tm + h * 16, v);
-          TMEM_ST8(tm + 64 + h * 8, a1);
+          TMEM_ST8(tg + h * 8, a1);
         }
         tmem_wait_st();
       }
       tc_fence_before();
-      mbar_arrive(gbar(eg, 2));
-      // ---- E1: h = silu(D1) -> A2 hi/lo in place (cols [128+16ch, +8) hi, [+8, +16) lo) ----
-      mbar_wait(gbar(eg, 3), ph);
+      mbar_arrive(gbar(eg, 1));
+      // ---- E1: h = silu(D1) -> A2 hi/lo in place (cols [64+16ch, +8) hi, [+8, +16) lo) ----
+      mbar_wait(gbar(eg, 2), ph);
       tc_fence_after();
 #pragma unroll
       for (int ch = 0; ch < 8; ++ch) {
         uint32_t v[16];
-        TMEM_LD16(tm + 128 + ch * 16, v);
+        TMEM_LD16(tg + 64 + ch * 16, v);
         tmem_wait_ld();
         uint32_t w[16];
 #pragma unroll
@@ -515,20 +546,20 @@ __global__ void __launch_bounds__(64 + NE * 128, 1) mol_tc_kernel(Params P, cons
           w[m] = hw;
           w[8 + m] = pack_bf16(h0 - __uint_as_float(hw << 16), h1 - __uint_as_float(hw & 0xFFFF0000u));
         }
-        TMEM_ST16(tm + 128 + ch * 16, w);
+        TMEM_ST16(tg + 64 + ch * 16, w);
       }
       tmem_wait_st();
       tc_fence_before();
-      mbar_arrive(gbar(eg, 4));
-      // ---- E2: combine + softmax + gated sum ----
-      mbar_wait(gbar(eg, 5), ph);
+      mbar_arrive(gbar(eg, 3));
+      // ---- E2: combine + softmax + gated sum (logits from CL) ----
+      mbar_wait(gbar(eg, 4), ph);
       tc_fence_after();
       float pre[64];
       float mx = -INFINITY;
 #pragma unroll
       for (int ch = 0; ch < 4; ++ch) {
         uint32_t v[16];
-        TMEM_LD16(tm + 64 + ch * 16, v);
+        TMEM_LD16(tg + ch * 16, v);
         tmem_wait_ld();
 #pragma unroll
         for (int m = 0; m < 16; ++m) {
@@ -542,16 +573,16 @@ __global__ void __launch_bounds__(64 + NE * 128, 1) mol_tc_kernel(Params P, cons
       }
       const float ml = mx * 1.4426950408889634f;
       float sum = 0.f, acc = 0.f;
+      const float4* row = reinterpret_cast<const float4*>(CL + p * CL_LD);
 #pragma unroll
-      for (int ch = 0; ch < 4; ++ch) {
-        uint32_t v[16];
-        TMEM_LD16(tm + ch * 16, v);
-        tmem_wait_ld();
+      for (int m4 = 0; m4 < 16; ++m4) {
+        const float4 c = row[m4];
+        const float cv[4] = {c.x, c.y, c.z, c.w};
 #pragma unroll
-        for (int m = 0; m < 16; ++m) {
-          const float e = ex2(fmaf(pre[ch * 16 + m], 1.4426950408889634f, -ml));
+        for (int i = 0; i < 4; ++i) {
+          const float e = ex2(fmaf(pre[m4 * 4 + i], 1.4426950408889634f, -ml));
           sum += e;
-          acc = fmaf(e, __uint_as_float(v[m]), acc);
+          acc = fmaf(e, cv[i], acc);
         }
       }
       if (p < t.np) {
@@ -560,6 +591,7 @@ __global__ void __launch_bounds__(64 + NE * 128, 1) mol_tc_kernel(Params P, cons
         else P.out[(int64_t)t.b * P.out_ld + t.j0 + p] = s;
       }
       tc_fence_before();
+      named_sync(bar_id, 128);  // CL / UW are rewritten by this group's next tile
       ph ^= 1;
     }
   }
@@ -568,7 +600,25 @@ __global__ void __launch_bounds__(64 + NE * 128, 1) mol_tc_kernel(Params P, cons
   __syncthreads();
   tc_fence_after();
   if (warp == 1) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(NE * TMEM_COLS_PER_GROUP));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
+  }
+}
+
+// B0 operand image per query: 16 rows x 64 bf16, SW128 K-major; rows 0-7 = bf16(u_a),
+// rows 8-15 = bf16(u_a - bf16(u_a)) (the fp32 query split hi + lo)
+__global__ void b0_image_kernel(int B, const float* __restrict__ ue, uint8_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < int64_t(B) * 128; i += (int64_t)gridDim.x * blockDim.x) {
+    const int b = int(i >> 7), r = int(i & 127) >> 3, c = int(i & 7), a = r & 7;
+    const float* u = ue + (int64_t)b * (KX * D) + a * D + c * 8;
+    const float4 v0 = __ldg(reinterpret_cast<const float4*>(u)), v1 = __ldg(reinterpret_cast<const float4*>(u) + 1);
+    const float f[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+    uint32_t w[4];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const uint32_t hw = pack_bf16(f[2 * m], f[2 * m + 1]);
+      w[m] = (r < 8) ? hw : pack_bf16(f[2 * m] - __uint_as_float(hw << 16), f[2 * m + 1] - __uint_as_float(hw & 0xFFFF0000u));
+    }
+    *reinterpret_cast<uint4*>(out + (int64_t)b * 2048 + sw128(r, c)) = make_uint4(w[0], w[1], w[2], w[3]);
   }
 }
 
@@ -593,8 +643,13 @@ int mol_score_tc(molr_ctx* ctx, const molr_cache* c, const molr_gating* g, int B
   MOLR_CUDA(cudaMemcpyAsync(&T, pre.as<int64_t>() + B, 8, cudaMemcpyDeviceToHost, s));
   MOLR_CUDA(cudaStreamSynchronize(s));
   if (T == 0) return MOLR_OK;
+  Scratch b0;
+  MOLR_TRY(b0.alloc(size_t(B) * 2048, s));
+  tc::b0_image_kernel<<<std::min(div_up(int64_t(B) * 128, 256), ctx->num_sms * 8), 256, 0, s>>>(B, ue, b0.as<uint8_t>());
+  MOLR_LAUNCHED(ctx);
   tc::Params P;
   P.B = B;
+  P.b0img = b0.as<uint8_t>();
   P.inv_tau = 1.0f / tau;
   P.embs = c->embs_bf16;
   P.gp = c->gp_bf16;
@@ -612,12 +667,14 @@ int mol_score_tc(molr_ctx* ctx, const molr_cache* c, const molr_gating* g, int B
   {
     const char* e = getenv("MOLR_E1");
     P.e1_tanh = (e && e[0] == 'a') ? 0 : 1;
+    const char* gm = getenv("MOLR_GATHER");
+    P.gather4 = (c->embs_tmap_ok && !(gm && gm[0] == 'b')) ? 1 : 0;
   }
   auto kern = tc::mol_tc_kernel<Id>;
   const int smem = tc::SMEM_BYTES;
   MOLR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const int grid = (int)std::min<int64_t>(T, ctx->num_sms);
-  kern<<<grid, 64 + tc::NE * 128, smem, s>>>(P, segs.ids);
+  kern<<<grid, 64 + tc::NE * 128, smem, s>>>(P, segs.ids, c->embs_tmap);
   MOLR_LAUNCHED(ctx);
   return MOLR_OK;
 }

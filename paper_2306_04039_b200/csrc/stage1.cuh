@@ -19,6 +19,7 @@ int s1_tc_scan(molr_ctx* ctx, int mode, const int8_t* codes, const float* scales
                const int8_t* qcodes, const uint32_t* tkeys, int strict, int64_t cap, int32_t* cand, int64_t* counts,
                void* out, int64_t ld, cudaStream_t s, bool emit_keys = false);
 // chunk (min, max) scale reciprocals of 32-row chunks [c0, c1) of a scale vector (filter bound)
+int encode_rows_tmap(CUtensorMap* tm, const void* base, int64_t rows);
 int chunk_minmax(molr_ctx* ctx, const float* scales, int64_t c0, int64_t c1, float2* mm, cudaStream_t s);
 int s1_update_chunk_mm(molr_cache* c, int64_t row0, int64_t n, cudaStream_t s);
 int s1_seal(molr_cache* c, cudaStream_t s);

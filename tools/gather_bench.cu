@@ -5,6 +5,7 @@
 #include <cstdint>
 #include <vector>
 #include <random>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -74,6 +75,44 @@ __global__ void gather(const uint4* __restrict__ src, const int* __restrict__ id
   if (acc == 12345) sink[0] = acc;
 }
 
+// gather4: one cp.async.bulk.tensor.2d ... tile::gather4 per 4 items (4 KB) — a quarter of the
+// TMA requests of mode 0
+template <int DEPTH>
+__global__ void gather4_kernel(const __grid_constant__ CUtensorMap tmap, const int* __restrict__ idx, int n_per_cta, int* sink) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ __align__(8) uint64_t bar[DEPTH];
+  const int t = threadIdx.x;
+  if (t < DEPTH) asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&bar[t])), "r"(1));
+  __syncthreads();
+  const int* my = idx + (int64_t)blockIdx.x * n_per_cta;
+  if (t < 32) {
+    uint32_t ph[DEPTH] = {0};
+    for (int base = 0, st = 0; base < n_per_cta; base += 16, st = (st + 1) % DEPTH) {
+      if (base >= 16 * DEPTH) {
+        asm volatile("{.reg .pred P1; W: mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1; @!P1 bra W;}" ::"r"(smem_u32(&bar[st])), "r"(ph[st]));
+        ph[st] ^= 1;
+      }
+      if (t == 0) asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar[st])), "r"(16 * 1024));
+      __syncwarp();
+      if (t < 4) {
+        const int* r = my + base + 4 * t;
+        asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];"
+                     ::"r"(smem_u32(sm + st * 16384 + t * 4096)), "l"(&tmap), "r"(0), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]),
+                       "r"(smem_u32(&bar[st])) : "memory");
+      }
+      __syncwarp();
+    }
+    for (int st = 0; st < DEPTH; ++st)
+      asm volatile("{.reg .pred P1; W2: mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1; @!P1 bra W2;}" ::"r"(smem_u32(&bar[st])), "r"(ph[st]));
+  }
+  __syncthreads();
+  if (sm[t] == 123) sink[0] = 1;
+}
+
+typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                             const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                             CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
 int main() {
   const int64_t X = 10'000'000;
   uint4* src;
@@ -118,6 +157,42 @@ int main() {
     run(gather<1, 8>, 512, 8 * 16384, "cp.async16 512thr depth8");
     run(gather<2, 1>, 256, 4 * 16384, "ldg128 256thr 16/thr");
     run(gather<2, 2>, 256, 4 * 16384, "ldg128 256thr 32/thr");
+    {
+      EncodeFn enc = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&enc, cudaEnableDefault, &q);
+      CUtensorMap tm;
+      cuuint64_t dims[2] = {256, (cuuint64_t)X};
+      cuuint64_t strides[1] = {1024};
+      cuuint32_t box[2] = {256, 1};
+      cuuint32_t es[2] = {1, 1};
+      for (int prom = 0; prom < 2; ++prom) {
+        CUresult r = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, src, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_NONE, prom ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B : CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) { printf("encode failed %d\n", (int)r); continue; }
+        auto k4 = gather4_kernel<4>;
+        auto k8 = gather4_kernel<8>;
+        auto runt = [&](auto kern, int smem, const char* name) {
+          cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+          cudaEvent_t a, b;
+          cudaEventCreate(&a);
+          cudaEventCreate(&b);
+          kern<<<ctas, 32, smem>>>(tm, idx, n_per, sink);
+          cudaEventRecord(a);
+          for (int r2 = 0; r2 < 3; ++r2) kern<<<ctas, 32, smem>>>(tm, idx, n_per, sink);
+          cudaEventRecord(b);
+          cudaEventSynchronize(b);
+          float ms;
+          cudaEventElapsedTime(&ms, a, b);
+          double bytes = 3.0 * ctas * n_per * 1024.0;
+          printf("%s %-28s %7.1f GB/s  (%s)\n", pass ? "local " : "random", name, bytes / ms / 1e6,
+                 cudaGetErrorString(cudaGetLastError()));
+        };
+        runt(k4, 4 * 16384, prom ? "gather4 depth4 l2prom256" : "gather4 depth4");
+        runt(k8, 8 * 16384, prom ? "gather4 depth8 l2prom256" : "gather4 depth8");
+      }
+    }
     cudaFree(idx);
   }
   return 0;
