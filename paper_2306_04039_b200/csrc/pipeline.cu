@@ -284,8 +284,11 @@ int molr_score(molr_ctx* ctx, const molr_cache* c, const molr_gating* g, int B, 
   }
   Out o;
   MOLR_TRY(o.stage(out, size_t(total) * 4, s));
-  MOLR_TRY(mol_score_any<int64_t>(ctx, c, g, B, k_u, iue.as<float>(), iuw.as<float>(), tau, segs, o.as<float>(),
-                                  c->X, s));
+  {
+    KTimer t(ctx, "mol_score", s, double(total));
+    MOLR_TRY(mol_score_any<int64_t>(ctx, c, g, B, k_u, iue.as<float>(), iuw.as<float>(), tau, segs, o.as<float>(),
+                                    c->X, s));
+  }
   return finish_outputs(s, {&o});
 }
 
@@ -332,7 +335,10 @@ int molr_mol_top_k(molr_ctx* ctx, const molr_cache* c, const molr_gating* g, int
   Out oi, os;
   MOLR_TRY(oi.stage(out_ids, size_t(B) * k * 8, s));
   MOLR_TRY(os.stage(out_scores, size_t(B) * k * 4, s));
-  MOLR_TRY(segmented_top_k<int64_t>(ctx, B, segs, sc.as<float>(), c->X, k, 0, oi.as<int64_t>(), os.as<float>(), s));
+  {
+    KTimer t(ctx, "topk_segmented", s, double(total));
+    MOLR_TRY(segmented_top_k<int64_t>(ctx, B, segs, sc.as<float>(), c->X, k, 0, oi.as<int64_t>(), os.as<float>(), s));
+  }
   return finish_outputs(s, {&oi, &os});
 }
 
