@@ -2,12 +2,14 @@
 """MoL + h-indexer top-100 retrieval benchmark (BASELINE.json metric: queries/sec over a 100M-item
 synthetic corpus, p50 latency, recall vs the exact MoL top-k).
 
-One step = one batch of B=1024 queries through the whole hot path on every rank: user_net MLP ->
+One step = one batch of B=1024 queries (raw user features) through the whole path on every rank:
+device query prep (user_proj MLP + L2 norm -> user components, user_net -> gating weights) ->
 stage-1 query + int8 quantisation -> sampled threshold -> full-corpus int8 scan + filter ->
 MoL re-scoring of the passers -> top-100 -> (N>1) NCCL all-gather of (score, id) + merge.
 The corpus (100M items, k_x=8 x d=64 bf16 item embeddings, bf16 gate pre-activations, int8
 stage-1 rows) is sharded across ranks by contiguous item ranges; it is built on the device from a
-seeded synthetic model with the reference's init convention (model.py:121-163).
+seeded synthetic model with the reference's init convention (model.py:121-163) by the product's
+fused device cache build (molr_cache_build_rows).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config 100m|10m|books|ml20m] [--impl reference]
 
@@ -82,26 +84,21 @@ def synthetic_model(seed=4242):
             "user_net": _mlp(rng, D_U, H, G), "item_net": _mlp(rng, D_X, H, G), "cross_net": _mlp(rng, G, H, G)}
 
 
-def _round_bf16_t(x):
-    import torch
-
-    return x.to(torch.bfloat16).to(torch.float32)
-
-
 def build_shard(model, X, lo, hi, seed, dev, lib, ctx):
-    """Build rows [lo, hi) of the global corpus on the device into a DeviceItemCache."""
+    """Build rows [lo, hi) of the global corpus on the device into a DeviceItemCache through the
+    product's fused cache build (molr_cache_build_rows: item_proj MLP -> L2 norm -> item_net ->
+    bf16 storage rounding -> stage-1 mean -> int8), from a synthetic item table drawn on the
+    device chunk by chunk (same global rows for every N)."""
     import torch
 
     from paper_2306_04039_b200 import _lib as L
     from paper_2306_04039_b200.mol import DeviceItemCache, MoLConfig
+    from paper_2306_04039_b200.numerics import DEFAULT_EPS
 
     cfg = MoLConfig(k_u=K_U, k_x=K_X, d=D, tau=TAU, gating_hidden=H, dropout_p=0.0)
     cache = DeviceItemCache(cfg, hi - lo, D, L.STORE_S1_INT8)
     W = {k: [torch.from_numpy(a).to(dev) for a in v] for k, v in model.items()}
-
-    def mlp(w, x):
-        return torch.nn.functional.silu(x @ w[0] + w[1]) @ w[2]
-
+    pw, nw = W["item_proj"], W["item_net"]
     s = torch.cuda.current_stream().cuda_stream
     with torch.no_grad():
         for ci in range(lo // CHUNK, (hi + CHUNK - 1) // CHUNK):
@@ -110,30 +107,21 @@ def build_shard(model, X, lo, hi, seed, dev, lib, ctx):
             gen.manual_seed(seed * 1_000_003 + ci)
             t = (torch.rand((g1 - g0, D_X), generator=gen, device=dev) * 2 - 1) / math.sqrt(D_X)
             c0, c1 = max(lo, g0), min(hi, g1)
-            t = t[c0 - g0:c1 - g0]
-            n = c1 - c0
-            e = mlp(W["item_proj"], t).view(n, K_X, D)
-            e = _round_bf16_t(e / e.norm(dim=-1, keepdim=True))
-            gp = _round_bf16_t(mlp(W["item_net"], t))
-            s1 = e.mean(dim=1).contiguous()
-            codes = torch.empty((n, D), dtype=torch.int8, device=dev)
-            scales = torch.empty((n,), dtype=torch.float32, device=dev)
-            L.call("molr_quantize_rows", ctx, n, D, s1.data_ptr(), codes.data_ptr(), scales.data_ptr(), s)
-            cache.fill(c0 - lo, n, e.contiguous(), gp.contiguous(), None, codes, scales, stream=s)
+            t = t[c0 - g0:c1 - g0].contiguous()
+            L.call("molr_cache_build_rows", cache.device_handle(), c0 - lo, c1 - c0, D_X, t.data_ptr(), PROJ_H,
+                   pw[0].data_ptr(), pw[1].data_ptr(), pw[2].data_ptr(), H, nw[0].data_ptr(), nw[1].data_ptr(),
+                   nw[2].data_ptr(), L.BUILD_L2_NORMALIZE | L.BUILD_ROUND_BF16, float(DEFAULT_EPS), s)
     torch.cuda.synchronize()
     return cfg, cache
 
 
 def make_queries(model, B, seed, dev):
+    """B users' raw features (the user_table rows of the reference convention, U(+-1/sqrt(d_u)))."""
     import torch
 
     rng = np.random.Generator(np.random.Philox(np.random.SeedSequence([seed, 7])))
     feats = (rng.uniform(-1, 1, (B, D_U)) / math.sqrt(D_U)).astype(np.float32)
-    w = model["user_proj"]
-    h = feats @ w[0] + w[1]
-    ue = ((h / (1 + np.exp(-h))) @ w[2]).reshape(B, K_U, D)
-    ue = (ue / np.linalg.norm(ue, axis=-1, keepdims=True)).astype(np.float32)
-    return feats, ue, torch.from_numpy(feats).to(dev), torch.from_numpy(ue).to(dev)
+    return feats, torch.from_numpy(feats).to(dev)
 
 
 # ------------------------------------------------------------------------------------------
@@ -367,8 +355,11 @@ def main():
     t_build = time.perf_counter() - t_build
     gating = GatingNetwork(Mlp(*model["user_net"]), Mlp(*model["item_net"]), Mlp(*model["cross_net"]))
     gh = _gating_handle(gating)
-    feats_h, ue_h, feats_d, ue_d = make_queries(model, B, 1, dev)
+    feats_h, feats_d = make_queries(model, B, 1, dev)
     uw1, ub1, uw2 = [torch.from_numpy(a).to(dev) for a in model["user_net"]]
+    up1, upb1, up2 = [torch.from_numpy(a).to(dev) for a in model["user_proj"]]
+    ue_d = torch.empty((B, K_U, D), dtype=torch.float32, device=dev)
+    from paper_2306_04039_b200.numerics import DEFAULT_EPS
     uw_d = torch.empty((B, G), dtype=torch.float32, device=dev)
     ids_d = torch.empty((B, k), dtype=torch.int64, device=dev)
     sc_d = torch.empty((B, k), dtype=torch.float32, device=dev)
@@ -380,12 +371,16 @@ def main():
     stream = torch.cuda.current_stream()
     sp = stream.cuda_stream
 
-    def step(i, ue_ptr, feats_ptr, host_out=None):
-        """One batch through the C-ABI.  ue_ptr / feats_ptr may be device or (pinned) host pointers;
-        with host_out=(ids, scores) host tensors the final top-k lands there (the C-ABI stages the
-        H2D / D2H copies on the call's stream)."""
-        L.call("molr_mlp_forward", ctx, B, D_U, H, G, uw1.data_ptr(), ub1.data_ptr(), uw2.data_ptr(), feats_ptr,
+    def step(i, feats_ptr, host_out=None):
+        """One batch through the C-ABI, from the users' raw features (the query a user makes,
+        engine.py:117): device query prep (user_proj + L2 norm -> user components, user_net ->
+        uw) then the two-stage retrieval.  feats_ptr may be a device or (pinned) host pointer;
+        with host_out=(ids, scores) host tensors the final top-k lands there (the C-ABI stages
+        the H2D / D2H copies on the call's stream)."""
+        L.call("molr_query_prep", ctx, B, D_U, feats_ptr, PROJ_H, up1.data_ptr(), upb1.data_ptr(), up2.data_ptr(), K_U,
+               D, 1, H, uw1.data_ptr(), ub1.data_ptr(), uw2.data_ptr(), G, float(DEFAULT_EPS), ue_d.data_ptr(),
                uw_d.data_ptr(), sp)
+        ue_ptr = ue_d.data_ptr()
         last = world == 1 and host_out is not None
         oi = host_out[0].data_ptr() if last else ids_d.data_ptr()
         osc = host_out[1].data_ptr() if last else sc_d.data_ptr()
@@ -415,7 +410,7 @@ def main():
     prof_range = os.environ.get("MOLR_PROFILE_RANGE") == "1"  # ncu --profile-from-start off
     with Clocks(local) as clk:  # sampling starts before the warm-up (nvidia-smi start-up stalls the GPU)
         for i in range(args.warmup):
-            step(i, ue_d.data_ptr(), feats_d.data_ptr())
+            step(i, feats_d.data_ptr())
         barrier()
         L.prof_reset(local)
         L.set_profiling(True, local)
@@ -430,7 +425,7 @@ def main():
         host_ms = []
         for i in range(args.steps):
             t_host = time.perf_counter()
-            step(args.warmup + i, ue_d.data_ptr(), feats_d.data_ptr())
+            step(args.warmup + i, feats_d.data_ptr())
             evs[i + 1].record(stream)
             host_ms.append(round(1e3 * (time.perf_counter() - t_host), 2))
             if trace:
@@ -457,19 +452,18 @@ def main():
 
     # ---------------- end-to-end through the public API with host buffers (e2e) ----------------
     feats_pin = torch.from_numpy(feats_h).pin_memory()
-    ue_pin = torch.from_numpy(ue_h).pin_memory()
     host_ids = torch.empty((B, k), dtype=torch.int64).pin_memory()
     host_sc = torch.empty((B, k), dtype=torch.float32).pin_memory()
     # inputs: the step's query features and user components from pinned host memory, passed to the
     # C-ABI as host pointers (copied H2D inside the call); outputs: the top-k ids/scores written to
     # pinned host memory (D2H inside the call)
     for i in range(2):
-        step(i, ue_pin.data_ptr(), feats_pin.data_ptr(), (host_ids, host_sc))
+        step(i, feats_pin.data_ptr(), (host_ids, host_sc))
     barrier()
     eev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     eev[0].record(stream)
     for i in range(args.steps):
-        step(args.warmup + i, ue_pin.data_ptr(), feats_pin.data_ptr(), (host_ids, host_sc))
+        step(args.warmup + i, feats_pin.data_ptr(), (host_ids, host_sc))
         eev[i + 1].record(stream)
     barrier()
     e2e_ms = eev[0].elapsed_time(eev[-1])
@@ -479,7 +473,7 @@ def main():
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_ms = float(tt.item())
     e2e_value = B * args.steps / (e2e_ms / 1e3)
-    h2d = feats_h.nbytes + ue_h.nbytes
+    h2d = feats_h.nbytes
     d2h = B * k * (8 + 4)
 
     # ---------------- single-query latency (B = 1) ----------------
@@ -488,8 +482,9 @@ def main():
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record(stream)
-        L.call("molr_mlp_forward", ctx, 1, D_U, H, G, uw1.data_ptr(), ub1.data_ptr(), uw2.data_ptr(),
-               feats_d.data_ptr(), uw_d.data_ptr(), sp)
+        L.call("molr_query_prep", ctx, 1, D_U, feats_d.data_ptr(), PROJ_H, up1.data_ptr(), upb1.data_ptr(),
+               up2.data_ptr(), K_U, D, 1, H, uw1.data_ptr(), ub1.data_ptr(), uw2.data_ptr(), G, float(DEFAULT_EPS),
+               ue_d.data_ptr(), uw_d.data_ptr(), sp)
         if exact:
             L.call("molr_mol_top_k", ctx, cache.device_handle(), gh, 1, K_U, ue_d.data_ptr(), uw_d.data_ptr(), TAU,
                    None, None, k, ids_d.data_ptr(), sc_d.data_ptr(), sp)
@@ -503,7 +498,7 @@ def main():
 
     # ---------------- recall vs the exact MoL top-k (GPU exact path, parity-tested vs the oracle) ----
     R = min(args.recall_queries, B)
-    res_i, _ = step(0, ue_d.data_ptr(), feats_d.data_ptr())
+    res_i, _ = step(0, feats_d.data_ptr())
     two = res_i[:R].cpu().numpy()
     ex_i = torch.empty((R, k), dtype=torch.int64, device=dev)
     ex_s = torch.empty((R, k), dtype=torch.float32, device=dev)

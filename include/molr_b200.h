@@ -99,12 +99,33 @@ int molr_cache_fill(molr_cache* cache, int64_t row0, int64_t n, const float* ite
                     const float* item_gate_pre, const float* stage1_embs,
                     const int8_t* stage1_codes, const float* stage1_scales, void* stream);
 int molr_cache_destroy(molr_cache* cache);
+/* Device-side build_item_cache (mol.py:294-326) for rows [row0, row0+n): item_table (n, d_x) ->
+ * item_proj MLP (d_x -> proj_hidden -> k_x*d) -> per-component L2 normalisation (numerics.py:41-50,
+ * ZERO_NORM if a norm <= eps) -> item_net MLP (d_x -> net_hidden -> G) -> stage-1 = mean over the
+ * k_x components -> rowwise int8 (quant.py:49-57) when the cache has an int8 view -> cache rows.
+ * flags: MOLR_BUILD_L2_NORMALIZE (MoLConfig.l2_normalized), MOLR_BUILD_ROUND_BF16 (round the item
+ * components and gate pre-activations to bf16 before the stage-1 mean: the production bf16 cache).
+ * Weights and table may be host or device pointers.  Replaces mol.py:294-326 for device corpora. */
+enum { MOLR_BUILD_L2_NORMALIZE = 1, MOLR_BUILD_ROUND_BF16 = 2 };
+int molr_cache_build_rows(molr_cache* cache, int64_t row0, int64_t n, int d_x, const float* item_table,
+                          int proj_hidden, const float* proj_w1, const float* proj_b1, const float* proj_w2,
+                          int net_hidden, const float* net_w1, const float* net_b1, const float* net_w2,
+                          int flags, float eps, void* stream);
 /* read rows back as f32 (exact: storage is lossless); any output pointer may be NULL */
 int molr_cache_read(const molr_cache* cache, int64_t row0, int64_t n, float* item_embs,
                     float* item_gate_pre, float* stage1_embs, int8_t* stage1_codes,
                     float* stage1_scales, void* stream);
 /* storage: the molr_storage bits the cache was built with */
 int molr_cache_info(const molr_cache* cache, int64_t* n_items, int* storage, int64_t* device_bytes);
+
+/* Batched user-side query prep (engine.py:113-115 -> model.py:179-208 user_forward, and
+ * mol.py:186 user_net): user_embs (B, k_u, d) = per-component L2-normalised user_proj(feats)
+ * (when l2_normalized; ZERO_NORM if a norm <= eps), uw (B, G) = user_net(feats).  Both MLPs are
+ * silu(x W1 + b1) W2 (mol.py:62-85).  Inputs/outputs host or device. */
+int molr_query_prep(molr_ctx* ctx, int B, int d_u, const float* feats, int proj_hidden, const float* proj_w1,
+                    const float* proj_b1, const float* proj_w2, int k_u, int d, int l2_normalized, int net_hidden,
+                    const float* net_w1, const float* net_b1, const float* net_w2, int G, float eps,
+                    float* user_embs, float* uw, void* stream);
 
 /* ---- gating weights (cross_net G->H->G, user_net du->Hu->G) — mol.py:62-109 ---------------- */
 int molr_gating_create(molr_ctx* ctx, int G, int H, const float* cross_w1, const float* cross_b1,

@@ -23,6 +23,7 @@ S1_FLOAT, S1_INT8, S1_INT8_RAW = 0, 1, 2
 INCLUSIVE, STRICT = 0, 1
 STORE_EMBS_F32, STORE_GP_F32, STORE_S1_F32, STORE_S1_INT8 = 1, 2, 4, 8
 DT_F32, DT_I32, DT_F64, DT_I64 = 0, 1, 2, 3
+BUILD_L2_NORMALIZE, BUILD_ROUND_BF16 = 1, 2
 
 P = C.c_void_p
 I = C.c_int
@@ -47,11 +48,13 @@ SIGNATURES = {
     "molr_cache_fill": [P, L, L, P, P, P, P, P, P],
     "molr_cache_read": [P, L, L, P, P, P, P, P, P],
     "molr_cache_destroy": [P],
+    "molr_cache_build_rows": [P, L, L, I, P, I, P, P, P, I, P, P, P, I, F, P],
     "molr_cache_info": [P, P, P, P],
     "molr_gating_create": [P, I, I, P, P, P, I, I, P, P, P, P],
     "molr_gating_destroy": [P],
     "molr_component_logits": [P, I, I, I, I, P, P, D, I, P, P],
     "molr_mlp_forward": [P, I, I, I, I, P, P, P, P, P, P],
+    "molr_query_prep": [P, I, I, P, I, P, P, P, I, I, I, I, P, P, P, I, F, P, P, P],
     "molr_decomposed_gating": [P, P, I, P, P, P, P, P],
     "molr_mol_score": [P, I, I, P, P, I, P, P],
     "molr_score": [P, P, P, I, I, P, P, F, P, P, P, P],

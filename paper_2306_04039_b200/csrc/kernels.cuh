@@ -44,6 +44,10 @@ int nth_largest_rows(molr_ctx* ctx, int B, int64_t n_values, const void* values,
 int nth_largest_keys(molr_ctx* ctx, int B, int64_t cap, const uint32_t* keys, const int64_t* counts, int64_t n,
                      uint32_t* out_keys, int* short_rows, cudaStream_t s);
 
+__global__ void mlp_forward_kernel(int rows, int in_dim, int hidden, int out_dim, const float* __restrict__ w1,
+                                   const float* __restrict__ b1, const float* __restrict__ w2,
+                                   const float* __restrict__ x, float* __restrict__ out);
+
 int quantize_rows(molr_ctx* ctx, int64_t rows, int dim, const float* x, int8_t* codes, float* scales,
                   cudaStream_t s);
 

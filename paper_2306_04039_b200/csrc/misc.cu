@@ -42,6 +42,12 @@ __global__ void l2norm_kernel(int64_t rows, int dim, const float* __restrict__ x
   }
 }
 
+// in-place round-to-nearest-even to bf16 precision (value stays f32)
+__global__ void round_bf16_kernel(float* __restrict__ x, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    x[i] = __bfloat162float(__float2bfloat16_rn(x[i]));
+}
+
 __global__ void mean_mid_kernel(int64_t n, int k, int d, const float* __restrict__ x, float* __restrict__ out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * d; i += (int64_t)gridDim.x * blockDim.x) {
     int64_t r = i / d, c = i % d;
@@ -130,6 +136,129 @@ int molr_mean_rows(molr_ctx* ctx, int64_t n, int k, int d, const float* x, float
   mean_mid_kernel<<<grid_for(ctx, n * d), 256, 0, s>>>(n, k, d, xi.as<float>(), o.as<float>());
   MOLR_LAUNCHED(ctx);
   return finish_outputs(s, {&o});
+}
+
+// Device-side build_item_cache for rows [row0, row0 + n) of a cache (mol.py:294-326), fused and
+// chunked: item_proj MLP -> (k_x, d) -> L2-normalise -> item_net MLP -> [bf16 rounding of the
+// stored fields] -> stage-1 = mean over k_x -> rowwise int8 quantisation -> cache rows.  Only
+// the item table chunk crosses PCIe; every intermediate stays on the device.
+int molr_cache_build_rows(molr_cache* c, int64_t row0, int64_t n, int d_x, const float* item_table, int proj_hidden,
+                          const float* pw1, const float* pb1, const float* pw2, int net_hidden, const float* nw1,
+                          const float* nb1, const float* nw2, int flags, float eps, void* stream) {
+  if (!c) MOLR_FAIL(MOLR_ERR_INVALID, "null cache");
+  if (row0 < 0 || n < 0 || row0 + n > c->X) MOLR_FAIL(MOLR_ERR_OUT_OF_RANGE, "build rows out of range");
+  if (d_x < 1 || proj_hidden < 1 || net_hidden < 1) MOLR_FAIL(MOLR_ERR_DIMENSION, "bad tower dims");
+  if (c->d1 && c->d1 != c->d) MOLR_FAIL(MOLR_ERR_DIMENSION, "stage-1 dim %d != d %d", c->d1, c->d);
+  if (n == 0) return MOLR_OK;
+  molr_ctx* ctx = c->ctx;
+  MOLR_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t s = pick_stream(ctx, stream);
+  const int kd = c->k_x * c->d, G = c->G;
+  if (size_t(d_x + std::max(proj_hidden, net_hidden)) * 4 > 200 * 1024) MOLR_FAIL(MOLR_ERR_DIMENSION, "mlp too wide");
+  In a1, a2, a3, b1, b2, b3;
+  MOLR_TRY(a1.stage(pw1, size_t(d_x) * proj_hidden * 4, s));
+  MOLR_TRY(a2.stage(pb1, size_t(proj_hidden) * 4, s));
+  MOLR_TRY(a3.stage(pw2, size_t(proj_hidden) * kd * 4, s));
+  MOLR_TRY(b1.stage(nw1, size_t(d_x) * net_hidden * 4, s));
+  MOLR_TRY(b2.stage(nb1, size_t(net_hidden) * 4, s));
+  MOLR_TRY(b3.stage(nw2, size_t(net_hidden) * G * 4, s));
+  const int64_t chunk = std::max<int64_t>(1, (int64_t(256) << 20) / (int64_t(kd + G + c->d + d_x) * 4));
+  Scratch bad;
+  MOLR_TRY(bad.alloc(4, s));
+  MOLR_CUDA(cudaMemsetAsync(bad.p, 0, 4, s));
+  for (int64_t r = 0; r < n; r += chunk) {
+    const int m = (int)std::min(chunk, n - r);
+    In xt;
+    MOLR_TRY(xt.stage(item_table + r * d_x, size_t(m) * d_x * 4, s));
+    Scratch e, g, s1, codes, scales;
+    MOLR_TRY(e.alloc(size_t(m) * kd * 4, s));
+    MOLR_TRY(g.alloc(size_t(m) * G * 4, s));
+    MOLR_TRY(s1.alloc(size_t(m) * c->d * 4, s));
+    auto mlp = [&](int hidden, const In& w1, const In& bb, const In& w2, int out_dim, float* out) -> int {
+      const size_t smem = size_t(d_x + hidden) * 4;
+      MOLR_CUDA(cudaFuncSetAttribute(mlp_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      mlp_forward_kernel<<<std::min(m, ctx->num_sms * 8), 128, smem, s>>>(m, d_x, hidden, out_dim, w1.as<float>(),
+                                                                        bb.as<float>(), w2.as<float>(), xt.as<float>(), out);
+      MOLR_LAUNCHED(ctx);
+      return MOLR_OK;
+    };
+    MOLR_TRY(mlp(proj_hidden, a1, a2, a3, kd, e.as<float>()));
+    if (flags & MOLR_BUILD_L2_NORMALIZE) {
+      l2norm_kernel<<<grid_for(ctx, int64_t(m) * c->k_x), 256, 0, s>>>(int64_t(m) * c->k_x, c->d, e.as<float>(), eps,
+                                                                      e.as<float>(), bad.as<int>());
+      MOLR_LAUNCHED(ctx);
+    }
+    MOLR_TRY(mlp(net_hidden, b1, b2, b3, G, g.as<float>()));
+    if (flags & MOLR_BUILD_ROUND_BF16) {  // production storage: the cache IS these bf16 values
+      round_bf16_kernel<<<grid_for(ctx, int64_t(m) * kd), 256, 0, s>>>(e.as<float>(), int64_t(m) * kd);
+      round_bf16_kernel<<<grid_for(ctx, int64_t(m) * G), 256, 0, s>>>(g.as<float>(), int64_t(m) * G);
+      ctx->launches += 2;
+    }
+    mean_mid_kernel<<<grid_for(ctx, int64_t(m) * c->d), 256, 0, s>>>(m, c->k_x, c->d, e.as<float>(), s1.as<float>());
+    MOLR_LAUNCHED(ctx);
+    if (c->s1_codes) {
+      MOLR_TRY(codes.alloc(size_t(m) * c->d, s));
+      MOLR_TRY(scales.alloc(size_t(m) * 4, s));
+      MOLR_TRY(quantize_rows(ctx, m, c->d, s1.as<float>(), codes.as<int8_t>(), scales.as<float>(), s));
+    }
+    int hb = 0;
+    MOLR_CUDA(cudaMemcpyAsync(&hb, bad.p, 4, cudaMemcpyDeviceToHost, s));
+    MOLR_CUDA(cudaStreamSynchronize(s));
+    if (hb) MOLR_FAIL(MOLR_ERR_ZERO_NORM, "at least one item component has norm <= eps");
+    MOLR_TRY(molr_cache_fill(c, row0 + r, m, e.as<float>(), g.as<float>(), c->s1_f32 ? s1.as<float>() : nullptr,
+                             codes.as<int8_t>(), scales.as<float>(), s));
+  }
+  return MOLR_OK;
+}
+
+// Batched user-side query prep (RetrievalEngine.query_state -> model.user_forward,
+// engine.py:113-115, model.py:179-208; and decomposed_gating's user_net, mol.py:186):
+// user_embs = L2-normalise(user_proj(feats).reshape(k_u, d)) and uw = user_net(feats), on device.
+int molr_query_prep(molr_ctx* ctx, int B, int d_u, const float* feats, int proj_hidden, const float* pw1,
+                    const float* pb1, const float* pw2, int k_u, int d, int l2_normalized, int net_hidden,
+                    const float* nw1, const float* nb1, const float* nw2, int G, float eps, float* user_embs, float* uw,
+                    void* stream) {
+  if (!ctx) MOLR_FAIL(MOLR_ERR_INVALID, "null ctx");
+  if (B < 0 || d_u < 1 || proj_hidden < 1 || net_hidden < 1 || k_u < 1 || d < 1 || G < 1)
+    MOLR_FAIL(MOLR_ERR_DIMENSION, "bad query-prep dims");
+  if (size_t(d_u + std::max(proj_hidden, net_hidden)) * 4 > 200 * 1024) MOLR_FAIL(MOLR_ERR_DIMENSION, "mlp too wide");
+  MOLR_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t s = pick_stream(ctx, stream);
+  if (B == 0) return MOLR_OK;
+  In x, a1, a2, a3, b1, b2, b3;
+  MOLR_TRY(x.stage(feats, size_t(B) * d_u * 4, s));
+  MOLR_TRY(a1.stage(pw1, size_t(d_u) * proj_hidden * 4, s));
+  MOLR_TRY(a2.stage(pb1, size_t(proj_hidden) * 4, s));
+  MOLR_TRY(a3.stage(pw2, size_t(proj_hidden) * k_u * d * 4, s));
+  MOLR_TRY(b1.stage(nw1, size_t(d_u) * net_hidden * 4, s));
+  MOLR_TRY(b2.stage(nb1, size_t(net_hidden) * 4, s));
+  MOLR_TRY(b3.stage(nw2, size_t(net_hidden) * G * 4, s));
+  Out oe, ow;
+  MOLR_TRY(oe.stage(user_embs, size_t(B) * k_u * d * 4, s));
+  MOLR_TRY(ow.stage(uw, size_t(B) * G * 4, s));
+  auto mlp = [&](int hidden, const In& w1, const In& bb, const In& w2, int out_dim, float* out) -> int {
+    const size_t smem = size_t(d_u + hidden) * 4;
+    MOLR_CUDA(cudaFuncSetAttribute(mlp_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    mlp_forward_kernel<<<std::min(B, ctx->num_sms * 8), 128, smem, s>>>(B, d_u, hidden, out_dim, w1.as<float>(),
+                                                                      bb.as<float>(), w2.as<float>(), x.as<float>(), out);
+    MOLR_LAUNCHED(ctx);
+    return MOLR_OK;
+  };
+  MOLR_TRY(mlp(proj_hidden, a1, a2, a3, k_u * d, oe.as<float>()));
+  MOLR_TRY(mlp(net_hidden, b1, b2, b3, G, ow.as<float>()));
+  Scratch bad;
+  if (l2_normalized) {
+    MOLR_TRY(bad.alloc(4, s));
+    MOLR_CUDA(cudaMemsetAsync(bad.p, 0, 4, s));
+    l2norm_kernel<<<grid_for(ctx, int64_t(B) * k_u), 256, 0, s>>>(int64_t(B) * k_u, d, oe.as<float>(), eps, oe.as<float>(),
+                                                                bad.as<int>());
+    MOLR_LAUNCHED(ctx);
+    int hb = 0;
+    MOLR_CUDA(cudaMemcpyAsync(&hb, bad.p, 4, cudaMemcpyDeviceToHost, s));
+    MOLR_CUDA(cudaStreamSynchronize(s));
+    if (hb) MOLR_FAIL(MOLR_ERR_ZERO_NORM, "a user component has norm <= eps");
+  }
+  return finish_outputs(s, {&oe, &ow});
 }
 
 int molr_dequantize_rows(molr_ctx* ctx, int64_t rows, int dim, const int8_t* codes, const float* scales, float* out,

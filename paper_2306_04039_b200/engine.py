@@ -44,14 +44,40 @@ def two_stage_top_k(cache, gating: GatingNetwork, user_embs, uw, k: int, hconfig
     return out_ids, out_scores, out_cand
 
 
-class BatchedRetrievalEngine:
-    """Immutable cache + gating + h-indexer config; any number of threads may query it."""
+def query_prep(user_proj, user_net, user_feats, config, *, stream=None, out_embs=None, out_uw=None):
+    """Batched user-side query state on the device (molr_query_prep): user_embs (B, k_u, d) =
+    user_components (model.py:179-191: user_proj MLP, per-component L2 norm) and uw (B, G) =
+    user_net(features) (mol.py:186).  Host arrays in -> host arrays out, or device tensors."""
+    from paper_2306_04039_b200.numerics import DEFAULT_EPS
 
-    def __init__(self, cache, gating: GatingNetwork, hconfig: HIndexerConfig, seed: int = 0):
+    feats = user_feats
+    host = isinstance(feats, np.ndarray) or not hasattr(feats, "data_ptr")
+    if host:
+        feats = L.f32(np.asarray(feats))
+    B, d_u = int(feats.shape[0]), int(feats.shape[1])
+    if user_proj.in_dim != d_u or user_net.in_dim != d_u:
+        raise ValueError("tower input dims do not match the user features")
+    G = config.num_logits
+    if out_embs is None:
+        out_embs = np.empty((B, config.k_u, config.d), np.float32)
+        out_uw = np.empty((B, G), np.float32)
+    w = [L.f32(a) for a in (user_proj.w1, user_proj.b1, user_proj.w2, user_net.w1, user_net.b1, user_net.w2)]
+    L.call("molr_query_prep", L.ctx(), B, d_u, L.ptr(feats), w[0].shape[1], L.ptr(w[0]), L.ptr(w[1]), L.ptr(w[2]),
+           config.k_u, config.d, int(config.l2_normalized), w[3].shape[1], L.ptr(w[3]), L.ptr(w[4]), L.ptr(w[5]), G,
+           float(DEFAULT_EPS), L.ptr(out_embs), L.ptr(out_uw), L.ptr(stream))
+    return out_embs, out_uw
+
+
+class BatchedRetrievalEngine:
+    """Immutable cache + gating + h-indexer config (+ the user tower for raw-feature queries);
+    any number of threads may query it (RetrievalEngine, engine.py:80-147, batched)."""
+
+    def __init__(self, cache, gating: GatingNetwork, hconfig: HIndexerConfig, seed: int = 0, user_proj=None):
         self.cache = cache
         self.gating = gating
         self.hconfig = hconfig
         self.seed = seed
+        self.user_proj = user_proj
 
     @property
     def num_items(self) -> int:
@@ -65,6 +91,17 @@ class BatchedRetrievalEngine:
         ids, sc, cand = two_stage_top_k(self.cache, self.gating, user_embs, uw, k, h,
                                         seed=self.seed if seed is None else seed)
         return ids, sc, cand
+
+    def query_features(self, user_feats, k: int, k_prime: int | None = None, seed: int | None = None):
+        """The whole query path from raw user features (RetrievalEngine.query, engine.py:117-138,
+        for a batch): device query prep -> two-stage top-k.  Needs `user_proj`."""
+        from dataclasses import replace
+
+        if self.user_proj is None:
+            raise ValueError("engine built without the user tower (user_proj)")
+        h = self.hconfig if k_prime is None else replace(self.hconfig, k_prime=k_prime)
+        ue, uw = query_prep(self.user_proj, self.gating.user_net, user_feats, self.cache.config)
+        return two_stage_top_k(self.cache, self.gating, ue, uw, k, h, seed=self.seed if seed is None else seed)
 
     def full_top_k_batch(self, user_embs, user_feats, k: int):
         from paper_2306_04039_b200.mol import batch_mol_top_k
@@ -82,3 +119,32 @@ def merge_top_k(ids, scores, k: int):
     L.call("molr_merge_top_k", L.ctx(), P, B, k_in, L.ptr(ids), L.ptr(scores), int(k), L.ptr(out_i), L.ptr(out_s),
            None)
     return out_i, out_s
+
+
+def bench_csv(engine: BatchedRetrievalEngine, user_embs, user_feats, k: int, k_primes, *, repeats: int = 1):
+    """`molr bench` (cli.py:229-281) on the batched device path: the exact top-k per user first
+    (untimed), then for every K' in the grid the two-stage top-k of the whole batch, timed; one
+    CSV row per K' with the mean recall@k vs exact and queries/s.  Header `k_prime,recall,qps`
+    (the contract pinned by test_cli.py:128-137)."""
+    import time
+
+    from paper_2306_04039_b200.mol import batch_mol_top_k
+
+    X = engine.num_items
+    k_eff = min(k, X)
+    exact_ids, _ = batch_mol_top_k(engine.cache, engine.gating, user_embs, user_feats, k_eff)
+    uw = engine.gating.user_net(np.asarray(user_feats))
+    lines = ["k_prime,recall,qps"]
+    B = len(user_embs)
+    for kp in k_primes:
+        from dataclasses import replace
+
+        h = replace(engine.hconfig, k_prime=int(kp))
+        ids, _, _ = two_stage_top_k(engine.cache, engine.gating, user_embs, uw, k_eff, h, seed=engine.seed)  # warm
+        t0 = time.perf_counter()
+        for _ in range(repeats):
+            ids, _, _ = two_stage_top_k(engine.cache, engine.gating, user_embs, uw, k_eff, h, seed=engine.seed)
+        dt = (time.perf_counter() - t0) / repeats
+        rec = float(np.mean([len(set(ids[b].tolist()) & set(exact_ids[b].tolist())) / k_eff for b in range(B)]))
+        lines.append(f"{int(kp)},{rec:.4f},{B / dt:.1f}")
+    return "\n".join(lines) + "\n"

@@ -253,6 +253,19 @@ class ItemCache:
     def stage1_dim(self) -> int:
         return self.stage1_embs.shape[1]
 
+    def save(self, path) -> None:
+        """MOLC container, byte-compatible with the reference's ItemCache.save (mol.py:253-273)."""
+        from paper_2306_04039_b200 import snapshot
+
+        snapshot.save_item_cache(self, path)
+
+    @classmethod
+    def load(cls, path) -> "ItemCache":
+        """ItemCache.load (mol.py:275-291)."""
+        from paper_2306_04039_b200 import snapshot
+
+        return snapshot.load_item_cache(path)
+
     def device_handle(self) -> int:
         """molr_cache* of this snapshot (uploaded on first use)."""
         if self._dev is None:
@@ -333,6 +346,44 @@ def build_item_cache(item_table, item_proj: Mlp, item_net: Mlp, config: MoLConfi
     L.call("molr_mean_rows", L.ctx(), n, config.k_x, config.d, L.ptr(e32), L.ptr(stage1), None)
     q = quantize_rowwise(stage1) if quantized else None
     return ItemCache(config=config, item_embs=e32, item_gate_pre=L.f32(gate_pre), stage1_embs=stage1, stage1_q=q)
+
+
+def build_device_item_cache(item_table, item_proj: Mlp, item_net: Mlp, config: MoLConfig, *, quantized: bool = True,
+                            round_bf16: bool = False, keep_stage1_f32: bool = True, chunk_rows: int = 1 << 20,
+                            stream=None) -> DeviceItemCache:
+    """build_item_cache (mol.py:294-326) straight into device memory, for corpora whose f32 host
+    image would not fit (100M items = 256 GB): the item table streams in by chunks of
+    `chunk_rows` and every derived tensor is produced on the GPU (molr_cache_build_rows).
+
+    round_bf16=False keeps item_embs / item_gate_pre in f32 storage (exactly the reference's
+    cache, served by the generic kernels); round_bf16=True rounds them to bf16 first and builds
+    the stage-1 mean and int8 view from the rounded values — the production cache the tcgen05
+    kernels read (1,220 B per item), equal to the reference's cache built from the same rounded
+    embeddings."""
+    item_table = np.asarray(item_table) if not hasattr(item_table, "data_ptr") else item_table
+    n = int(item_table.shape[0])
+    if len(item_table.shape) != 2 or n == 0:
+        raise EmptyCorpusError(f"item table must be nonempty 2-D, got {tuple(item_table.shape)}")
+    d_x = int(item_table.shape[1])
+    if item_proj.in_dim != d_x or item_net.in_dim != d_x:
+        raise DimensionMismatchError("tower input dims do not match the item table")
+    if item_proj.out_dim != config.k_x * config.d or item_net.out_dim != config.num_logits:
+        raise DimensionMismatchError("tower output dims do not match the MoL config")
+    storage = (0 if round_bf16 else (L.STORE_EMBS_F32 | L.STORE_GP_F32)) | (L.STORE_S1_F32 if keep_stage1_f32 else 0) | (
+        L.STORE_S1_INT8 if quantized else 0)
+    dev = DeviceItemCache(config, n, config.d, storage)
+    w = [L.f32(a) for a in (item_proj.w1, item_proj.b1, item_proj.w2, item_net.w1, item_net.b1, item_net.w2)]
+    flags = (L.BUILD_L2_NORMALIZE if config.l2_normalized else 0) | (L.BUILD_ROUND_BF16 if round_bf16 else 0)
+    table = L.f32(item_table) if isinstance(item_table, np.ndarray) else item_table
+    from paper_2306_04039_b200.numerics import DEFAULT_EPS
+
+    for r in range(0, n, chunk_rows):
+        m = min(chunk_rows, n - r)
+        ptr = table[r:r + m] if isinstance(table, np.ndarray) else table[r:r + m].contiguous()
+        L.call("molr_cache_build_rows", dev.device_handle(), r, m, d_x, L.ptr(ptr), w[0].shape[1], L.ptr(w[0]),
+               L.ptr(w[1]), L.ptr(w[2]), w[3].shape[1], L.ptr(w[3]), L.ptr(w[4]), L.ptr(w[5]), flags,
+               float(DEFAULT_EPS), L.ptr(stream))
+    return dev
 
 
 def _validate_candidates(cache, candidate_ids) -> np.ndarray:

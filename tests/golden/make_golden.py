@@ -220,7 +220,49 @@ def engine_case():
     np.savez_compressed(os.path.join(OUT, "engine_small.npz"), **out)
 
 
+def snapshot_case():
+    """ItemCache.save (mol.py:253-273, snapshot.py:86-112) of a small quantized cache, plus the
+    arrays ItemCache.load gives back; and a production-shape build_item_cache (mol.py:294-326)
+    with its inputs, for the device cache-build parity test."""
+    cfg = MoLConfig(k_u=2, k_x=3, d=8, tau=20.0, gating_hidden=16, dropout_p=0.0)
+    dims = TowerDims(n_users=4, n_items=40, d_u=12, d_x=12, proj_hidden=24)
+    params = init_params(dims, cfg, make_rng(7))
+    cache = build_item_cache(params.item_table, params.item_proj, params.gating.item_net, cfg, quantized=True)
+    path = os.path.join(OUT, "item_cache_ref.molc")
+    cache.save(path)
+    back = ItemCache.load(path)
+    np.savez_compressed(os.path.join(OUT, "snapshot_case.npz"), item_embs=back.item_embs,
+                        item_gate_pre=back.item_gate_pre, stage1_embs=back.stage1_embs,
+                        codes=back.stage1_q.codes, scales=back.stage1_q.scales,
+                        cfg=np.array([cfg.k_u, cfg.k_x, cfg.d, cfg.gating_hidden], dtype=np.int64))
+    pcfg = MoLConfig(k_u=8, k_x=8, d=64, tau=20.0, gating_hidden=128, dropout_p=0.0)
+    pdims = TowerDims(n_users=4, n_items=1000, d_u=64, d_x=64, proj_hidden=128)
+    pp = init_params(pdims, pcfg, make_rng(4242))
+    pc = build_item_cache(pp.item_table, pp.item_proj, pp.gating.item_net, pcfg, quantized=True)
+    np.savez_compressed(os.path.join(OUT, "build_case.npz"), item_table=pp.item_table,
+                        **mlp_arrays("item_proj", pp.item_proj), **mlp_arrays("item_net", pp.gating.item_net),
+                        item_embs=pc.item_embs, item_gate_pre=pc.item_gate_pre, stage1_embs=pc.stage1_embs,
+                        codes=pc.stage1_q.codes, scales=pc.stage1_q.scales)
+
+
+def query_case():
+    """Production-shape user side (model.py:179-191 user_components, mol.py:186 user_net) for the
+    device query-prep parity test."""
+    cfg = MoLConfig(k_u=8, k_x=8, d=64, tau=20.0, gating_hidden=128, dropout_p=0.0)
+    dims = TowerDims(n_users=64, n_items=10, d_u=64, d_x=64, proj_hidden=128)
+    params = init_params(dims, cfg, make_rng(99))
+    users = np.arange(64)
+    np.savez_compressed(os.path.join(OUT, "query_case.npz"), user_table=params.user_table,
+                        **mlp_arrays("user_proj", params.user_proj), **mlp_arrays("user_net", params.gating.user_net),
+                        user_embs=user_components(params, users, cfg),
+                        uw=params.gating.user_net(params.user_table[users]))
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1:  # regenerate selected cases only, e.g. `make_golden.py snapshot_case`
+        for name in sys.argv[1:]:
+            globals()[name]()
+        sys.exit(0)
     small_case()
     production_case()
     known_answers()
