@@ -29,6 +29,7 @@
 //   E2: pi = softmax(silu(uw * gate_pre + D2)); score = sum pi * CL  -> global
 // The G logits and H hidden units never leave the SM.
 #include <algorithm>
+#include <vector>
 #include <cstdlib>
 
 #include "kernels.cuh"
@@ -261,11 +262,12 @@ struct Params {
   float* out;
   int64_t out_ld;
   int e1_tanh;  // hidden SiLU via tanh.approx (1 MUFU) instead of ex2 + rcp (2 MUFU)
+  unsigned long long* trace;  // dev tool (MOLR_TRACE_MOL): CTA 0 epilogue timeline, else null
   int gather4;  // item fetch by TMA tile::gather4 (4 items per request) instead of 1 KB bulk copies
 };
 
 template <class Id>
-__global__ void __launch_bounds__(64 + NE * 128, 1) mol_tc_kernel(Params P, const Id* __restrict__ ids,
+__global__ void __launch_bounds__(64 + NE * 256 + 32 * NE, 1) mol_tc_kernel(Params P, const Id* __restrict__ ids,
                                                                   const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ __align__(1024) uint8_t sm[];
   const uint32_t sbase = smem_u32(sm);
@@ -306,12 +308,12 @@ __global__ void __launch_bounds__(64 + NE * 128, 1) mol_tc_kernel(Params P, cons
         mbar_init(b0full(s), 1);
         mbar_init(b0empty(s), 1);
       }
-      mbar_init(d0free, 128);
+      mbar_init(d0free, 256);
       for (int g = 0; g < NE; ++g) {
         mbar_init(gbar(g, 0), 1);
-        mbar_init(gbar(g, 1), 128);
+        mbar_init(gbar(g, 1), 256);
         mbar_init(gbar(g, 2), 1);
-        mbar_init(gbar(g, 3), 128);
+        mbar_init(gbar(g, 3), 256);
         mbar_init(gbar(g, 4), 1);
       }
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -393,7 +395,7 @@ __global__ void __launch_bounds__(64 + NE * 128, 1) mol_tc_kernel(Params P, cons
         gk[g] = g;
       }
       const int64_t my_tiles = T > blockIdx.x ? (T - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-      while (kc < my_tiles || gk[0] < my_tiles || gk[1] < my_tiles) {
+      while (kc < my_tiles) {
         // ---- component GEMM stream ----
         if (kc < my_tiles) {
           if (cgrp < 0) {
@@ -431,72 +433,89 @@ __global__ void __launch_bounds__(64 + NE * 128, 1) mol_tc_kernel(Params P, cons
             }
           }
         }
-        // ---- cross-net layers of each group's current tile ----
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 2 + 8 * NE) {
+    // ================= cross-net issuers: one thread per epilogue group =================
+    // blocking waits (the thread sleeps until its group's A operand is ready), so each handoff
+    // costs one barrier wake-up rather than a poll of every stream
+    const int g = warp - (2 + 8 * NE);
+    if (lane == 0) {
+      constexpr uint32_t ID128 = idesc_bf16(128), ID64 = idesc_bf16(64);
+      const uint32_t tg = tmem_base + tm_grp(g);
+      const int64_t my_tiles = T > blockIdx.x ? (T - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+      uint32_t up = 0;
+      for (int64_t k = g; k < my_tiles; k += NE, up ^= 1) {
+        mbar_wait(gbar(g, 1), up);  // A1 stored by the group
+        tc_fence_after();
 #pragma unroll
-        for (int g = 0; g < NE; ++g) {
-          if (gk[g] >= my_tiles) continue;
-          const uint32_t tg = tmem_base + tm_grp(g);
-          const uint32_t up = guse[g] & 1;
-          if (gstate[g] == 0) {
-            if (!mbar_test(gbar(g, 1), up)) continue;
-            tc_fence_after();
+        for (int kk = 0; kk < 4; ++kk)
+          mma_bf16_ts(tg + 64, tg + kk * 8, desc_sw128(sbase + OFF_W1T + kk * 32), ID128, kk > 0);
+        mma_bf16(tg + 64, desc_interleave(sbase + OFF_BIASA, 128, 256), desc_interleave(sbase + OFF_W1B, 128, 256),
+                 ID128, 1);
+        mma_commit(gbar(g, 2));
+        mbar_wait(gbar(g, 3), up);  // A2 (SiLU hidden, hi/lo) stored by the group
+        tc_fence_after();
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk)
-              mma_bf16_ts(tg + 64, tg + kk * 8, desc_sw128(sbase + OFF_W1T + kk * 32), ID128, kk > 0);
-            mma_bf16(tg + 64, desc_interleave(sbase + OFF_BIASA, 128, 256), desc_interleave(sbase + OFF_W1B, 128, 256),
-                     ID128, 1);
-            mma_commit(gbar(g, 2));
-            gstate[g] = 1;
-          } else {
-            if (!mbar_test(gbar(g, 3), up)) continue;
-            tc_fence_after();
-#pragma unroll
-            for (int ch = 0; ch < 8; ++ch) {  // hidden chunk ch = K [16ch, 16ch+16)
-              const uint32_t bo = (ch >> 2) * 8192 + (ch & 3) * 32;
-              const uint64_t bhi = desc_sw128(sbase + OFF_W2T + bo), blo = desc_sw128(sbase + OFF_W2L + bo);
-              mma_bf16_ts(tg, tg + 64 + ch * 16, bhi, ID64, ch > 0);  // h_hi . W2_hi
-              mma_bf16_ts(tg, tg + 64 + ch * 16 + 8, bhi, ID64, 1);   // h_lo . W2_hi
-              mma_bf16_ts(tg, tg + 64 + ch * 16, blo, ID64, 1);       // h_hi . W2_lo
-            }
-            mma_commit(gbar(g, 4));
-            gstate[g] = 0;
-            ++guse[g];
-            gk[g] += NE;
-          }
+        for (int ch = 0; ch < 8; ++ch) {  // hidden chunk ch = K [16ch, 16ch+16)
+          const uint32_t bo = (ch >> 2) * 8192 + (ch & 3) * 32;
+          const uint64_t bhi = desc_sw128(sbase + OFF_W2T + bo), blo = desc_sw128(sbase + OFF_W2L + bo);
+          mma_bf16_ts(tg, tg + 64 + ch * 16, bhi, ID64, ch > 0);  // h_hi . W2_hi
+          mma_bf16_ts(tg, tg + 64 + ch * 16 + 8, bhi, ID64, 1);   // h_lo . W2_hi
+          mma_bf16_ts(tg, tg + 64 + ch * 16, blo, ID64, 1);       // h_hi . W2_lo
         }
+        mma_commit(gbar(g, 4));
       }
     }
     __syncwarp();
   } else {
-    // ================= epilogue warpgroups =================
-    const int eg = (warp - 2) >> 2;          // group id
+    // ================= epilogue groups: 8 warps each =================
+    // Group eg = warps 2+8eg .. 9+8eg.  Warp w of a group reads TMEM lane quarter w & 3 (its
+    // tile rows p) and column half hf = w >> 2 of every phase, so each SMSP runs four epilogue
+    // warps and each phase is half as long; the two halves of a row exchange the softmax max and
+    // partial sums through the spare columns 64..67 of the row's CL line.
+    const int eg = (warp - 2) >> 3;
+    const int hf = ((warp - 2) >> 2) & 1;    // column half
     const int quarter = warp & 3;            // TMEM lane quarter this warp may access
     const int p = quarter * 32 + lane;       // tile row = TMEM lane
     uint8_t* gs = sm + OFF_GRP + eg * SZ_GRP;
     float* CL = reinterpret_cast<float*>(gs + G_CL);
     float* UW = reinterpret_cast<float*>(gs + G_UW);
+    float* XR = CL + p * CL_LD + 64;         // row p's exchange slots: [max h0, max h1, sum h1, acc h1]
     const uint32_t lq = (uint32_t)(quarter * 32) << 16;
     const uint32_t td0 = tmem_base + TM_D0 + lq;
     const uint32_t tg = tmem_base + tm_grp(eg) + lq;
     const int bar_id = 1 + eg;
+    constexpr int NT = 256;                  // threads per group
     uint32_t ph = 0;
+#define TRACE(tag)                                                                                     \
+  if (P.trace && blockIdx.x == 0 && p == 0 && hf == 0) {                                               \
+    unsigned long long c;                                                                              \
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));                                                  \
+    const unsigned long long i = atomicAdd(P.trace, 1ull);                                             \
+    if (i < 65535) P.trace[1 + i] = (uint64_t(eg * 16 + (tag)) << 56) | (c & ((1ull << 56) - 1));      \
+  }
     TileCursor cur;
     for (int64_t tile = blockIdx.x + (int64_t)eg * gridDim.x; tile < T; tile += (int64_t)NE * gridDim.x) {
       const TileInfo t = tile_info(cur, tile, P.B, P.tile_pre, P.begin, P.end, P.X);
-      if (p < G) UW[p] = __ldg(P.uw + (int64_t)t.b * G + p);
-      // prefetch this row's gate pre-activations (bf16 x 64 = 128 B)
-      uint4 gpr[8];
+      if (hf == 0 && p < G) UW[p] = __ldg(P.uw + (int64_t)t.b * G + p);
+      // prefetch this row's gate pre-activations of this half (bf16 x 32 = 64 B)
+      uint4 gpr[4];
       {
         const int64_t x = cand_id(ids, t, p < t.np ? p : 0);
-        const uint4* src = reinterpret_cast<const uint4*>(P.gp + x * G);
+        const uint4* src = reinterpret_cast<const uint4*>(P.gp + x * G) + hf * 4;
 #pragma unroll
-        for (int m = 0; m < 8; ++m) gpr[m] = __ldg(src + m);
+        for (int m = 0; m < 4; ++m) gpr[m] = __ldg(src + m);
       }
       // ---- E0: component logits (shared D0) -> CL (transpose to one row per pair); free D0 ----
+      TRACE(0);
       mbar_wait(gbar(eg, 0), ph);
+      TRACE(1);
       tc_fence_after();
 #pragma unroll
-      for (int grp = 0; grp < NGROUPS; grp += 2) {
+      for (int gi = 0; gi < NGROUPS / 2; gi += 2) {
+        const int grp = hf * (NGROUPS / 2) + gi;
         uint32_t v[16], w[16];
         TMEM_LD16(td0 + grp * 16, v);
         TMEM_LD16(td0 + grp * 16 + 16, w);
@@ -510,12 +529,13 @@ __global__ void __launch_bounds__(64 + NE * 128, 1) mol_tc_kernel(Params P, cons
       }
       tc_fence_before();
       mbar_arrive(d0free);  // the next tile's component GEMM may overwrite D0
-      named_sync(bar_id, 128);
-      // ---- E0.5: row p -> A1 (bf16 pairs, group cols [0,32)) ----
+      TRACE(2);
+      named_sync(bar_id, NT);
+      // ---- E0.5: row p, logits [32 hf, 32 hf + 32) -> A1 (bf16 pairs, group cols [16 hf, 16 hf + 16)) ----
       {
-        const float4* row = reinterpret_cast<const float4*>(CL + p * CL_LD);
+        const float4* row = reinterpret_cast<const float4*>(CL + p * CL_LD + 32 * hf);
 #pragma unroll
-        for (int h = 0; h < 4; ++h) {
+        for (int h = 0; h < 2; ++h) {
           uint32_t a1[8];
 #pragma unroll
           for (int m = 0; m < 4; ++m) {
@@ -523,59 +543,75 @@ __global__ void __launch_bounds__(64 + NE * 128, 1) mol_tc_kernel(Params P, cons
             a1[2 * m] = pack_bf16(x.x, x.y);
             a1[2 * m + 1] = pack_bf16(x.z, x.w);
           }
-          TMEM_ST8(tg + h * 8, a1);
+          TMEM_ST8(tg + 16 * hf + h * 8, a1);
         }
         tmem_wait_st();
       }
       tc_fence_before();
       mbar_arrive(gbar(eg, 1));
-      // ---- E1: h = silu(D1) -> A2 hi/lo in place (cols [64+16ch, +8) hi, [+8, +16) lo) ----
+      TRACE(3);
+      // ---- E1: h = silu(D1) -> A2 hi/lo in place, hidden chunks [4 hf, 4 hf + 4) ----
       mbar_wait(gbar(eg, 2), ph);
+      TRACE(4);
       tc_fence_after();
+      {
+        uint32_t va[16], vb[16];
+        TMEM_LD16(tg + 64 + (4 * hf) * 16, va);
 #pragma unroll
-      for (int ch = 0; ch < 8; ++ch) {
-        uint32_t v[16];
-        TMEM_LD16(tg + 64 + ch * 16, v);
-        tmem_wait_ld();
-        uint32_t w[16];
+        for (int c4 = 0; c4 < 4; ++c4) {
+          const int ch = 4 * hf + c4;
+          uint32_t* v = (c4 & 1) ? vb : va;
+          tmem_wait_ld();
+          if (c4 < 3) {  // next chunk loads under this chunk's SiLU
+            if (c4 & 1) TMEM_LD16(tg + 64 + (ch + 1) * 16, va);
+            else TMEM_LD16(tg + 64 + (ch + 1) * 16, vb);
+          }
+          uint32_t w[16];
 #pragma unroll
-        for (int m = 0; m < 8; ++m) {
-          const float x0 = __uint_as_float(v[2 * m]), x1 = __uint_as_float(v[2 * m + 1]);
-          const float h0 = P.e1_tanh ? silu_tanh(x0) : silu_acc(x0), h1 = P.e1_tanh ? silu_tanh(x1) : silu_acc(x1);
-          const uint32_t hw = pack_bf16(h0, h1);
-          w[m] = hw;
-          w[8 + m] = pack_bf16(h0 - __uint_as_float(hw << 16), h1 - __uint_as_float(hw & 0xFFFF0000u));
+          for (int m = 0; m < 8; ++m) {
+            const float x0 = __uint_as_float(v[2 * m]), x1 = __uint_as_float(v[2 * m + 1]);
+            const float h0 = P.e1_tanh ? silu_tanh(x0) : silu_acc(x0), h1 = P.e1_tanh ? silu_tanh(x1) : silu_acc(x1);
+            const uint32_t hw = pack_bf16(h0, h1);
+            w[m] = hw;
+            w[8 + m] = pack_bf16(h0 - __uint_as_float(hw << 16), h1 - __uint_as_float(hw & 0xFFFF0000u));
+          }
+          TMEM_ST16(tg + 64 + ch * 16, w);
         }
-        TMEM_ST16(tg + 64 + ch * 16, w);
       }
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(gbar(eg, 3));
-      // ---- E2: combine + softmax + gated sum (logits from CL) ----
+      TRACE(5);
+      // ---- E2: combine + softmax + gated sum over gates [32 hf, 32 hf + 32), halves merged ----
       mbar_wait(gbar(eg, 4), ph);
+      TRACE(6);
       tc_fence_after();
-      float pre[64];
+      float pre[32];
       float mx = -INFINITY;
-#pragma unroll
-      for (int ch = 0; ch < 4; ++ch) {
-        uint32_t v[16];
-        TMEM_LD16(tg + ch * 16, v);
+      {
+        uint32_t v0[16], v1[16];
+        TMEM_LD16(tg + 32 * hf, v0);
+        TMEM_LD16(tg + 32 * hf + 16, v1);
         tmem_wait_ld();
 #pragma unroll
-        for (int m = 0; m < 16; ++m) {
-          const int g = ch * 16 + m;
-          const uint32_t wv = (&gpr[g >> 3].x)[(g & 7) >> 1];
-          const float gpv = __uint_as_float((g & 1) ? (wv & 0xFFFF0000u) : (wv << 16));
-          const float x = silu_acc(fmaf(UW[g], gpv, __uint_as_float(v[m])));
-          pre[g] = x;
+        for (int m = 0; m < 32; ++m) {
+          const int g = 32 * hf + m;
+          const uint32_t wv = (&gpr[m >> 3].x)[(m & 7) >> 1];
+          const float gpv = __uint_as_float((m & 1) ? (wv & 0xFFFF0000u) : (wv << 16));
+          const float d2 = __uint_as_float(m < 16 ? v0[m] : v1[m - 16]);
+          const float x = silu_acc(fmaf(UW[g], gpv, d2));
+          pre[m] = x;
           mx = fmaxf(mx, x);
         }
       }
+      XR[hf] = mx;
+      named_sync(bar_id, NT);
+      mx = fmaxf(XR[0], XR[1]);
       const float ml = mx * 1.4426950408889634f;
       float sum = 0.f, acc = 0.f;
-      const float4* row = reinterpret_cast<const float4*>(CL + p * CL_LD);
+      const float4* row = reinterpret_cast<const float4*>(CL + p * CL_LD + 32 * hf);
 #pragma unroll
-      for (int m4 = 0; m4 < 16; ++m4) {
+      for (int m4 = 0; m4 < 8; ++m4) {
         const float4 c = row[m4];
         const float cv[4] = {c.x, c.y, c.z, c.w};
 #pragma unroll
@@ -585,13 +621,19 @@ __global__ void __launch_bounds__(64 + NE * 128, 1) mol_tc_kernel(Params P, cons
           acc = fmaf(e, cv[i], acc);
         }
       }
-      if (p < t.np) {
-        const float s = __fdiv_rn(acc, sum);
+      if (hf == 1) {
+        XR[2] = sum;
+        XR[3] = acc;
+      }
+      named_sync(bar_id, NT);
+      if (hf == 0 && p < t.np) {
+        const float s = __fdiv_rn(acc + XR[3], sum + XR[2]);
         if (P.begin) P.out[t.seg0 + t.j0 + p] = s;
         else P.out[(int64_t)t.b * P.out_ld + t.j0 + p] = s;
       }
       tc_fence_before();
-      named_sync(bar_id, 128);  // CL / UW are rewritten by this group's next tile
+      TRACE(7);
+      named_sync(bar_id, NT);  // CL / UW / exchange slots are rewritten by this group's next tile
       ph ^= 1;
     }
   }
@@ -670,12 +712,29 @@ int mol_score_tc(molr_ctx* ctx, const molr_cache* c, const molr_gating* g, int B
     const char* gm = getenv("MOLR_GATHER");
     P.gather4 = (c->embs_tmap_ok && !(gm && gm[0] == 'b')) ? 1 : 0;
   }
+  Scratch trace;
+  P.trace = nullptr;
+  const char* trace_path = getenv("MOLR_TRACE_MOL");
+  if (trace_path) {
+    MOLR_TRY(trace.alloc(65536 * 8, s));
+    MOLR_CUDA(cudaMemsetAsync(trace.p, 0, 8, s));
+    P.trace = trace.as<unsigned long long>();
+  }
   auto kern = tc::mol_tc_kernel<Id>;
   const int smem = tc::SMEM_BYTES;
   MOLR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const int grid = (int)std::min<int64_t>(T, ctx->num_sms);
-  kern<<<grid, 64 + tc::NE * 128, smem, s>>>(P, segs.ids, c->embs_tmap);
+  kern<<<grid, 64 + tc::NE * 256 + 32 * tc::NE, smem, s>>>(P, segs.ids, c->embs_tmap);
   MOLR_LAUNCHED(ctx);
+  if (trace_path) {  // dev tool: dump CTA 0's epilogue timeline
+    std::vector<unsigned long long> h(65536);
+    MOLR_CUDA(cudaMemcpyAsync(h.data(), trace.p, 65536 * 8, cudaMemcpyDeviceToHost, s));
+    MOLR_CUDA(cudaStreamSynchronize(s));
+    if (FILE* f = fopen(trace_path, "wb")) {
+      fwrite(h.data(), 8, h.size(), f);
+      fclose(f);
+    }
+  }
   return MOLR_OK;
 }
 

@@ -1,4 +1,5 @@
-"""Dev tool: run the tc MoL kernel once with MOLR_TRACE_MOL set and print CTA 0's timeline."""
+"""Dev tool: run the tc MoL kernel with MOLR_TRACE_MOL set and summarise CTA 0's epilogue
+timeline (per-phase cycles per tile, averaged over tiles)."""
 import os
 import sys
 
@@ -9,20 +10,23 @@ os.environ["MOLR_TRACE_MOL"] = "/tmp/mol_trace.bin"
 from tests.test_gpu_parity import _prod_gating, _synthetic_prod_cache  # noqa: E402
 from paper_2306_04039_b200.mol import batch_score_all  # noqa: E402
 
-cache, syn, ue, feats = _synthetic_prod_cache(200_000, seed=5, n_users=8)
+cache, syn, ue, feats = _synthetic_prod_cache(200_000, seed=5, n_users=64)
 gating, _ = _prod_gating(syn)
 for _ in range(2):
     batch_score_all(cache, gating, ue, feats)
 t = np.fromfile("/tmp/mol_trace.bin", dtype=np.uint64)
-n = int(t[0])
+n = min(int(t[0]), 65535)
 ev = t[1:1 + n]
 tags = (ev >> np.uint64(56)).astype(int)
 clk = (ev & np.uint64((1 << 56) - 1)).astype(np.int64)
-clk -= clk.min()
-order = np.argsort(clk, kind="stable")
-names = {1: "prod_stage", 2: "C_done", 3: "L1_issued", 4: "L2_issued", 5: "E0_start", 6: "E1_start", 7: "E2_start",
-         8: "E2_end"}
-print("events", n)
-for i in order[:400]:
-    g, k = divmod(tags[i], 16)
-    print(f"{clk[i]:>10d}  g{g} {names.get(k, k)}")
+names = ["start", "d0_ready", "E0_done", "E05_done", "d1_ready", "E1_done", "d2_ready", "E2_done"]
+for g in range(2):
+    sel = [clk[(tags == g * 16 + k)] for k in range(8)]
+    m = min(len(x) for x in sel)
+    a = np.stack([x[:m] for x in sel])  # (8, tiles)
+    d = np.diff(a, axis=0)
+    per_tile = np.diff(a[0])
+    print(f"group {g}: {m} tiles, cycles per tile {np.median(per_tile):.0f}")
+    for k in range(7):
+        print(f"   {names[k]:>9s} -> {names[k + 1]:<9s} {np.median(d[k]):8.0f}")
+    print(f"   E2_done -> next start {np.median(a[0, 1:] - a[7, :-1]):8.0f}")
