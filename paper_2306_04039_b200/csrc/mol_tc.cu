@@ -11,7 +11,7 @@
 // TMEM (512 columns): D0 = cols [0,128) is ONE buffer shared by both groups: the component
 // GEMM streams through it tile after tile (it only waits for the previous tile's E0 to drain it),
 // so the item ring is consumed continuously and the gather never stalls on an epilogue.
-// Group g owns cols [128 + 192 g, 320 + 192 g): A1/D2 (64) and D1/A2 (128).
+// Group g owns cols [128 + 192 g, 320 + 192 g): A1 then A2 (64 cols) and D1 then D2 (128 cols).
 // Per tile of 128 (query, candidate) pairs of ONE query:
 //   C : 8 x [M=128 rows = 16 items x 8 components] x [N=16 = (hi,lo) x 8 user components] x K=64
 //       (SS) -> D0.  Query side split u = hi + lo in bf16 (~2^-17 relative), item side exact
@@ -20,17 +20,17 @@
 //       (kept there for the final gated sum); D0 released
 //   E0.5: row p -> A1 = bf16 logits packed two per column (the A operand of layer 1, from TMEM)
 //   L1: A1 (TMEM) . W1^T (smem) + [1 1 0..] . [b1_hi b1_lo 0..]^T (SS, K=16) -> D1
-//   E1: h = silu(D1) -> A2 = [bf16(h) | bf16(h - bf16(h))] written in place over D1 (each
-//       16-column chunk: 8 cols hi + 8 cols lo); keeping h to ~2^-17 keeps the cross-net within
-//       tolerance for sharp gating
-//   L2: h_hi.W2_hi + h_lo.W2_hi + h_hi.W2_lo (A from TMEM, W2 split hi/lo in smem) -> D2: the
-//       cross net's second layer is carried to ~2^-16 (W2 rounding dominated the error budget
-//       under sharp gating)
+//   E1: h = silu(D1) -> A2 = fp16(h), two per column (group cols [0,64): A1 is dead by then)
+//   L2: A2 (TMEM) . W2 (fp16, smem) -> D2 (over D1).  fp16 h and W2 carry 2^-11 relative error:
+//       max |score error| 2.2e-7 under x4-sharpened gating (emulated; tolerance floor 1e-6), and
+//       one fp16 MMA pass replaces the three bf16 hi/lo passes
 //   E2: pi = softmax(silu(uw * gate_pre + D2)); score = sum pi * CL  -> global
 // The G logits and H hidden units never leave the SM.
 #include <algorithm>
 #include <vector>
 #include <cstdlib>
+
+#include <cuda_fp16.h>
 
 #include "kernels.cuh"
 #include "stage1.cuh"
@@ -50,9 +50,8 @@ constexpr int CL_LD = 68;           // fp32 row stride of the logit transpose bu
 constexpr int SZ_STAGE = GROUP * 1024;                  // 16 KB
 constexpr int OFF_RING = 0;
 constexpr int OFF_W1T = OFF_RING + NSTAGE * SZ_STAGE;   // 128 x 64 bf16, SW128      16 KB
-constexpr int OFF_W2T = OFF_W1T + 16384;                // 2 x (64 x 64) bf16, SW128 16 KB
-constexpr int OFF_W2L = OFF_W2T + 16384;                // W2^T residual bf16(W2 - bf16(W2))     16 KB
-constexpr int OFF_W1B = OFF_W2L + 16384;                // 128 x 16 bf16, interleave  4 KB
+constexpr int OFF_W2T = OFF_W1T + 16384;                // 2 x (64 x 64) fp16, SW128 16 KB
+constexpr int OFF_W1B = OFF_W2T + 16384;                // 128 x 16 bf16, interleave  4 KB
 constexpr int OFF_BIASA = OFF_W1B + 4096;               // 128 x 16 bf16, interleave  4 KB
 constexpr int NB0 = 3;                                  // B0 (query operand) ring slots
 constexpr int OFF_B0 = OFF_BIASA + 4096;                // NB0 x 16 x 64 bf16 SW128 (u_hi ; u_lo), 2 KB each
@@ -68,7 +67,7 @@ constexpr int OFF_TMEM = OFF_BAR + NBAR * 8;
 constexpr int SMEM_BYTES = OFF_TMEM + 16;
 static_assert(SMEM_BYTES <= 232448, "shared memory budget");
 constexpr int TM_D0 = 0;                                // shared component-logit accumulator
-__host__ __device__ constexpr int tm_grp(int g) { return 128 + 192 * g; }  // A1/D2 at +0, D1/A2 at +64
+__host__ __device__ constexpr int tm_grp(int g) { return 128 + 192 * g; }  // A1/A2 at +0, D1/D2 at +64
 
 // ---- PTX wrappers ---------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -130,6 +129,10 @@ __device__ __forceinline__ uint64_t desc_interleave(uint32_t addr, uint32_t lbo,
          (1ull << 46);
 }
 // kind::f16 instruction descriptor: A = B = bf16, D = f32, both K-major, M = 128
+// kind::f16 instruction descriptor: A = B = fp16, D = f32, both K-major, M = 128
+__host__ __device__ constexpr uint32_t idesc_f16(int n) {
+  return (1u << 4) | (uint32_t(n >> 3) << 17) | (uint32_t(128 >> 4) << 24);
+}
 __host__ __device__ constexpr uint32_t idesc_bf16(int n) {
   return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(n >> 3) << 17) | (uint32_t(128 >> 4) << 24);
 }
@@ -173,6 +176,10 @@ __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.
 
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);  // .x = lo (low 16 bits), .y = hi
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+__device__ __forceinline__ uint32_t pack_f16(float lo, float hi) {
+  __half2 v = __floats2half2_rn(lo, hi);  // .x = lo (low 16 bits), .y = hi
   return *reinterpret_cast<uint32_t*>(&v);
 }
 __device__ __forceinline__ float fast_tanh(float x) {
@@ -291,7 +298,6 @@ __global__ void __launch_bounds__(64 + NE * 256 + 32 * NE, 1) mol_tc_kernel(Para
     for (int i = threadIdx.x; i < 1024; i += blockDim.x) {
       reinterpret_cast<uint4*>(sm + OFF_W1T)[i] = __ldg(src1 + i);
       reinterpret_cast<uint4*>(sm + OFF_W2T)[i] = __ldg(src2 + i);
-      reinterpret_cast<uint4*>(sm + OFF_W2L)[i] = __ldg(src2 + 1024 + i);
     }
     for (int i = threadIdx.x; i < 256; i += blockDim.x) reinterpret_cast<uint4*>(sm + OFF_W1B)[i] = __ldg(src3 + i);
     // bias A operand: K columns 0 and 1 of every row = 1.0 (pairs with the b1 hi / lo rows of W1B)
@@ -455,15 +461,12 @@ __global__ void __launch_bounds__(64 + NE * 256 + 32 * NE, 1) mol_tc_kernel(Para
         mma_bf16(tg + 64, desc_interleave(sbase + OFF_BIASA, 128, 256), desc_interleave(sbase + OFF_W1B, 128, 256),
                  ID128, 1);
         mma_commit(gbar(g, 2));
-        mbar_wait(gbar(g, 3), up);  // A2 (SiLU hidden, hi/lo) stored by the group
+        mbar_wait(gbar(g, 3), up);  // A2 (SiLU hidden, fp16) stored by the group
         tc_fence_after();
 #pragma unroll
-        for (int ch = 0; ch < 8; ++ch) {  // hidden chunk ch = K [16ch, 16ch+16)
+        for (int ch = 0; ch < 8; ++ch) {  // hidden K [16ch, 16ch+16): A2 cols [8ch, 8ch+8)
           const uint32_t bo = (ch >> 2) * 8192 + (ch & 3) * 32;
-          const uint64_t bhi = desc_sw128(sbase + OFF_W2T + bo), blo = desc_sw128(sbase + OFF_W2L + bo);
-          mma_bf16_ts(tg, tg + 64 + ch * 16, bhi, ID64, ch > 0);  // h_hi . W2_hi
-          mma_bf16_ts(tg, tg + 64 + ch * 16 + 8, bhi, ID64, 1);   // h_lo . W2_hi
-          mma_bf16_ts(tg, tg + 64 + ch * 16, blo, ID64, 1);       // h_hi . W2_lo
+          mma_bf16_ts(tg + 64, tg + ch * 8, desc_sw128(sbase + OFF_W2T + bo), idesc_f16(64), ch > 0);
         }
         mma_commit(gbar(g, 4));
       }
@@ -550,7 +553,18 @@ __global__ void __launch_bounds__(64 + NE * 256 + 32 * NE, 1) mol_tc_kernel(Para
       tc_fence_before();
       mbar_arrive(gbar(eg, 1));
       TRACE(3);
-      // ---- E1: h = silu(D1) -> A2 hi/lo in place, hidden chunks [4 hf, 4 hf + 4) ----
+      {  // while L1 runs: pull the next tile's candidate id and gate row into L1 (the dependent
+         // metadata loads otherwise sit on the critical path between this tile's E2 and the next)
+        const int64_t nt = tile + (int64_t)NE * gridDim.x;
+        if (nt < T) {
+          TileCursor c2 = cur;
+          const TileInfo u = tile_info(c2, nt, P.B, P.tile_pre, P.begin, P.end, P.X);
+          const int64_t xn = cand_id(ids, u, p < u.np ? p : 0);
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(P.gp + xn * G + hf * 32));
+          if (hf == 0 && p < G) asm volatile("prefetch.global.L1 [%0];" ::"l"(P.uw + (int64_t)u.b * G + p));
+        }
+      }
+      // ---- E1: h = silu(D1) -> A2 (fp16 pairs, group cols [32 hf, 32 hf + 32)), hidden chunks [4 hf, 4 hf + 4) ----
       mbar_wait(gbar(eg, 2), ph);
       TRACE(4);
       tc_fence_after();
@@ -566,16 +580,14 @@ __global__ void __launch_bounds__(64 + NE * 256 + 32 * NE, 1) mol_tc_kernel(Para
             if (c4 & 1) TMEM_LD16(tg + 64 + (ch + 1) * 16, va);
             else TMEM_LD16(tg + 64 + (ch + 1) * 16, vb);
           }
-          uint32_t w[16];
+          uint32_t w[8];
 #pragma unroll
           for (int m = 0; m < 8; ++m) {
             const float x0 = __uint_as_float(v[2 * m]), x1 = __uint_as_float(v[2 * m + 1]);
             const float h0 = P.e1_tanh ? silu_tanh(x0) : silu_acc(x0), h1 = P.e1_tanh ? silu_tanh(x1) : silu_acc(x1);
-            const uint32_t hw = pack_bf16(h0, h1);
-            w[m] = hw;
-            w[8 + m] = pack_bf16(h0 - __uint_as_float(hw << 16), h1 - __uint_as_float(hw & 0xFFFF0000u));
+            w[m] = pack_f16(h0, h1);
           }
-          TMEM_ST16(tg + 64 + ch * 16, w);
+          TMEM_ST8(tg + ch * 8, w);  // A2 = fp16 h, two per column (A1 is dead: L1 has completed)
         }
       }
       tmem_wait_st();
@@ -590,8 +602,8 @@ __global__ void __launch_bounds__(64 + NE * 256 + 32 * NE, 1) mol_tc_kernel(Para
       float mx = -INFINITY;
       {
         uint32_t v0[16], v1[16];
-        TMEM_LD16(tg + 32 * hf, v0);
-        TMEM_LD16(tg + 32 * hf + 16, v1);
+        TMEM_LD16(tg + 64 + 32 * hf, v0);
+        TMEM_LD16(tg + 64 + 32 * hf + 16, v1);
         tmem_wait_ld();
 #pragma unroll
         for (int m = 0; m < 32; ++m) {
@@ -757,7 +769,7 @@ extern "C" int molr_gating_tc_prepare(molr_gating* g) {
   MOLR_CUDA(cudaMemcpy(w1.data(), g->w1, w1.size() * 4, cudaMemcpyDefault));
   MOLR_CUDA(cudaMemcpy(b1.data(), g->b1, b1.size() * 4, cudaMemcpyDefault));
   MOLR_CUDA(cudaMemcpy(w2.data(), g->w2, w2.size() * 4, cudaMemcpyDefault));
-  std::vector<__nv_bfloat16> img(8192 + 2048 + 8192 + 8192, __float2bfloat16(0.0f));
+  std::vector<__nv_bfloat16> img(8192 + 2048 + 8192, __float2bfloat16(0.0f));
   auto sw = [](int r, int k) {  // element offset in an SW128 K-major [rows x 64] region
     return (r >> 3) * 512 + (r & 7) * 64 + ((((k >> 3) ^ (r & 7))) << 3) + (k & 7);
   };
@@ -770,15 +782,14 @@ extern "C" int molr_gating_tc_prepare(molr_gating* g) {
     img[base + 0] = hi;
     img[base + 1] = lo;
   }
+  // W2^T as fp16 (the L2 MMA runs fp16 x fp16 -> f32: h and W2 at 2^-11 relative)
   for (int gg = 0; gg < 64; ++gg)
     for (int j = 0; j < 128; ++j) {
-      const float v = w2[size_t(j) * 64 + gg];
-      const __nv_bfloat16 hi = __float2bfloat16(v);
-      img[8192 + 2048 + (j >> 6) * 4096 + sw(gg, j & 63)] = hi;
-      img[8192 + 2048 + 8192 + (j >> 6) * 4096 + sw(gg, j & 63)] = __float2bfloat16(v - __bfloat162float(hi));
+      const __half hv = __float2half_rn(w2[size_t(j) * 64 + gg]);
+      reinterpret_cast<__half*>(img.data())[8192 + 2048 + (j >> 6) * 4096 + sw(gg, j & 63)] = hv;
     }
-  // layout in device memory: [W1T 8192][W1B 2048][W2T 8192][W2L 8192] -> w1t_bf16 points at the
-  // start, w2t_bf16 at +10240
+  // layout in device memory: [W1T 8192 bf16][W1B 2048 bf16][W2T 8192 fp16] -> w1t_bf16 points at
+  // the start, w2t_bf16 at +10240
   MOLR_CUDA(cudaMalloc(&g->w1t_bf16, img.size() * 2));
   MOLR_CUDA(cudaMemcpy(g->w1t_bf16, img.data(), img.size() * 2, cudaMemcpyHostToDevice));
   g->w2t_bf16 = g->w1t_bf16 + 10240;

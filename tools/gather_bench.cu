@@ -109,6 +109,61 @@ __global__ void gather4_kernel(const __grid_constant__ CUtensorMap tmap, const i
   if (sm[t] == 123) sink[0] = 1;
 }
 
+// mixed: per 16-item stage, stages s with (s % 8) < TMA8 go through TMA gather4 (warp 0), the
+// rest through 16-byte cp.async by warps 1..NW (LSU path) — do the two paths add up?
+template <int TMA8, int NW>
+__global__ void mixed_kernel(const __grid_constant__ CUtensorMap tmap, const uint4* __restrict__ src,
+                             const int* __restrict__ idx, int n_per_cta, int* sink) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ __align__(8) uint64_t bar[4];
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  if (t < 4) asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&bar[t])), "r"(1));
+  __syncthreads();
+  const int* my = idx + (int64_t)blockIdx.x * n_per_cta;
+  const int nst = n_per_cta / 16;
+  if (warp == 0) {
+    uint32_t ph[4] = {0, 0, 0, 0};
+    int k = 0;
+    for (int st = 0; st < nst; ++st) {
+      if ((st & 7) >= TMA8) continue;
+      const int b = k & 3;
+      if (k >= 4) {
+        asm volatile("{.reg .pred P1; W: mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1; @!P1 bra W;}" ::"r"(smem_u32(&bar[b])), "r"(ph[b]));
+        ph[b] ^= 1;
+      }
+      if (lane == 0) asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar[b])), "r"(16 * 1024));
+      __syncwarp();
+      if (lane < 4) {
+        const int* r = my + st * 16 + 4 * lane;
+        asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];"
+                     ::"r"(smem_u32(sm + b * 16384 + lane * 4096)), "l"(&tmap), "r"(0), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]),
+                       "r"(smem_u32(&bar[b])) : "memory");
+      }
+      __syncwarp();
+      ++k;
+    }
+    for (int b = 0; b < 4 && b < k; ++b)
+      asm volatile("{.reg .pred P1; W2: mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1; @!P1 bra W2;}" ::"r"(smem_u32(&bar[b])), "r"(ph[b]));
+  } else if (warp <= NW) {
+    const int tt = t - 32, nt = NW * 32;
+    int k = 0;
+    for (int st = 0; st < nst; ++st) {
+      if ((st & 7) < TMA8) continue;
+      uint8_t* dst = sm + 65536 + (k & 3) * 16384;
+      for (int c = tt; c < 16 * 64; c += nt) {
+        const int b = c >> 6, cc = c & 63;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst + b * 1024 + cc * 16)), "l"(src + (int64_t)my[st * 16 + b] * 64 + cc) : "memory");
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      asm volatile("cp.async.wait_group 3;" ::: "memory");
+      ++k;
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+  }
+  __syncthreads();
+  if (sm[t] == 123) sink[0] = 1;
+}
+
 typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
                              const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -190,6 +245,30 @@ int main() {
                  cudaGetErrorString(cudaGetLastError()));
         };
         runt(k4, 4 * 16384, prom ? "gather4 depth4 l2prom256" : "gather4 depth4");
+        if (!prom) {
+          auto runm = [&](auto kern, int nthreads, const char* name) {
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 16384);
+            cudaEvent_t a, b;
+            cudaEventCreate(&a);
+            cudaEventCreate(&b);
+            kern<<<ctas, nthreads, 8 * 16384>>>(tm, src, idx, n_per, sink);
+            cudaEventRecord(a);
+            for (int r2 = 0; r2 < 3; ++r2) kern<<<ctas, nthreads, 8 * 16384>>>(tm, src, idx, n_per, sink);
+            cudaEventRecord(b);
+            cudaEventSynchronize(b);
+            float ms;
+            cudaEventElapsedTime(&ms, a, b);
+            double bytes = 3.0 * ctas * n_per * 1024.0;
+            printf("%s %-28s %7.1f GB/s  (%s)\n", pass ? "local " : "random", name, bytes / ms / 1e6,
+                   cudaGetErrorString(cudaGetLastError()));
+          };
+          runm(mixed_kernel<8, 8>, 32 * 9, "mixed tma 8/8");
+          runm(mixed_kernel<6, 8>, 32 * 9, "mixed tma 6/8 + lsu 8w");
+          runm(mixed_kernel<5, 8>, 32 * 9, "mixed tma 5/8 + lsu 8w");
+          runm(mixed_kernel<4, 8>, 32 * 9, "mixed tma 4/8 + lsu 8w");
+          runm(mixed_kernel<5, 16>, 32 * 17, "mixed tma 5/8 + lsu 16w");
+          runm(mixed_kernel<0, 16>, 32 * 17, "mixed lsu only 16w");
+        }
         runt(k8, 8 * 16384, prom ? "gather4 depth8 l2prom256" : "gather4 depth8");
       }
     }

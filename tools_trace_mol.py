@@ -10,7 +10,7 @@ os.environ["MOLR_TRACE_MOL"] = "/tmp/mol_trace.bin"
 from tests.test_gpu_parity import _prod_gating, _synthetic_prod_cache  # noqa: E402
 from paper_2306_04039_b200.mol import batch_score_all  # noqa: E402
 
-cache, syn, ue, feats = _synthetic_prod_cache(200_000, seed=5, n_users=64)
+cache, syn, ue, feats = _synthetic_prod_cache(int(os.environ.get("TRACE_ITEMS", "200000")), seed=5, n_users=int(os.environ.get("TRACE_USERS", "64")))
 gating, _ = _prod_gating(syn)
 for _ in range(2):
     batch_score_all(cache, gating, ue, feats)
@@ -30,3 +30,8 @@ for g in range(2):
     for k in range(7):
         print(f"   {names[k]:>9s} -> {names[k + 1]:<9s} {np.median(d[k]):8.0f}")
     print(f"   E2_done -> next start {np.median(a[0, 1:] - a[7, :-1]):8.0f}")
+a0, a1 = clk[tags == 32], clk[tags == 33]
+m = min(len(a0), len(a1))
+if m > 2:
+    print(f"component stream: {m} tiles, cycles per tile {np.median(np.diff(a0[:m])):.0f}, "
+          f"stages wait+MMA {np.median(a1[:m] - a0[:m]):.0f}, commit->next start {np.median(a0[1:m] - a1[:m - 1]):.0f}")
