@@ -42,7 +42,7 @@ constexpr int KX = 8, D = 64, G = 64, H = 128;
 constexpr int TILE = 128;           // pairs per tile (MMA M)
 constexpr int GROUP = 16;           // items per component MMA (16 items x 8 rows = 128)
 constexpr int NGROUPS = TILE / GROUP;
-constexpr int NSTAGE = 6;           // ring stages (16 KB each): ~96 KB of item blocks in flight per SM
+constexpr int NSTAGE = 7;           // ring stages (16 KB each): 112 KB of item blocks in flight per SM
 constexpr int NE = 2;               // epilogue groups
 constexpr int CL_LD = 68;           // fp32 row stride of the logit transpose buffer (conflict-free LDS.128)
 

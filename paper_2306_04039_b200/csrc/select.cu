@@ -130,6 +130,54 @@ segmented_topk_kernel(int B, const int64_t* __restrict__ begin, const int64_t* _
   const int kk = (int)imin64(k, n);
   if (kk <= 0) return;
   auto idof = [&](int64_t i) -> uint32_t { return id ? (uint32_t)id[i] : (uint32_t)i; };
+  // ---- fast path: sampled bound + one filtering pass ----------------------------------------
+  // bound = the r-th largest of every 16th score, r ~ 4 sigma above the expected number of
+  // samples beating the k-th largest, so bound <= k-th largest with overwhelming probability.
+  // Every score >= bound is gathered (with its id) and sorted; when at least kk passed, the
+  // k-th largest is >= bound, so the passers contain the exact top-k including its ties.
+  // Otherwise (or on overflow of the smem buffer) the two-radix-select path below runs.
+  if (n >= int64_t(32) * kk && kk <= 512) {
+    constexpr int kStride = 16;
+    const int64_t ns = n / kStride;
+    const double mu = double(kk) / kStride;
+    const int64_t r = imin64(ns, int64_t(mu + 4.0 * sqrt(mu) + 3.0));
+    uint32_t bkey;
+    int64_t bless;
+    block_radix_select<uint32_t>([&](int64_t i, uint32_t* kk2) { *kk2 = desc_key(sc[i * kStride]); return true; }, ns, r,
+                                 hist, &bkey, &bless);
+    if (threadIdx.x == 0) s_count = 0;
+    __syncthreads();
+    const int64_t n_pad = (n + 31) / 32 * 32;
+    for (int64_t i = threadIdx.x; i < n_pad; i += blockDim.x) {
+      uint32_t key = 0;
+      bool take = false;
+      if (i < n) {
+        key = desc_key(sc[i]);
+        take = key <= bkey;  // score >= bound
+      }
+      unsigned bal = __ballot_sync(0xffffffffu, take);
+      int base = 0;
+      if ((threadIdx.x & 31) == 0 && bal) base = atomicAdd(&s_count, __popc(bal));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      const int pos = base + __popc(bal & ((1u << (threadIdx.x & 31)) - 1));
+      if (take && pos < kSortCap) buf[pos] = (uint64_t(key) << 32) | idof(i);
+    }
+    __syncthreads();
+    const int cnt = s_count;
+    if (cnt >= kk && cnt <= kSortCap) {
+      const int64_t m2 = next_pow2(cnt);
+      for (int64_t i = cnt + threadIdx.x; i < m2; i += blockDim.x) buf[i] = ~0ull;
+      __syncthreads();
+      block_bitonic_sort(buf, m2);
+      for (int i = threadIdx.x; i < kk; i += blockDim.x) {
+        const uint64_t v = buf[i];
+        out_ids[int64_t(b) * k + i] = int64_t(uint32_t(v)) + id_offset;
+        out_scores[int64_t(b) * k + i] = key_f32(~uint32_t(v >> 32));
+      }
+      return;  // uniform: every thread read the same s_count
+    }
+    __syncthreads();
+  }
   uint32_t kstar, istar;
   int64_t less, less2;
   block_radix_select<uint32_t>([&](int64_t i, uint32_t* kk2) { *kk2 = desc_key(sc[i]); return true; }, n, kk,

@@ -591,3 +591,38 @@ def test_sample_threshold_pilot_exact(strict, raw, monkeypatch):
         np.testing.assert_array_equal(runs["pilot"][0], runs[tag][0])
         np.testing.assert_array_equal(runs["pilot"][1], runs[tag][1])
     assert np.all(np.abs(runs["pilot"][2] - 3000) < 3000 * 0.3)
+
+
+def test_topk_sampled_bound_path_ties():
+    """The segmented top-k's sampled-bound fast path (n >= 32 k) keeps the reference order
+    (score desc, id asc — np.lexsort((ids, -scores)), mol.py:407) with massive ties: 40 distinct
+    items each repeated 250 times, top-100 = ties across the boundary, ragged candidate lists."""
+    from paper_2306_04039_b200.mol import ItemCache, MoLConfig, QueryState, batch_mol_top_k, mol_top_k
+    from paper_2306_04039_b200.quant import quantize_rowwise
+
+    cache0, syn, ue, feats = _synthetic_prod_cache(40, seed=23, n_users=6)
+    gating, og = _prod_gating(syn)
+    rep = np.tile(np.arange(40), 250)
+    embs, gp = cache0.item_embs[rep], cache0.item_gate_pre[rep]
+    s1 = embs.mean(axis=1).astype(np.float32)
+    cfg = MoLConfig(k_u=8, k_x=8, d=64, tau=20.0, gating_hidden=128, dropout_p=0.0)
+    cache = ItemCache(config=cfg, item_embs=embs, item_gate_pre=gp, stage1_embs=s1, stage1_q=quantize_rowwise(s1))
+    oc = O.Cache(cache.item_embs, cache.item_gate_pre, cache.stage1_embs, None, 20.0, 8)
+    X = cache.num_items
+    rng = np.random.default_rng(4)
+    lists = [np.arange(X), rng.permutation(X)[:7000], rng.permutation(X)[:3300]]
+    for u in range(3):
+        ids, sc = mol_top_k(cache, gating, lists[u], QueryState(ue[u], feats[u]), 100)
+        oi, osc = O.mol_top_k(oc, og, lists[u], ue[u], feats[u], 100)
+        ref_all = np.full(X, -np.inf)
+        ref_all[lists[u]] = O.score_candidates(oc, og, lists[u], ue[u], feats[u])
+        assert topk_equal_modulo_ties(ids, oi, ref_all)
+        # among equal GPU scores the ids ascend (the reference's tie-break)
+        for a in range(99):
+            if sc[a] == sc[a + 1]:
+                assert ids[a] < ids[a + 1]
+    bi, bs = batch_mol_top_k(cache, gating, ue[:4], feats[:4], 100)
+    for u in range(4):
+        oi, _ = O.mol_top_k(oc, og, np.arange(X), ue[u], feats[u], 100)
+        ref_all = O.score_candidates(oc, og, np.arange(X), ue[u], feats[u])
+        assert topk_equal_modulo_ties(bi[u], oi, ref_all)
