@@ -8,10 +8,9 @@
 // Layout: queries (B <= 1024, padded to blocks of 128) stay resident in shared memory for the
 // whole launch (64 KB); item tiles of 256 rows (16 KB of codes in the cache's interleaved
 // layout + 1 KB of scales + per-32-row scale min/max) stream through a 4-stage ring by bulk copy.
-// Per (tile, query block) the single MMA thread issues four M=128 x N=64 x K=64 MMAs, one per
-// 64-item quarter of the tile, into eight 64-column TMEM buffers: epilogue warpgroup w owns
-// quarter w and double-buffers it (buffers 2w, 2w+1), so an epilogue never waits on an MMA that
-// is queued behind another warpgroup's buffer.
+// Per (tile, query block) the single MMA thread issues one M=128 x N=256 x K=64 MMA pair into
+// one of two 256-column TMEM buffers (double-buffered by job parity); epilogue warpgroup w tests
+// columns [64w, 64w+64) (its 64-item quarter of the tile) of every job.
 //
 // Passers go to per-CTA private segments of each query's candidate list with shared-memory
 // counters (no global atomics on the hot path); a compaction kernel concatenates the segments.
@@ -37,7 +36,7 @@ constexpr int OFF_RING = OFF_A + MAXQB * 8192;
 constexpr int OFF_T = OFF_RING + NSTAGE * SZ_STAGE;  // per-query threshold (f32 or s32), 4 KB
 constexpr int OFF_CNT = OFF_T + MAXQB * QB * 4;      // per-query passer counters of this CTA, 4 KB
 constexpr int NEPI = 4;    // epilogue warpgroups: warpgroup w owns tile columns [64w, 64w + 64)
-constexpr int NBUF = 2 * NEPI;  // 64-column TMEM accumulators
+constexpr int NBUF = 2;         // 256-column TMEM accumulators (parity of the job); WG w reads cols [64w, 64w+64)
 constexpr int NTHREADS = 64 + NEPI * 128;
 constexpr int OFF_BAR = OFF_CNT + MAXQB * QB * 4;
 constexpr int NBAR = 2 * NSTAGE + 2 * NBUF;
@@ -92,7 +91,7 @@ __device__ __forceinline__ uint64_t desc_ilv(uint32_t addr) {  // interleave K-m
   return uint64_t((addr >> 4) & 0x3FFF) | (uint64_t(128 >> 4) << 16) | (uint64_t(512 >> 4) << 32) | (1ull << 46);
 }
 // kind::i8: A = B = signed 8-bit, D = s32, K-major, M = 128, N = 64
-constexpr uint32_t IDESC_I8 = (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(64 >> 3) << 17) | (uint32_t(QB >> 4) << 24);
+constexpr uint32_t IDESC_I8 = (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(NT >> 3) << 17) | (uint32_t(QB >> 4) << 24);
 __device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t accum) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
@@ -189,7 +188,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) s1_tc_kernel(Params P) {
     }
     for (int e = 0; e < NBUF; ++e) {
       mbar_init(tfull(e), 1);
-      mbar_init(tempty(e), 128);
+      mbar_init(tempty(e), NEPI * 128);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -224,27 +223,25 @@ __global__ void __launch_bounds__(NTHREADS, 1) s1_tc_kernel(Params P) {
     }
   } else if (warp == 1) {
     // ================= MMA issuer =================
-    // per (tile, query block): four M=128 x N=64 x K=64 MMAs, one per tile quarter, each into
-    // its warpgroup's next buffer (blocking waits: the hardware sleeps the thread)
+    // per (tile, query block): one M=128 x N=256 x K=64 MMA pair into the job's 256-column
+    // buffer (parity jc & 1) once all four warpgroups have drained it; one wait per job
+    // (blocking: the hardware sleeps the thread)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      uint32_t jc = 0;  // (tile, query block) jobs issued: buffer parity = jc & 1, use = jc >> 1
+      uint32_t jc = 0;  // (tile, query block) jobs issued: buffer = jc & 1, use = jc >> 1
       for (int64_t tile = tile_lo; tile < tile_hi; ++tile) {
         mbar_wait(full_bar(stage), phase);
         tc_fence_after();
         const uint32_t bt = sbase + OFF_RING + stage * SZ_STAGE;
         for (int qb = 0; qb < nqb; ++qb, ++jc) {
           const uint32_t at = sbase + OFF_A + qb * 8192;
-#pragma unroll
-          for (int qt = 0; qt < NEPI; ++qt) {
-            const int buf = qt * 2 + int(jc & 1);
-            mbar_wait(tempty(buf), ((jc >> 1) & 1) ^ 1);
-            tc_fence_after();
-            mma_i8(tmem_base + buf * 64, desc_ilv(at), desc_ilv(bt + qt * 4096), 0);
-            mma_i8(tmem_base + buf * 64, desc_ilv(at + 256), desc_ilv(bt + qt * 4096 + 256), 1);
-            mma_commit(tfull(buf));
-          }
+          const int buf = int(jc & 1);
+          mbar_wait(tempty(buf), ((jc >> 1) & 1) ^ 1);
+          tc_fence_after();
+          mma_i8(tmem_base + buf * 256, desc_ilv(at), desc_ilv(bt), 0);
+          mma_i8(tmem_base + buf * 256, desc_ilv(at + 256), desc_ilv(bt + 256), 1);
+          mma_commit(tfull(buf));
         }
         mma_commit(empty_bar(stage));
         if (++stage == NSTAGE) {
@@ -276,8 +273,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) s1_tc_kernel(Params P) {
       const int nvalid = (int)imax64(0, imin64(64, P.n - row0));
       for (int qb = 0; qb < nqb; ++qb, ++jc) {
         const int q = qb * QB + p;
-        const int buf = w * 2 + int(jc & 1);
-        const uint32_t tm = tmem_base + buf * 64 + tlane;
+        const int buf = int(jc & 1);
+        const uint32_t tm = tmem_base + buf * 256 + w * 64 + tlane;
         mbar_wait(tfull(buf), uint32_t((jc >> 1) & 1));
         tc_fence_after();
         if (WRITE) {
