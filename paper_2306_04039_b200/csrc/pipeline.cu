@@ -173,7 +173,7 @@ int sample_threshold_tc(molr_ctx* ctx, int mode, const int8_t* scodes, const flo
                         const int8_t* qc, int64_t n_rank, Scratch& ss, uint32_t* tkey, cudaStream_t s) {
   const bool raw = mode == MOLR_S1_INT8_RAW;
   const double p = double(n_rank) / double(lam);
-  int64_t lam0 = (int64_t)std::ceil(48.0 / p);
+  int64_t lam0 = (int64_t)std::ceil(16.0 / p);
   lam0 = (lam0 + 255) / 256 * 256;
   if (!getenv("MOLR_NO_PILOT") && lam0 * 4 <= lam) {
     const double mu = double(lam0) * p;
