@@ -5,7 +5,7 @@ import sys
 
 import numpy as np
 
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 os.environ["MOLR_TRACE_MOL"] = "/tmp/mol_trace.bin"
 from tests.test_gpu_parity import _prod_gating, _synthetic_prod_cache  # noqa: E402
 from paper_2306_04039_b200.mol import batch_score_all  # noqa: E402
