@@ -118,6 +118,12 @@ int molr_cache_read(const molr_cache* cache, int64_t row0, int64_t n, float* ite
 /* storage: the molr_storage bits the cache was built with */
 int molr_cache_info(const molr_cache* cache, int64_t* n_items, int* storage, int64_t* device_bytes);
 
+/* Elementwise primitives (numerics.py:69-81): op 0 sigmoid (scipy expit), 1 silu, 2 silu_grad;
+ * dtype 0 = f32, 2 = f64 (the input's NumPy dtype). */
+int molr_eltwise(molr_ctx* ctx, int op, int dtype, int64_t n, const void* x, void* out, void* stream);
+/* Max-shifted softmax along the last axis (numerics.py:61-66). */
+int molr_softmax_rows(molr_ctx* ctx, int dtype, int64_t rows, int dim, const void* x, void* out, void* stream);
+
 /* Batched user-side query prep (engine.py:113-115 -> model.py:179-208 user_forward, and
  * mol.py:186 user_net): user_embs (B, k_u, d) = per-component L2-normalised user_proj(feats)
  * (when l2_normalized; ZERO_NORM if a norm <= eps), uw (B, G) = user_net(feats).  Both MLPs are

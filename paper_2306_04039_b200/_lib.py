@@ -54,6 +54,8 @@ SIGNATURES = {
     "molr_gating_destroy": [P],
     "molr_component_logits": [P, I, I, I, I, P, P, D, I, P, P],
     "molr_mlp_forward": [P, I, I, I, I, P, P, P, P, P, P],
+    "molr_eltwise": [P, I, I, L, P, P, P],
+    "molr_softmax_rows": [P, I, L, I, P, P, P],
     "molr_query_prep": [P, I, I, P, I, P, P, P, I, I, I, I, P, P, P, I, F, P, P, P],
     "molr_decomposed_gating": [P, P, I, P, P, P, P, P],
     "molr_mol_score": [P, I, I, P, P, I, P, P],

@@ -95,6 +95,37 @@ __global__ void codes_from_ilv_kernel(const int8_t* __restrict__ src, const int3
 
 static int grid_for(molr_ctx* ctx, int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, ctx->num_sms * 16)); }
 
+// Elementwise primitives of numerics.py:52-81 (sigmoid = scipy expit, silu, silu_grad) and the
+// row softmax (numerics.py:61-66), f32 or f64 like the NumPy inputs.  The hot kernels inline
+// their own forms; these serve the drop-in module surface.
+template <class T>
+__device__ __forceinline__ T expit_(T x) {
+  return T(1) / (T(1) + exp(-x));
+}
+template <class T>
+__global__ void eltwise_kernel(int op, int64_t n, const T* __restrict__ x, T* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const T v = x[i], sg = expit_(v);
+    out[i] = op == 0 ? sg : (op == 1 ? v * sg : sg * (T(1) + v * (T(1) - sg)));
+  }
+}
+// one warp per row: max, exp(x - max), sum, divide
+template <class T>
+__global__ void softmax_rows_kernel(int64_t rows, int dim, const T* __restrict__ x, T* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < rows;
+       r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const T* xr = x + r * dim;
+    T mx = -INFINITY;
+    for (int j = lane; j < dim; j += 32) mx = max(mx, xr[j]);
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    T sum = 0;
+    for (int j = lane; j < dim; j += 32) sum += exp(xr[j] - mx);
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    for (int j = lane; j < dim; j += 32) out[r * dim + j] = exp(xr[j] - mx) / sum;
+  }
+}
+
 }  // namespace molr
 
 using namespace molr;
@@ -259,6 +290,41 @@ int molr_query_prep(molr_ctx* ctx, int B, int d_u, const float* feats, int proj_
     if (hb) MOLR_FAIL(MOLR_ERR_ZERO_NORM, "a user component has norm <= eps");
   }
   return finish_outputs(s, {&oe, &ow});
+}
+
+int molr_eltwise(molr_ctx* ctx, int op, int dtype, int64_t n, const void* x, void* out, void* stream) {
+  if (!ctx) MOLR_FAIL(MOLR_ERR_INVALID, "null ctx");
+  if (op < 0 || op > 2 || (dtype != 0 && dtype != 2)) MOLR_FAIL(MOLR_ERR_INVALID, "op %d dtype %d", op, dtype);
+  MOLR_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t s = pick_stream(ctx, stream);
+  if (n <= 0) return MOLR_OK;
+  const size_t es = dtype == 2 ? 8 : 4;
+  In xi;
+  Out o;
+  MOLR_TRY(xi.stage(x, size_t(n) * es, s));
+  MOLR_TRY(o.stage(out, size_t(n) * es, s));
+  if (dtype == 2) eltwise_kernel<double><<<grid_for(ctx, n), 256, 0, s>>>(op, n, xi.as<double>(), o.as<double>());
+  else eltwise_kernel<float><<<grid_for(ctx, n), 256, 0, s>>>(op, n, xi.as<float>(), o.as<float>());
+  MOLR_LAUNCHED(ctx);
+  return finish_outputs(s, {&o});
+}
+
+int molr_softmax_rows(molr_ctx* ctx, int dtype, int64_t rows, int dim, const void* x, void* out, void* stream) {
+  if (!ctx) MOLR_FAIL(MOLR_ERR_INVALID, "null ctx");
+  if (dim < 1 || (dtype != 0 && dtype != 2)) MOLR_FAIL(MOLR_ERR_INVALID, "dim %d dtype %d", dim, dtype);
+  MOLR_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t s = pick_stream(ctx, stream);
+  if (rows <= 0) return MOLR_OK;
+  const size_t es = dtype == 2 ? 8 : 4;
+  In xi;
+  Out o;
+  MOLR_TRY(xi.stage(x, size_t(rows) * dim * es, s));
+  MOLR_TRY(o.stage(out, size_t(rows) * dim * es, s));
+  const int blocks = (int)std::min<int64_t>((rows + 7) / 8, int64_t(ctx->num_sms) * 16);
+  if (dtype == 2) softmax_rows_kernel<double><<<blocks, 256, 0, s>>>(rows, dim, xi.as<double>(), o.as<double>());
+  else softmax_rows_kernel<float><<<blocks, 256, 0, s>>>(rows, dim, xi.as<float>(), o.as<float>());
+  MOLR_LAUNCHED(ctx);
+  return finish_outputs(s, {&o});
 }
 
 int molr_dequantize_rows(molr_ctx* ctx, int64_t rows, int dim, const int8_t* codes, const float* scales, float* out,

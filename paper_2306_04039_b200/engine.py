@@ -44,6 +44,79 @@ def two_stage_top_k(cache, gating: GatingNetwork, user_embs, uw, k: int, hconfig
     return out_ids, out_scores, out_cand
 
 
+class RetrievalEngine:
+    """Drop-in for molr.engine.RetrievalEngine (engine.py:80-147): immutable artifacts plus the
+    two-stage query path with the reference's exact per-query semantics — the first-stage
+    sample comes from make_rng([seed, user_id]) (so repeated identical queries return identical
+    results), candidates from the drop-in h_indexer, the top-k from the drop-in mol_top_k, all
+    on the GPU.  `params` is the reference's TowerParams (read duck-typed: user_table, user_proj,
+    gating, n_users; item_table / item_proj for from_params)."""
+
+    def __init__(self, params, config, cache, hconfig: HIndexerConfig, seed: int = 0):
+        self.params = params
+        self.config = config
+        self.cache = cache
+        self.hconfig = hconfig
+        self.seed = seed
+
+    @classmethod
+    def from_params(cls, params, config, hconfig: HIndexerConfig, *, seed: int = 0) -> "RetrievalEngine":
+        from paper_2306_04039_b200.mol import build_item_cache
+
+        cache = build_item_cache(params.item_table, params.item_proj, params.gating.item_net, config,
+                                 quantized=hconfig.quantized)
+        return cls(params, config, cache, hconfig, seed)
+
+    @property
+    def num_items(self) -> int:
+        return self.cache.num_items
+
+    @property
+    def num_users(self) -> int:
+        return int(getattr(self.params, "n_users", np.asarray(self.params.user_table).shape[0]))
+
+    def query_state(self, user_id: int):
+        """user_forward (model.py:203-208): device query prep of one user."""
+        from paper_2306_04039_b200.errors import OutOfRangeError
+        from paper_2306_04039_b200.mol import QueryState
+
+        if not 0 <= user_id < self.num_users:
+            raise OutOfRangeError(f"user id {user_id} outside [0, {self.num_users})")
+        if getattr(self.params, "compression", None) is not None:
+            raise ValueError("user-side compression maps are outside the B200 path (SURVEY.md §2)")
+        feats = np.asarray(self.params.user_table)[user_id]
+        ue, _ = query_prep(self.params.user_proj, self.params.gating.user_net, feats[None, :], self.config)
+        return QueryState(user_embs=ue[0], gate_features=feats)
+
+    def query(self, user_id: int, k: int, k_prime: int | None = None):
+        """First-stage candidates, then exact MoL top-k (engine.py:117-138)."""
+        from paper_2306_04039_b200.hindexer import h_indexer, stage1_view, with_k_prime
+        from paper_2306_04039_b200.mol import mol_top_k
+        from paper_2306_04039_b200.numerics import make_rng
+
+        hcfg = self.hconfig if k_prime is None else with_k_prime(self.hconfig, k_prime)
+        state = self.query_state(user_id)
+        if hcfg.k_prime >= self.num_items:
+            candidates = np.arange(self.num_items)
+        else:
+            rng = make_rng([self.seed, user_id])
+            stage1_query = state.user_embs.mean(axis=0)
+            candidates = h_indexer(stage1_view(self.cache, hcfg), stage1_query, hcfg, rng).indices
+            if candidates.size < k:
+                candidates = np.arange(self.num_items)
+        ids, scores = mol_top_k(self.cache, self.params.gating, candidates, state, min(k, candidates.size))
+        return [(int(i), float(s)) for i, s in zip(ids, scores)]
+
+    def full_top_k(self, user_id: int, k: int):
+        """Exhaustive MoL ranking, no first stage (engine.py:140-147)."""
+        from paper_2306_04039_b200.mol import mol_top_k
+
+        state = self.query_state(user_id)
+        ids, scores = mol_top_k(self.cache, self.params.gating, np.arange(self.num_items), state,
+                                min(k, self.num_items))
+        return [(int(i), float(s)) for i, s in zip(ids, scores)]
+
+
 def query_prep(user_proj, user_net, user_feats, config, *, stream=None, out_embs=None, out_uw=None):
     """Batched user-side query state on the device (molr_query_prep): user_embs (B, k_u, d) =
     user_components (model.py:179-191: user_proj MLP, per-component L2 norm) and uw (B, G) =

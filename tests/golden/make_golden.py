@@ -245,6 +245,26 @@ def snapshot_case():
                         codes=pc.stage1_q.codes, scales=pc.stage1_q.scales)
 
 
+def engine_case2():
+    """RetrievalEngine.from_params + query / full_top_k (engine.py:80-147) end to end, with the
+    towers, for the drop-in RetrievalEngine test."""
+    cfg = MoLConfig(k_u=4, k_x=4, d=16, tau=20.0, gating_hidden=32, dropout_p=0.0)
+    dims = TowerDims(n_users=40, n_items=3000, d_u=12, d_x=12, proj_hidden=24)
+    params = init_params(dims, cfg, make_rng(4242))
+    hcfg = HIndexerConfig(k_prime=300, sample_ratio=0.1, quantized=True)
+    eng = RetrievalEngine.from_params(params, cfg, hcfg, seed=11)
+    users = np.arange(10)
+    q = [eng.query(int(u), 10) for u in users]
+    f = [eng.full_top_k(int(u), 10) for u in users]
+    out = {"user_table": params.user_table, "item_table": params.item_table,
+           **mlp_arrays("user_proj", params.user_proj), **mlp_arrays("item_proj", params.item_proj),
+           **mlp_arrays("user_net", params.gating.user_net), **mlp_arrays("item_net", params.gating.item_net),
+           **mlp_arrays("cross_net", params.gating.cross_net),
+           "query_ids": np.array([[i for i, _ in r] for r in q]), "query_scores": np.array([[s for _, s in r] for r in q]),
+           "full_ids": np.array([[i for i, _ in r] for r in f]), "full_scores": np.array([[s for _, s in r] for r in f])}
+    np.savez_compressed(os.path.join(OUT, "engine_case2.npz"), **out)
+
+
 def query_case():
     """Production-shape user side (model.py:179-191 user_components, mol.py:186 user_net) for the
     device query-prep parity test."""

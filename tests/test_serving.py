@@ -156,3 +156,59 @@ def test_bench_csv_contract():
     assert all(b >= a - 1e-9 for a, b in zip(rec, rec[1:])), rec
     assert rec[-1] == 1.0
     assert all(float(l.split(",")[2]) > 0 for l in lines[1:])
+
+
+@pytest.mark.gpu
+def test_retrieval_engine_drop_in(golden):
+    """Drop-in RetrievalEngine (engine.py:80-147) vs the reference engine's own query /
+    full_top_k outputs (golden engine_case2: from_params, K'=300, r=0.1, int8, seed 11)."""
+    from types import SimpleNamespace
+
+    import oracle as O
+    from paper_2306_04039_b200.engine import RetrievalEngine
+    from paper_2306_04039_b200.hindexer import HIndexerConfig
+    from paper_2306_04039_b200.mol import GatingNetwork, Mlp, MoLConfig
+
+    g = golden("engine_case2")
+    mk = lambda p: Mlp(g[p + ".w1"], g[p + ".b1"], g[p + ".w2"])  # noqa: E731
+    params = SimpleNamespace(user_table=g["user_table"], item_table=g["item_table"], user_proj=mk("user_proj"),
+                             item_proj=mk("item_proj"), n_users=g["user_table"].shape[0], compression=None,
+                             gating=GatingNetwork(user_net=mk("user_net"), item_net=mk("item_net"),
+                                                  cross_net=mk("cross_net")))
+    cfg = MoLConfig(k_u=4, k_x=4, d=16, tau=20.0, gating_hidden=32, dropout_p=0.0)
+    eng = RetrievalEngine.from_params(params, cfg, HIndexerConfig(k_prime=300, sample_ratio=0.1, quantized=True),
+                                      seed=11)
+    for u in range(10):
+        q = eng.query(u, 10)
+        f = eng.full_top_k(u, 10)
+        assert [i for i, _ in f] == list(g["full_ids"][u]) or O.score_close(
+            np.array([s for _, s in f]), g["full_scores"][u]).all()
+        np.testing.assert_allclose([s for _, s in f], g["full_scores"][u], rtol=1e-3, atol=1e-6)
+        np.testing.assert_allclose([s for _, s in q], g["query_scores"][u], rtol=1e-3, atol=1e-6)
+        assert len(set(i for i, _ in q) & set(g["query_ids"][u].tolist())) >= 9
+    assert eng.query(3, 10) == eng.query(3, 10)  # deterministic per (seed, user)
+    with pytest.raises(Exception):
+        eng.query(10_000, 5)
+
+
+@pytest.mark.gpu
+def test_numerics_primitives_match_reference_forms():
+    """sigmoid / silu / silu_grad / softmax(_rows) (numerics.py:52-81) on the GPU vs NumPy/SciPy."""
+    from scipy.special import expit
+
+    from paper_2306_04039_b200.numerics import sigmoid, silu, silu_grad, softmax, softmax_rows
+
+    rng = np.random.default_rng(0)
+    for dt, tol in ((np.float32, 2e-6), (np.float64, 1e-13)):
+        x = (rng.normal(size=(37, 19)) * 6).astype(dt)
+        s = expit(x)
+        np.testing.assert_allclose(sigmoid(x), s, rtol=tol, atol=tol)
+        np.testing.assert_allclose(silu(x), x * s, rtol=tol, atol=tol)
+        np.testing.assert_allclose(silu_grad(x), s * (1 + x * (1 - s)), rtol=tol, atol=tol)
+        e = np.exp(x - x.max(axis=-1, keepdims=True))
+        np.testing.assert_allclose(softmax_rows(x), e / e.sum(axis=-1, keepdims=True), rtol=tol * 4, atol=tol)
+        assert softmax_rows(x).dtype == dt and silu(x).dtype == dt
+        v = x[0]
+        ev = np.exp(v - v.max())
+        np.testing.assert_allclose(softmax(v), ev / ev.sum(), rtol=tol * 4, atol=tol)
+    assert abs(float(silu(np.float32(1.0))) - 0.731059) < 1e-6  # test_numerics.py:94-105
