@@ -612,7 +612,7 @@ def main():
         "build_s": t_build,
     }
     line["clocks"] = clk.summary()
-    if not args.no_cpu:
+    if not args.no_cpu and world == 1:  # the host baseline is timed on rank 0 at N=1 only
         try:
             cb = cpu_baseline(cfg)
             line["cpu_baseline"] = {k2: cb[k2] for k2 in ("value", "unit", "cores", "kind", "sample")}
