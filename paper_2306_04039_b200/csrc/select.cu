@@ -62,6 +62,7 @@ __device__ void block_radix_select(KeyFn key_of, int64_t n, int64_t rank, uint32
       }
       uint32_t excl = incl - tot;
       int64_t r = s_rank;
+      __syncwarp();  // every lane has read s_rank before the owning lane rewrites it
       if ((int64_t)excl < r && r <= (int64_t)incl) {  // the lane whose range contains rank
         uint32_t run = excl;
         for (int j = 0; j < 8; ++j) {
