@@ -277,7 +277,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) s1_tc_kernel(Params P) {
         const uint32_t tm = tmem_base + buf * 256 + w * 64 + tlane;
         mbar_wait(tfull(buf), uint32_t((jc >> 1) & 1));
         tc_fence_after();
-        if (WRITE) {
+        // warps whose 32 query rows are all padding (small batches) have nothing to test or write
+        const bool live = qb * QB + quarter * 32 < P.B;
+        if (!live) {
+        } else if (WRITE) {
 #pragma unroll 1
           for (int cc = 0; cc < 2; ++cc) {
             uint32_t a[32];
