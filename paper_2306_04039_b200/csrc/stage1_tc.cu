@@ -423,6 +423,231 @@ __global__ void __launch_bounds__(NTHREADS, 1) s1_tc_kernel(Params P) {
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
 }
 
+// ---------------------------------------------------------------------------------------------
+// Small batches (B <= 32): items in M, queries in N.  With a 128-query M block a batch of a few
+// queries leaves most TMEM lanes (and so most epilogue warps) idle and one warp walks all 64
+// columns of its quarter serially; swapping the operands puts 128 items in the TMEM lanes and the
+// (<= 32) queries in the columns, so all 16 epilogue warps share every tile: warp (w, quarter)
+// owns item rows (w & 1) * 128 + 32 * quarter + lane and queries [16 (w >> 1), +16).
+// Per tile: two M=128 x N=32 x K=64 MMA pairs into one of two 64-column TMEM buffers.
+constexpr int SB = 32;          // queries per small launch (MMA N)
+constexpr int S_NSTAGE = 8;
+constexpr int S_OFF_A = 0;      // 32 x 64 B query codes (interleave), 2 KB
+constexpr int S_OFF_RING = 2048;
+constexpr int S_OFF_T = S_OFF_RING + S_NSTAGE * SZ_STAGE;
+constexpr int S_OFF_CNT = S_OFF_T + SB * 4;
+constexpr int S_OFF_BAR = S_OFF_CNT + SB * 4;
+constexpr int S_OFF_TMEM = S_OFF_BAR + (2 * S_NSTAGE + 4) * 8;
+constexpr int S_SMEM_BYTES = S_OFF_TMEM + 16;
+constexpr uint32_t IDESC_I8_S = (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(SB >> 3) << 17) | (uint32_t(128 >> 4) << 24);
+
+#define TMEM_LD16(taddr, r)                                                                                          \
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];" \
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),       \
+                 "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])   \
+               : "r"(taddr))
+#define TMEM_WAIT16(r)                                                                                               \
+  asm volatile("tcgen05.wait::ld.sync.aligned;"                                                                      \
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),     \
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15])  \
+               :                                                                                                     \
+               : "memory")
+
+__device__ __forceinline__ void mma_i8_s(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(IDESC_I8_S), "r"(accum)
+      : "memory");
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(NTHREADS, 1) s1_small_kernel(Params P) {
+  constexpr bool WRITE = MODE == WRITE_SCALED || MODE == WRITE_RAW;
+  constexpr bool KEYS = MODE == KEYS_SCALED || MODE == KEYS_RAW;
+  constexpr bool RAW = (MODE == FILTER_RAW || MODE == WRITE_RAW || MODE == KEYS_RAW);
+  extern __shared__ __align__(1024) uint8_t sm[];
+  const uint32_t sbase = smem_u32(sm);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t ntiles = (P.n + NT - 1) / NT;
+  const int64_t tile_lo = (int64_t(blockIdx.x) * ntiles) / gridDim.x;
+  const int64_t tile_hi = (int64_t(blockIdx.x + 1) * ntiles) / gridDim.x;
+  auto bar = [&](int i) { return sbase + S_OFF_BAR + 8 * i; };
+  auto full_bar = [&](int s) { return bar(s); };
+  auto empty_bar = [&](int s) { return bar(S_NSTAGE + s); };
+  auto tfull = [&](int e) { return bar(2 * S_NSTAGE + e); };
+  auto tempty = [&](int e) { return bar(2 * S_NSTAGE + 2 + e); };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + S_OFF_TMEM);
+  uint32_t* scnt = reinterpret_cast<uint32_t*>(sm + S_OFF_CNT);
+
+  for (int i = threadIdx.x; i < SB * 4; i += blockDim.x) {
+    const int q = i >> 2, c = i & 3;
+    int4 v = make_int4(0, 0, 0, 0);
+    if (q < P.B) v = __ldg(reinterpret_cast<const int4*>(P.qcodes + int64_t(q) * 64) + c);
+    *reinterpret_cast<int4*>(sm + S_OFF_A + (q >> 3) * 512 + c * 128 + (q & 7) * 16) = v;
+  }
+  if (threadIdx.x < SB) {
+    const int q = threadIdx.x;
+    uint32_t t = 0;
+    if (!WRITE && q < P.B) {
+      // the exact per-query bound: scaled -> fl(acc * scale) >= tfe (strict as the next float
+      // above t); raw -> acc >= t (+1 when strict)
+      const uint32_t traw = RAW ? uint32_t(key_i32(__ldg(P.tkeys + q))) : __float_as_uint(key_f32(__ldg(P.tkeys + q)));
+      if (RAW) {
+        t = uint32_t(int32_t(traw) + (P.strict ? 1 : 0));
+      } else {
+        const float tf = __uint_as_float(traw);
+        t = P.strict ? (tf >= 0.f ? (tf == 0.f ? 1u : traw + 1u) : traw - 1u) : traw;
+      }
+    }
+    reinterpret_cast<uint32_t*>(sm + S_OFF_T)[q] = t;
+    scnt[q] = 0;
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S_NSTAGE; ++s) {
+      mbar_init(full_bar(s), 1);
+      mbar_init(empty_bar(s), 1 + NEPI * 128);
+    }
+    for (int e = 0; e < 2; ++e) {
+      mbar_init(tfull(e), 1);
+      mbar_init(tempty(e), NEPI * 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)), "r"(128));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t tile = tile_lo; tile < tile_hi; ++tile) {
+        mbar_wait(empty_bar(stage), phase ^ 1);
+        const uint32_t st = sbase + S_OFF_RING + stage * SZ_STAGE;
+        mbar_arrive_expect_tx(full_bar(stage), SZ_CODES + NT * 4 + ((WRITE || KEYS) ? 0 : NT * 4));
+        bulk_g2s(st, P.codes + tile * SZ_CODES, SZ_CODES, full_bar(stage));
+        bulk_g2s(st + ST_SC, P.scales + tile * NT, NT * 4, full_bar(stage));
+        if (!WRITE && !KEYS) bulk_g2s(st + ST_PERM, P.perm + tile * NT, NT * 4, full_bar(stage));
+        if (++stage == S_NSTAGE) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      uint32_t jc = 0;
+      const uint32_t at = sbase + S_OFF_A;
+      for (int64_t tile = tile_lo; tile < tile_hi; ++tile, ++jc) {
+        mbar_wait(full_bar(stage), phase);
+        const int buf = int(jc & 1);
+        mbar_wait(tempty(buf), ((jc >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t bt = sbase + S_OFF_RING + stage * SZ_STAGE;
+#pragma unroll
+        for (int mb = 0; mb < 2; ++mb) {  // item rows [128 mb, 128 mb + 128) -> columns [32 mb, +32)
+          mma_i8_s(tmem_base + buf * 64 + mb * 32, desc_ilv(bt + mb * 8192), desc_ilv(at), 0);
+          mma_i8_s(tmem_base + buf * 64 + mb * 32, desc_ilv(bt + mb * 8192 + 256), desc_ilv(at + 256), 1);
+        }
+        mma_commit(tfull(buf));
+        mma_commit(empty_bar(stage));
+        if (++stage == S_NSTAGE) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    const int w = (warp - 2) >> 2;
+    const int quarter = warp & 3;
+    const int mb = w & 1, qh = w >> 1;
+    const int r = mb * 128 + quarter * 32 + lane;  // this thread's item row within the tile
+    const int nq = min(16, P.B - 16 * qh);          // live query columns of this warp
+    const uint32_t* tq = reinterpret_cast<const uint32_t*>(sm + S_OFF_T) + 16 * qh;
+    uint32_t tv[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) tv[j] = tq[j];
+    int stage = 0;
+    uint32_t phase = 0;
+    int64_t jc = 0;
+    int32_t* cand_cta = P.cand ? P.cand + int64_t(blockIdx.x) * P.seg : nullptr;
+    for (int64_t tile = tile_lo; tile < tile_hi; ++tile, ++jc) {
+      const int buf = int(jc & 1);
+      mbar_wait(full_bar(stage), phase);
+      mbar_wait(tfull(buf), uint32_t((jc >> 1) & 1));
+      tc_fence_after();
+      if (nq > 0) {
+        const uint8_t* st = sm + S_OFF_RING + stage * SZ_STAGE;
+        const float s = reinterpret_cast<const float*>(st + ST_SC)[r];
+        const bool valid = tile * NT + r < P.n;
+        uint32_t a[16];
+        TMEM_LD16(tmem_base + buf * 64 + mb * 32 + qh * 16 + ((uint32_t)(quarter * 32) << 16), a);
+        TMEM_WAIT16(a);
+        if (WRITE) {
+          if (valid) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (j < nq) {
+                const int64_t o = int64_t(16 * qh + j) * P.ld + tile * NT + r;
+                if (RAW) reinterpret_cast<int32_t*>(P.out)[o] = int32_t(a[j]);
+                else reinterpret_cast<float*>(P.out)[o] = __fmul_rn((float)int32_t(a[j]), s);
+              }
+          }
+        } else {
+          uint32_t m = 0;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const bool pass = RAW ? int32_t(a[j]) >= int32_t(tv[j]) : __fmul_rn((float)int32_t(a[j]), s) >= __uint_as_float(tv[j]);
+            m |= uint32_t(pass && j < nq) << j;
+          }
+          if (!valid) m = 0;
+          if (__any_sync(0xffffffffu, m != 0)) {
+            const int32_t id = KEYS ? 0 : reinterpret_cast<const int32_t*>(st + ST_PERM)[r];
+            while (m) {
+              const int j = __ffs(m) - 1;
+              m &= m - 1;
+              uint32_t accv = 0;
+#pragma unroll
+              for (int jj = 0; jj < 16; ++jj) accv = (jj == j) ? a[jj] : accv;
+              const int q = 16 * qh + j;
+              const uint32_t pos = atomicAdd(scnt + q, 1u);
+              if ((int64_t)pos < P.seg) {
+                int32_t v = id;
+                if (KEYS) v = int32_t(RAW ? i32_key(int32_t(accv)) : f32_key(__fmul_rn((float)int32_t(accv), s)));
+                cand_cta[int64_t(q) * P.cap + pos] = v;
+              }
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(tempty(buf));
+      mbar_arrive(empty_bar(stage));
+      if (++stage == S_NSTAGE) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (!WRITE)
+    for (int q = threadIdx.x; q < P.B; q += blockDim.x) P.cta_counts[int64_t(q) * gridDim.x + blockIdx.x] = int32_t(scnt[q]);
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(128));
+}
+
 // Concatenate the per-CTA segments of each query's candidate list (row b: G segments of `seg`
 // entries at src + b*cap_in + g*seg, counts cnt[b*G + g]) into dst + b*cap_out; counts[b] = the
 // true total (may exceed cap_out); *max_cta = the largest per-CTA count (overflow if > seg).
@@ -506,19 +731,32 @@ int s1_tc_scan(molr_ctx* ctx, int mode, const int8_t* codes, const float* scales
       }
       P.out = out ? reinterpret_cast<char*>(out) + int64_t(b0) * ld * 4 : nullptr;
       P.ld = ld;
+      const bool small = Bc <= SB && !getenv("MOLR_S1_NO_SMALL");
       auto launch = [&](auto kern) -> int {
-        MOLR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
-        kern<<<grid, NTHREADS, SMEM_BYTES, s>>>(P);
+        const int bytes = small ? S_SMEM_BYTES : SMEM_BYTES;
+        MOLR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+        kern<<<grid, NTHREADS, bytes, s>>>(P);
         MOLR_LAUNCHED(ctx);
         return MOLR_OK;
       };
-      switch (m) {
-        case FILTER_SCALED: MOLR_TRY(launch(s1_tc_kernel<FILTER_SCALED>)); break;
-        case FILTER_RAW: MOLR_TRY(launch(s1_tc_kernel<FILTER_RAW>)); break;
-        case WRITE_SCALED: MOLR_TRY(launch(s1_tc_kernel<WRITE_SCALED>)); break;
-        case WRITE_RAW: MOLR_TRY(launch(s1_tc_kernel<WRITE_RAW>)); break;
-        case KEYS_SCALED: MOLR_TRY(launch(s1_tc_kernel<KEYS_SCALED>)); break;
-        default: MOLR_TRY(launch(s1_tc_kernel<KEYS_RAW>)); break;
+      if (small) {
+        switch (m) {
+          case FILTER_SCALED: MOLR_TRY(launch(s1_small_kernel<FILTER_SCALED>)); break;
+          case FILTER_RAW: MOLR_TRY(launch(s1_small_kernel<FILTER_RAW>)); break;
+          case WRITE_SCALED: MOLR_TRY(launch(s1_small_kernel<WRITE_SCALED>)); break;
+          case WRITE_RAW: MOLR_TRY(launch(s1_small_kernel<WRITE_RAW>)); break;
+          case KEYS_SCALED: MOLR_TRY(launch(s1_small_kernel<KEYS_SCALED>)); break;
+          default: MOLR_TRY(launch(s1_small_kernel<KEYS_RAW>)); break;
+        }
+      } else {
+        switch (m) {
+          case FILTER_SCALED: MOLR_TRY(launch(s1_tc_kernel<FILTER_SCALED>)); break;
+          case FILTER_RAW: MOLR_TRY(launch(s1_tc_kernel<FILTER_RAW>)); break;
+          case WRITE_SCALED: MOLR_TRY(launch(s1_tc_kernel<WRITE_SCALED>)); break;
+          case WRITE_RAW: MOLR_TRY(launch(s1_tc_kernel<WRITE_RAW>)); break;
+          case KEYS_SCALED: MOLR_TRY(launch(s1_tc_kernel<KEYS_SCALED>)); break;
+          default: MOLR_TRY(launch(s1_tc_kernel<KEYS_RAW>)); break;
+        }
       }
       if (!filter) break;
       compact_segments_kernel<<<Bc, 256, 0, s>>>(grid, seg, P.cap, P.cand, P.cta_counts, cap, cand + int64_t(b0) * cap,
