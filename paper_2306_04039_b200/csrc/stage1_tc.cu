@@ -430,16 +430,19 @@ __global__ void __launch_bounds__(NTHREADS, 1) s1_tc_kernel(Params P) {
 // (<= 32) queries in the columns, so all 16 epilogue warps share every tile: warp (w, quarter)
 // owns item rows (w & 1) * 128 + 32 * quarter + lane and queries [16 (w >> 1), +16).
 // Per tile: two M=128 x N=32 x K=64 MMA pairs into one of two 64-column TMEM buffers.
-constexpr int SB = 32;          // queries per small launch (MMA N)
+constexpr int SB = 32;          // largest small launch (MMA N = 16 or 32 queries)
 constexpr int S_NSTAGE = 8;
-constexpr int S_OFF_A = 0;      // 32 x 64 B query codes (interleave), 2 KB
-constexpr int S_OFF_RING = 2048;
+constexpr int S_OFF_A = 0;      // <= 64 x 64 B query codes (interleave), 4 KB
+constexpr int S_OFF_RING = 4096;
 constexpr int S_OFF_T = S_OFF_RING + S_NSTAGE * SZ_STAGE;
 constexpr int S_OFF_CNT = S_OFF_T + SB * 4;
 constexpr int S_OFF_BAR = S_OFF_CNT + SB * 4;
-constexpr int S_OFF_TMEM = S_OFF_BAR + (2 * S_NSTAGE + 4) * 8;
+constexpr int S_OFF_TMEM = S_OFF_BAR + (2 * S_NSTAGE + 16) * 8;
 constexpr int S_SMEM_BYTES = S_OFF_TMEM + 16;
-constexpr uint32_t IDESC_I8_S = (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(SB >> 3) << 17) | (uint32_t(128 >> 4) << 24);
+template <int SBQ>
+constexpr uint32_t idesc_i8_s() {
+  return (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(SBQ >> 3) << 17) | (uint32_t(128 >> 4) << 24);
+}
 
 #define TMEM_LD16(taddr, r)                                                                                          \
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];" \
@@ -453,17 +456,26 @@ constexpr uint32_t IDESC_I8_S = (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(S
                :                                                                                                     \
                : "memory")
 
+template <int SBQ>
 __device__ __forceinline__ void mma_i8_s(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t accum) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "l"(a), "l"(b), "r"(IDESC_I8_S), "r"(accum)
+      "l"(a), "l"(b), "r"(idesc_i8_s<SBQ>()), "r"(accum)
       : "memory");
 }
 
-template <int MODE>
+template <int MODE, int SBQ>
 __global__ void __launch_bounds__(NTHREADS, 1) s1_small_kernel(Params P) {
+  // SBQ = 16: every warp tests all (<= 16) queries and the two warp halves take alternate tiles
+  // (two tiles in flight per warp slot); SBQ = 32: the halves split the queries 16 / 16
+  constexpr bool SPLIT_T = SBQ == 16;
+  constexpr int QW = SPLIT_T ? SBQ : SBQ / 2;  // query columns per epilogue warp
+  constexpr int NB = 8;                // TMEM accumulator buffers: the MMA of later tiles never
+                                       // waits for this tile's epilogue
+  constexpr uint32_t TCOLS = NB * 2 * SBQ;
+  constexpr int NARRIVE = SPLIT_T ? NEPI * 64 : NEPI * 128;  // epilogue threads per tile
   constexpr bool WRITE = MODE == WRITE_SCALED || MODE == WRITE_RAW;
   constexpr bool KEYS = MODE == KEYS_SCALED || MODE == KEYS_RAW;
   constexpr bool RAW = (MODE == FILTER_RAW || MODE == WRITE_RAW || MODE == KEYS_RAW);
@@ -477,17 +489,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) s1_small_kernel(Params P) {
   auto full_bar = [&](int s) { return bar(s); };
   auto empty_bar = [&](int s) { return bar(S_NSTAGE + s); };
   auto tfull = [&](int e) { return bar(2 * S_NSTAGE + e); };
-  auto tempty = [&](int e) { return bar(2 * S_NSTAGE + 2 + e); };
+  auto tempty = [&](int e) { return bar(2 * S_NSTAGE + 8 + e); };
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + S_OFF_TMEM);
   uint32_t* scnt = reinterpret_cast<uint32_t*>(sm + S_OFF_CNT);
 
-  for (int i = threadIdx.x; i < SB * 4; i += blockDim.x) {
+  for (int i = threadIdx.x; i < SBQ * 4; i += blockDim.x) {
     const int q = i >> 2, c = i & 3;
     int4 v = make_int4(0, 0, 0, 0);
     if (q < P.B) v = __ldg(reinterpret_cast<const int4*>(P.qcodes + int64_t(q) * 64) + c);
     *reinterpret_cast<int4*>(sm + S_OFF_A + (q >> 3) * 512 + c * 128 + (q & 7) * 16) = v;
   }
-  if (threadIdx.x < SB) {
+  if (threadIdx.x < SBQ) {
     const int q = threadIdx.x;
     uint32_t t = 0;
     if (!WRITE && q < P.B) {
@@ -507,16 +519,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) s1_small_kernel(Params P) {
   if (threadIdx.x == 0) {
     for (int s = 0; s < S_NSTAGE; ++s) {
       mbar_init(full_bar(s), 1);
-      mbar_init(empty_bar(s), 1 + NEPI * 128);
+      mbar_init(empty_bar(s), 1 + NARRIVE);
     }
-    for (int e = 0; e < 2; ++e) {
+    for (int e = 0; e < NB; ++e) {
       mbar_init(tfull(e), 1);
-      mbar_init(tempty(e), NEPI * 128);
+      mbar_init(tempty(e), NARRIVE);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)), "r"(128));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)), "r"(TCOLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   fence_async_smem();
@@ -550,14 +562,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) s1_small_kernel(Params P) {
       const uint32_t at = sbase + S_OFF_A;
       for (int64_t tile = tile_lo; tile < tile_hi; ++tile, ++jc) {
         mbar_wait(full_bar(stage), phase);
-        const int buf = int(jc & 1);
-        mbar_wait(tempty(buf), ((jc >> 1) & 1) ^ 1);
+        const int buf = int(jc % NB);
+        mbar_wait(tempty(buf), ((jc / NB) & 1) ^ 1);
         tc_fence_after();
         const uint32_t bt = sbase + S_OFF_RING + stage * SZ_STAGE;
 #pragma unroll
-        for (int mb = 0; mb < 2; ++mb) {  // item rows [128 mb, 128 mb + 128) -> columns [32 mb, +32)
-          mma_i8_s(tmem_base + buf * 64 + mb * 32, desc_ilv(bt + mb * 8192), desc_ilv(at), 0);
-          mma_i8_s(tmem_base + buf * 64 + mb * 32, desc_ilv(bt + mb * 8192 + 256), desc_ilv(at + 256), 1);
+        for (int mb = 0; mb < 2; ++mb) {  // item rows [128 mb, 128 mb + 128) -> columns [SBQ mb, +SBQ)
+          mma_i8_s<SBQ>(tmem_base + buf * 2 * SBQ + mb * SBQ, desc_ilv(bt + mb * 8192), desc_ilv(at), 0);
+          mma_i8_s<SBQ>(tmem_base + buf * 2 * SBQ + mb * SBQ, desc_ilv(bt + mb * 8192 + 256), desc_ilv(at + 256), 1);
         }
         mma_commit(tfull(buf));
         mma_commit(empty_bar(stage));
@@ -573,33 +585,43 @@ __global__ void __launch_bounds__(NTHREADS, 1) s1_small_kernel(Params P) {
     const int quarter = warp & 3;
     const int mb = w & 1, qh = w >> 1;
     const int r = mb * 128 + quarter * 32 + lane;  // this thread's item row within the tile
-    const int nq = min(16, P.B - 16 * qh);          // live query columns of this warp
-    const uint32_t* tq = reinterpret_cast<const uint32_t*>(sm + S_OFF_T) + 16 * qh;
-    uint32_t tv[16];
+    const int qo = SPLIT_T ? 0 : QW * qh;          // first query column of this warp
+    const int nq = min(QW, P.B - qo);              // live query columns of this warp
+    const uint32_t* tq = reinterpret_cast<const uint32_t*>(sm + S_OFF_T) + qo;
+    uint32_t tv[QW];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) tv[j] = tq[j];
+    for (int j = 0; j < QW; ++j) tv[j] = tq[j];
     int stage = 0;
     uint32_t phase = 0;
     int64_t jc = 0;
     int32_t* cand_cta = P.cand ? P.cand + int64_t(blockIdx.x) * P.seg : nullptr;
     for (int64_t tile = tile_lo; tile < tile_hi; ++tile, ++jc) {
-      const int buf = int(jc & 1);
+      const int buf = int(jc % NB);
+      if (SPLIT_T && int(jc & 1) != qh) {  // the other half's tile (stage and buffer parity = jc's)
+        if (++stage == S_NSTAGE) {
+          stage = 0;
+          phase ^= 1;
+        }
+        continue;
+      }
       mbar_wait(full_bar(stage), phase);
-      mbar_wait(tfull(buf), uint32_t((jc >> 1) & 1));
+      mbar_wait(tfull(buf), uint32_t((jc / NB) & 1));
       tc_fence_after();
       if (nq > 0) {
         const uint8_t* st = sm + S_OFF_RING + stage * SZ_STAGE;
         const float s = reinterpret_cast<const float*>(st + ST_SC)[r];
         const bool valid = tile * NT + r < P.n;
-        uint32_t a[16];
-        TMEM_LD16(tmem_base + buf * 64 + mb * 32 + qh * 16 + ((uint32_t)(quarter * 32) << 16), a);
+        uint32_t a[QW];
+        const uint32_t ta = tmem_base + buf * 2 * SBQ + mb * SBQ + qo + ((uint32_t)(quarter * 32) << 16);
+        static_assert(QW == 16, "one 16-column TMEM load per warp");
+        TMEM_LD16(ta, a);
         TMEM_WAIT16(a);
         if (WRITE) {
           if (valid) {
 #pragma unroll
-            for (int j = 0; j < 16; ++j)
+            for (int j = 0; j < QW; ++j)
               if (j < nq) {
-                const int64_t o = int64_t(16 * qh + j) * P.ld + tile * NT + r;
+                const int64_t o = int64_t(qo + j) * P.ld + tile * NT + r;
                 if (RAW) reinterpret_cast<int32_t*>(P.out)[o] = int32_t(a[j]);
                 else reinterpret_cast<float*>(P.out)[o] = __fmul_rn((float)int32_t(a[j]), s);
               }
@@ -607,7 +629,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) s1_small_kernel(Params P) {
         } else {
           uint32_t m = 0;
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
+          for (int j = 0; j < QW; ++j) {
             const bool pass = RAW ? int32_t(a[j]) >= int32_t(tv[j]) : __fmul_rn((float)int32_t(a[j]), s) >= __uint_as_float(tv[j]);
             m |= uint32_t(pass && j < nq) << j;
           }
@@ -619,8 +641,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) s1_small_kernel(Params P) {
               m &= m - 1;
               uint32_t accv = 0;
 #pragma unroll
-              for (int jj = 0; jj < 16; ++jj) accv = (jj == j) ? a[jj] : accv;
-              const int q = 16 * qh + j;
+              for (int jj = 0; jj < QW; ++jj) accv = (jj == j) ? a[jj] : accv;
+              const int q = qo + j;
               const uint32_t pos = atomicAdd(scnt + q, 1u);
               if ((int64_t)pos < P.seg) {
                 int32_t v = id;
@@ -645,7 +667,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) s1_small_kernel(Params P) {
   tc_fence_after();
   if (!WRITE)
     for (int q = threadIdx.x; q < P.B; q += blockDim.x) P.cta_counts[int64_t(q) * gridDim.x + blockIdx.x] = int32_t(scnt[q]);
-  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(128));
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TCOLS));
 }
 
 // Concatenate the per-CTA segments of each query's candidate list (row b: G segments of `seg`
@@ -740,13 +762,14 @@ int s1_tc_scan(molr_ctx* ctx, int mode, const int8_t* codes, const float* scales
         return MOLR_OK;
       };
       if (small) {
+        auto pick = [&](auto k16, auto k32) { return Bc <= 16 ? launch(k16) : launch(k32); };
         switch (m) {
-          case FILTER_SCALED: MOLR_TRY(launch(s1_small_kernel<FILTER_SCALED>)); break;
-          case FILTER_RAW: MOLR_TRY(launch(s1_small_kernel<FILTER_RAW>)); break;
-          case WRITE_SCALED: MOLR_TRY(launch(s1_small_kernel<WRITE_SCALED>)); break;
-          case WRITE_RAW: MOLR_TRY(launch(s1_small_kernel<WRITE_RAW>)); break;
-          case KEYS_SCALED: MOLR_TRY(launch(s1_small_kernel<KEYS_SCALED>)); break;
-          default: MOLR_TRY(launch(s1_small_kernel<KEYS_RAW>)); break;
+          case FILTER_SCALED: MOLR_TRY(pick(s1_small_kernel<FILTER_SCALED, 16>, s1_small_kernel<FILTER_SCALED, 32>)); break;
+          case FILTER_RAW: MOLR_TRY(pick(s1_small_kernel<FILTER_RAW, 16>, s1_small_kernel<FILTER_RAW, 32>)); break;
+          case WRITE_SCALED: MOLR_TRY(pick(s1_small_kernel<WRITE_SCALED, 16>, s1_small_kernel<WRITE_SCALED, 32>)); break;
+          case WRITE_RAW: MOLR_TRY(pick(s1_small_kernel<WRITE_RAW, 16>, s1_small_kernel<WRITE_RAW, 32>)); break;
+          case KEYS_SCALED: MOLR_TRY(pick(s1_small_kernel<KEYS_SCALED, 16>, s1_small_kernel<KEYS_SCALED, 32>)); break;
+          default: MOLR_TRY(pick(s1_small_kernel<KEYS_RAW, 16>, s1_small_kernel<KEYS_RAW, 32>)); break;
         }
       } else {
         switch (m) {

@@ -544,6 +544,38 @@ def test_batched_stage1_tc_counts_exact(strict, raw):
         assert cand[u] == c_ids.size, (u, cand[u], c_ids.size)
 
 
+@pytest.mark.parametrize("nb", [1, 5, 16, 17, 32, 33])
+def test_batched_stage1_small_batch_kernel(nb, monkeypatch):
+    """Small batches (B <= 32) take the items-in-M stage-1 kernel (queries in the MMA N dimension):
+    exact passer counts vs the oracle at lambda = X for every comparator / ordering mode, and the
+    sampled path (pilot WRITE + KEYS scans) identical to the 128-query-block kernel."""
+    from paper_2306_04039_b200.engine import two_stage_top_k
+    from paper_2306_04039_b200.hindexer import HIndexerConfig
+
+    cache, syn, ue, feats = _synthetic_prod_cache(120_000, seed=31, n_users=64)
+    gating, og = _prod_gating(syn)
+    ue, feats = ue[:nb], feats[:nb]
+    uw = gating.user_net(feats)
+    X = cache.num_items
+    q = O.Quant(cache.stage1_q.codes, cache.stage1_q.scales)
+    for strict, raw in ((False, False), (True, False), (False, True)):
+        comp = "strict" if strict else "inclusive"
+        hcfg = HIndexerConfig(k_prime=1500, lam=X, quantized=True, comparator=comp, raw_int_ordering=raw)
+        ids, sc, cand = two_stage_top_k(cache, gating, ue, uw, 10, hcfg, seed=1)
+        for u in range(nb):
+            c_ids, _, _ = O.h_indexer(q, ue[u].mean(axis=0), 1500, O.make_rng(0), lam=X, comparator=comp,
+                                      raw_int_ordering=raw)
+            assert cand[u] == c_ids.size, (strict, raw, u, cand[u], c_ids.size)
+        hs = HIndexerConfig(k_prime=1500, sample_ratio=0.1, quantized=True, comparator=comp, raw_int_ordering=raw)
+        monkeypatch.delenv("MOLR_S1_NO_SMALL", raising=False)
+        a = two_stage_top_k(cache, gating, ue, uw, 20, hs, seed=5)
+        monkeypatch.setenv("MOLR_S1_NO_SMALL", "1")
+        b = two_stage_top_k(cache, gating, ue, uw, 20, hs, seed=5)
+        monkeypatch.delenv("MOLR_S1_NO_SMALL")
+        for x, y in zip(a, b):
+            np.testing.assert_array_equal(x, y)
+
+
 def test_batched_two_stage_recall_device_sample():
     """Device-drawn sample (lambda = 1% of X): candidate counts near K' and top-100 recall vs the
     oracle's exact MoL top-100 >= 0.99 (north-star bar), 100k items."""

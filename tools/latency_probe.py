@@ -14,7 +14,7 @@ cfg, cache = Bm.build_shard(model, X, 0, X, seed=11, dev=dev, lib=lib, ctx=ctx)
 gh = _gating_handle(GatingNetwork(Mlp(*model['user_net']), Mlp(*model['item_net']), Mlp(*model['cross_net'])))
 feats_h, feats_d = Bm.make_queries(model, 64, 1, dev)
 W = {k: [torch.from_numpy(a).to(dev) for a in v] for k, v in model.items()}
-for B in (1, 8, 64):
+for B in (1, 8, 32, 64, 128):
     ue = torch.empty((B, 8, 64), device=dev); uw = torch.empty((B, 64), device=dev)
     ids = torch.empty((B, 100), dtype=torch.int64, device=dev); sc = torch.empty((B, 100), device=dev)
     def run(i):
