@@ -84,7 +84,7 @@ def synthetic_model(seed=4242):
             "user_net": _mlp(rng, D_U, H, G), "item_net": _mlp(rng, D_X, H, G), "cross_net": _mlp(rng, G, H, G)}
 
 
-def build_shard(model, X, lo, hi, seed, dev, lib, ctx):
+def build_shard(model, X, lo, hi, seed, dev, lib, ctx, storage=None):
     """Build rows [lo, hi) of the global corpus on the device into a DeviceItemCache through the
     product's fused cache build (molr_cache_build_rows: item_proj MLP -> L2 norm -> item_net ->
     bf16 storage rounding -> stage-1 mean -> int8), from a synthetic item table drawn on the
@@ -96,7 +96,7 @@ def build_shard(model, X, lo, hi, seed, dev, lib, ctx):
     from paper_2306_04039_b200.numerics import DEFAULT_EPS
 
     cfg = MoLConfig(k_u=K_U, k_x=K_X, d=D, tau=TAU, gating_hidden=H, dropout_p=0.0)
-    cache = DeviceItemCache(cfg, hi - lo, D, L.STORE_S1_INT8)
+    cache = DeviceItemCache(cfg, hi - lo, D, L.STORE_S1_INT8 if storage is None else storage)
     W = {k: [torch.from_numpy(a).to(dev) for a in v] for k, v in model.items()}
     pw, nw = W["item_proj"], W["item_net"]
     s = torch.cuda.current_stream().cuda_stream

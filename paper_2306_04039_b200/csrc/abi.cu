@@ -349,9 +349,11 @@ int molr_cache_fill(molr_cache* c, int64_t row0, int64_t n, const float* embs, c
         MOLR_LAUNCHED(ctx);
       }
     }
-    if (s1 && c->s1_f32)
+    if (s1 && c->s1_f32) {
       MOLR_CUDA(cudaMemcpyAsync(c->s1_f32 + size_t(row0 + r) * c->d1, s1 + r * c->d1,
                                 size_t(m) * c->d1 * 4, cudaMemcpyDefault, s));
+      c->s1_bf_ready.store(0, std::memory_order_release);  // the bf16 image is rebuilt on next use
+    }
     if (codes && c->s1_codes) {
       if (s1_interleaved(c->d1)) {
         In e;
@@ -438,6 +440,9 @@ int molr_cache_destroy(molr_cache* c) {
   cudaFree(c->s1_chunk_mm);
   cudaFree(c->s1_perm);
   cudaFree(c->s1_inv);
+  cudaFree(c->s1_bf);
+  cudaFree(c->s1_bnorm);
+  cudaFree(c->s1_bnmax);
   delete c;
   return MOLR_OK;
 }

@@ -96,7 +96,20 @@ filter_scan_kernel(int64_t n, int dim, const float* __restrict__ vf, const int8_
         const float* v = vf + r * dim;
         const float* q = reinterpret_cast<const float*>(qs) + b * dim;
         float acc = 0.f;
-        for (int k = 0; k < dim; ++k) acc = fmaf(v[k], q[k], acc);
+        if (dim == 64) {  // (the row is re-read from L1 per query; same sequential fmaf chain)
+          const float4* v4 = reinterpret_cast<const float4*>(v);
+          const float4* q4 = reinterpret_cast<const float4*>(q);
+#pragma unroll
+          for (int k = 0; k < 16; ++k) {
+            const float4 x = __ldg(v4 + k), y = q4[k];
+            acc = fmaf(x.x, y.x, acc);
+            acc = fmaf(x.y, y.y, acc);
+            acc = fmaf(x.z, y.z, acc);
+            acc = fmaf(x.w, y.w, acc);
+          }
+        } else {
+          for (int k = 0; k < dim; ++k) acc = fmaf(v[k], q[k], acc);
+        }
         key = f32_key(acc);
       } else {
         int32_t acc = 0;
@@ -480,19 +493,27 @@ int molr_two_stage_top_k(molr_ctx* ctx, const molr_cache* c, const molr_gating* 
     for (int attempt = 0; attempt < 2; ++attempt) {
       MOLR_TRY(cand.alloc(size_t(B) * cap * 4, s));
       MOLR_CUDA(cudaMemsetAsync(counts.p, 0, size_t(B) * 8, s));
-      const int qbytes = mode == MOLR_S1_FLOAT ? B * c->d1 * 4 : B * c->d1;
-      const size_t smem = size_t((B * 4 + 15) / 16) * 16 + qbytes;
-      if (smem > 200 * 1024) MOLR_FAIL(MOLR_ERR_OUT_OF_RANGE, "batch %d too large for one scan", B);
+      const int per_q = mode == MOLR_S1_FLOAT ? c->d1 * 4 : c->d1;
+      const int bchunk = std::max(1, std::min(B, (128 * 1024) / (per_q + 4)));  // queries per launch
       auto launch = [&](auto kern) -> int {
-        MOLR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        int blocks = std::min(div_up(X, 256), ctx->num_sms * std::max(1, int((220 * 1024) / (smem + 1024))));
-        kern<<<blocks, 256, smem, s>>>(X, c->d1, c->s1_f32, c->s1_codes, c->s1_inv, c->s1_scales, B, q.as<float>(),
-                                       qc.as<int8_t>(), tkey.as<uint32_t>(), comparator == MOLR_STRICT, cap,
-                                       cand.as<int32_t>(), counts.as<int64_t>());
-        MOLR_LAUNCHED(ctx);
+        for (int b0 = 0; b0 < B; b0 += bchunk) {
+          const int bb = std::min(bchunk, B - b0);
+          const size_t smem = size_t((bb * 4 + 15) / 16) * 16 + size_t(bb) * per_q;
+          MOLR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+          int blocks = std::min(div_up(X, 256), ctx->num_sms * std::max(1, int((220 * 1024) / (smem + 1024))));
+          kern<<<blocks, 256, smem, s>>>(X, c->d1, c->s1_f32, c->s1_codes, c->s1_inv, c->s1_scales, bb,
+                                         q.as<float>() + size_t(b0) * c->d1, qc.p ? qc.as<int8_t>() + size_t(b0) * c->d1 : nullptr,
+                                         tkey.as<uint32_t>() + b0, comparator == MOLR_STRICT, cap,
+                                         cand.as<int32_t>() + size_t(b0) * cap, counts.as<int64_t>() + b0);
+          MOLR_LAUNCHED(ctx);
+        }
         return MOLR_OK;
       };
-      if (use_tc) {
+      if (s1_bf_supported(c, mode)) {
+        KTimer t(ctx, "stage1_filter_bf16", s, double(B) * X);
+        MOLR_TRY(s1_bf_scan(ctx, c, B, q.as<float>(), tkey.as<uint32_t>(), comparator == MOLR_STRICT, cap,
+                            cand.as<int32_t>(), counts.as<int64_t>(), s));
+      } else if (use_tc) {
         KTimer t(ctx, "stage1_filter_tc", s, double(B) * X);
         MOLR_TRY(s1_tc_scan(ctx, mode, c->s1_codes, c->s1_scales, c->s1_chunk_mm, c->s1_perm, X, B, qc.as<int8_t>(),
                             tkey.as<uint32_t>(), comparator == MOLR_STRICT, cap, cand.as<int32_t>(), counts.as<int64_t>(),

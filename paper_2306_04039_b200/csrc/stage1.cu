@@ -78,7 +78,29 @@ __global__ void scan_scores_kernel(int mode, int64_t n, int dim, const float* __
   __syncthreads();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = rows_idx ? rows_idx[i] : i;
-    if (mode == MOLR_S1_FLOAT) {
+    if (mode == MOLR_S1_FLOAT && dim == 64) {
+      // the row stays in registers across the queries (same sequential fmaf chain)
+      float v[64];
+      const float4* v4 = reinterpret_cast<const float4*>(vf + r * 64);
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const float4 x = __ldg(v4 + k);
+        v[4 * k] = x.x, v[4 * k + 1] = x.y, v[4 * k + 2] = x.z, v[4 * k + 3] = x.w;
+      }
+      for (int b = 0; b < B; ++b) {
+        const float4* q4 = reinterpret_cast<const float4*>(sq) + b * 16;
+        float acc = 0.f;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const float4 y = q4[k];
+          acc = fmaf(v[4 * k], y.x, acc);
+          acc = fmaf(v[4 * k + 1], y.y, acc);
+          acc = fmaf(v[4 * k + 2], y.z, acc);
+          acc = fmaf(v[4 * k + 3], y.w, acc);
+        }
+        reinterpret_cast<float*>(out)[b * ld + i] = acc;
+      }
+    } else if (mode == MOLR_S1_FLOAT) {
       const float* v = vf + r * dim;
       for (int b = 0; b < B; ++b) {
         const float* q = reinterpret_cast<const float*>(sq) + b * dim;

@@ -23,6 +23,11 @@ int encode_rows_tmap(CUtensorMap* tm, const void* base, int64_t rows);
 int chunk_minmax(molr_ctx* ctx, const float* scales, int64_t c0, int64_t c1, float2* mm, cudaStream_t s);
 int s1_update_chunk_mm(molr_cache* c, int64_t row0, int64_t n, cudaStream_t s);
 int s1_seal(molr_cache* c, cudaStream_t s);
+// float view (MOLR_S1_FLOAT) on the tensor cores: bf16 MMA pre-test + exact fp32 re-check of the
+// band the bf16 rounding cannot decide (same candidate set as the fp32 scan)
+bool s1_bf_supported(const molr_cache* c, int mode);
+int s1_bf_scan(molr_ctx* ctx, const molr_cache* c, int B, const float* q, const uint32_t* tkeys, int strict,
+               int64_t cap, int32_t* cand, int64_t* counts, cudaStream_t s);
 int int_to_float_inplace(molr_ctx* ctx, int32_t* p, int64_t n, cudaStream_t s);
 
 }  // namespace molr

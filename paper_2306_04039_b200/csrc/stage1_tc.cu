@@ -704,6 +704,361 @@ __global__ void __launch_bounds__(256) compact_segments_kernel(int G, int64_t se
 
 }  // namespace s1tc
 
+// ---------------------------------------------------------------------------------------------
+// Float view (MOLR_S1_FLOAT, hindexer.py:112 `view @ q` in fp32) on the tensor cores.
+//
+// The reference's float score is an fp32 dot; the product's fp32 definition is the sequential
+// fmaf chain of filter_scan_kernel / scan_scores_kernel (the sample threshold comes from it).
+// bf16(v) . bf16(q) with fp32 accumulation differs from it by at most
+//   |D - s| <= (2^-7 + 2^-16 + 2 * 64 * 2^-24) * sum|v_i q_i| <= EPS * ||v||_2 * ||q||_2
+// (bf16 round-to-nearest: relative error <= 2^-8 per operand; both fp32 accumulations), so per
+// (query, row) with m = EPS ||q|| ||v||:  D >= t + m  -> passes for certain;  D < t - m -> fails
+// for certain; otherwise the row is in the undecided band and is re-scored exactly in fp32 by
+// recheck_band_kernel.  The candidate SET equals the fp32 scan's bit for bit; only the order of
+// the list differs (certain passers in id order, then the re-checked band).
+//
+// Layout: bf16 view in the interleaved K-major layout with 128 B rows (8-row groups of 1 KB),
+// 256-row tiles of 32 KB + 1 KB of row norms + 32 B of chunk max norms per stage; all B <= 1024
+// queries resident as bf16 (128 KB).  Per (tile, 128-query block): 4 x (M=128, N=256, K=16)
+// kind::f16 MMAs into one of two 256-column TMEM buffers; the epilogue is the int8 kernel's with
+// a float max tree and no scale.
+namespace s1bf {
+using s1tc::smem_u32; using s1tc::mbar_init; using s1tc::mbar_arrive; using s1tc::mbar_arrive_expect_tx; using s1tc::mbar_wait;
+using s1tc::bulk_g2s; using s1tc::fence_async_smem; using s1tc::tc_fence_before; using s1tc::tc_fence_after; using s1tc::mma_commit;
+constexpr float EPS = 0.0079f;
+constexpr int NT = 256, QB = 128, MAXQB = 8, NSTAGE = 2, NBUF = 2, NEPI = 4;
+constexpr int SZ_TILE = NT * 128;
+constexpr int ST_NRM = SZ_TILE, ST_CMX = SZ_TILE + NT * 4;
+constexpr int SZ_STAGE = SZ_TILE + NT * 4 + 1024;
+constexpr int OFF_A = 0;
+constexpr int OFF_RING = OFF_A + MAXQB * 16384;
+constexpr int OFF_T = OFF_RING + NSTAGE * SZ_STAGE;
+constexpr int OFF_E = OFF_T + MAXQB * QB * 4;
+constexpr int OFF_CNT = OFF_E + MAXQB * QB * 4;
+constexpr int OFF_BCNT = OFF_CNT + MAXQB * QB * 4;
+constexpr int OFF_BAR = OFF_BCNT + MAXQB * QB * 4;
+constexpr int NBAR = 2 * NSTAGE + 2 * NBUF;
+constexpr int OFF_TMEM = OFF_BAR + NBAR * 8;
+constexpr int SMEM_BYTES = OFF_TMEM + 16;
+constexpr int NTHREADS = 64 + NEPI * 128;
+static_assert(SMEM_BYTES <= 232448, "shared memory");
+constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(NT >> 3) << 17) | (uint32_t(QB >> 4) << 24);
+
+__host__ __device__ __forceinline__ int64_t bf_offset(int64_t r, int k) {  // element offset of v[r][k]
+  return ((r >> 3) << 9) + int64_t(k >> 3) * 64 + ((r & 7) << 3) + (k & 7);
+}
+__device__ __forceinline__ uint64_t desc_bf(uint32_t addr) {  // interleave K-major: LBO 128 B, SBO 1 KB
+  return uint64_t((addr >> 4) & 0x3FFF) | (uint64_t(128 >> 4) << 16) | (uint64_t(1024 >> 4) << 32) | (1ull << 46);
+}
+__device__ __forceinline__ void mma_bf(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(IDESC), "r"(accum)
+      : "memory");
+}
+__device__ __forceinline__ float up_norm(float ss) { return sqrtf(ss) * (1.0f + 1e-6f) + 1e-30f; }
+
+// fp32 rows -> bf16 interleaved image + row norms (padding rows zero)
+__global__ void build_kernel(int64_t X, int64_t xr, const float* __restrict__ v, __nv_bfloat16* __restrict__ out,
+                             float* __restrict__ nrm) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < xr; r += (int64_t)gridDim.x * blockDim.x) {
+    float ss = 0.f;
+    for (int c = 0; c < 8; ++c) {
+      __align__(16) __nv_bfloat16 h[8];
+      for (int j = 0; j < 8; ++j) {
+        const float x = r < X ? v[r * 64 + c * 8 + j] : 0.f;
+        ss = fmaf(x, x, ss);
+        h[j] = __float2bfloat16_rn(x);
+      }
+      *reinterpret_cast<int4*>(out + bf_offset(r, c * 8)) = *reinterpret_cast<const int4*>(h);
+    }
+    nrm[r] = r < X ? up_norm(ss) : 0.f;
+  }
+}
+__global__ void chunk_max_kernel(int64_t nch, const float* __restrict__ nrm, float* __restrict__ cmx) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < nch; c += (int64_t)gridDim.x * blockDim.x) {
+    float m = 0.f;
+    for (int j = 0; j < 32; ++j) m = fmaxf(m, nrm[c * 32 + j]);
+    cmx[c] = m;
+  }
+}
+
+struct Params {
+  const __nv_bfloat16* view;
+  const float* nrm;
+  const float* cmx;
+  int64_t n;
+  int B;
+  const float* q;         // (B, 64) fp32 queries
+  const uint32_t* tkeys;  // (B,) threshold keys
+  int64_t cap, seg;
+  int32_t* cand;          // certain passers: (B, cap) as gridDim.x segments of seg
+  int32_t* band;          // undecided rows, same shape
+  int32_t* cta_counts;    // (B, gridDim.x)
+  int32_t* cta_bcounts;
+};
+
+__global__ void __launch_bounds__(NTHREADS, 1) bf_kernel(Params P) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  const uint32_t sbase = smem_u32(sm);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nqb = (P.B + QB - 1) / QB;
+  const int64_t ntiles = (P.n + NT - 1) / NT;
+  const int64_t tile_lo = (int64_t(blockIdx.x) * ntiles) / gridDim.x;
+  const int64_t tile_hi = (int64_t(blockIdx.x + 1) * ntiles) / gridDim.x;
+  auto bar = [&](int i) { return sbase + OFF_BAR + 8 * i; };
+  auto full_bar = [&](int s) { return bar(s); };
+  auto empty_bar = [&](int s) { return bar(NSTAGE + s); };
+  auto tfull = [&](int e) { return bar(2 * NSTAGE + e); };
+  auto tempty = [&](int e) { return bar(2 * NSTAGE + NBUF + e); };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + OFF_TMEM);
+  uint32_t* scnt = reinterpret_cast<uint32_t*>(sm + OFF_CNT);
+  uint32_t* sbcnt = reinterpret_cast<uint32_t*>(sm + OFF_BCNT);
+  float* st_t = reinterpret_cast<float*>(sm + OFF_T);
+  float* st_e = reinterpret_cast<float*>(sm + OFF_E);
+
+  // queries -> bf16 operand blocks (zero padded); per query threshold and EPS * ||q||
+  for (int i = threadIdx.x; i < nqb * QB * 8; i += blockDim.x) {
+    const int q = i >> 3, c = i & 7;
+    __align__(16) __nv_bfloat16 h[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) h[j] = __float2bfloat16_rn(q < P.B ? __ldg(P.q + int64_t(q) * 64 + c * 8 + j) : 0.f);
+    const int qb = q / QB, m = q % QB;
+    *reinterpret_cast<int4*>(sm + OFF_A + qb * 16384 + (m >> 3) * 1024 + c * 128 + (m & 7) * 16) =
+        *reinterpret_cast<const int4*>(h);
+  }
+  for (int q = threadIdx.x; q < nqb * QB; q += blockDim.x) {
+    float t = 0.f, e = 0.f;
+    if (q < P.B) {
+      t = key_f32(__ldg(P.tkeys + q));
+      float ss = 0.f;
+      for (int k = 0; k < 64; ++k) {
+        const float x = __ldg(P.q + int64_t(q) * 64 + k);
+        ss = fmaf(x, x, ss);
+      }
+      e = EPS * up_norm(ss);
+    }
+    st_t[q] = t;
+    st_e[q] = e;
+    scnt[q] = 0;
+    sbcnt[q] = 0;
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NSTAGE; ++s) {
+      mbar_init(full_bar(s), 1);
+      mbar_init(empty_bar(s), 1 + NEPI * 128);
+    }
+    for (int e = 0; e < NBUF; ++e) {
+      mbar_init(tfull(e), 1);
+      mbar_init(tempty(e), NEPI * 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)), "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t tile = tile_lo; tile < tile_hi; ++tile) {
+        mbar_wait(empty_bar(stage), phase ^ 1);
+        const uint32_t st = sbase + OFF_RING + stage * SZ_STAGE;
+        mbar_arrive_expect_tx(full_bar(stage), SZ_TILE + NT * 4 + 32);
+        bulk_g2s(st, P.view + tile * (NT * 64), SZ_TILE, full_bar(stage));
+        bulk_g2s(st + ST_NRM, P.nrm + tile * NT, NT * 4, full_bar(stage));
+        bulk_g2s(st + ST_CMX, P.cmx + tile * (NT / 32), 32, full_bar(stage));
+        if (++stage == NSTAGE) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      uint32_t jc = 0;
+      for (int64_t tile = tile_lo; tile < tile_hi; ++tile) {
+        mbar_wait(full_bar(stage), phase);
+        tc_fence_after();
+        const uint32_t bt = sbase + OFF_RING + stage * SZ_STAGE;
+        for (int qb = 0; qb < nqb; ++qb, ++jc) {
+          const uint32_t at = sbase + OFF_A + qb * 16384;
+          const int buf = int(jc & 1);
+          mbar_wait(tempty(buf), ((jc >> 1) & 1) ^ 1);
+          tc_fence_after();
+#pragma unroll
+          for (int k = 0; k < 4; ++k) mma_bf(tmem_base + buf * 256, desc_bf(at + k * 256), desc_bf(bt + k * 256), k > 0);
+          mma_commit(tfull(buf));
+        }
+        mma_commit(empty_bar(stage));
+        if (++stage == NSTAGE) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    const int w = (warp - 2) >> 2;
+    const int quarter = warp & 3;
+    const int p = quarter * 32 + lane;
+    const uint32_t tlane = (uint32_t)(quarter * 32) << 16;
+    int stage = 0;
+    uint32_t phase = 0;
+    int64_t jc = 0;
+    int32_t* cand_cta = P.cand + int64_t(blockIdx.x) * P.seg;
+    int32_t* band_cta = P.band + int64_t(blockIdx.x) * P.seg;
+    for (int64_t tile = tile_lo; tile < tile_hi; ++tile) {
+      mbar_wait(full_bar(stage), phase);
+      const uint8_t* st = sm + OFF_RING + stage * SZ_STAGE;
+      const float* nrm = reinterpret_cast<const float*>(st + ST_NRM) + w * 64;
+      const float* cmx = reinterpret_cast<const float*>(st + ST_CMX) + w * 2;
+      const int64_t row0 = tile * NT + w * 64;
+      const int nvalid = (int)imax64(0, imin64(64, P.n - row0));
+      for (int qb = 0; qb < nqb; ++qb, ++jc) {
+        const int q = qb * QB + p;
+        const int buf = int(jc & 1);
+        const uint32_t tm = tmem_base + buf * 256 + w * 64 + tlane;
+        mbar_wait(tfull(buf), uint32_t((jc >> 1) & 1));
+        tc_fence_after();
+        if (qb * QB + quarter * 32 < P.B) {
+          const float t = st_t[q], e = st_e[q];
+          const float slack = fabsf(t) * 1e-6f + 1e-30f;
+          uint32_t cert[2], bnd[2];
+          uint32_t ra[32], rb[32];
+          TMEM_LD32(tm, ra);
+#pragma unroll
+          for (int cc = 0; cc < 2; ++cc) {
+            uint32_t* a = cc ? rb : ra;
+            const float lo = t - (e * cmx[cc] + slack);  // below it the whole chunk fails for certain
+            TMEM_WAIT32(a);
+            if (cc == 0) TMEM_LD32(tm + 32, rb);
+            const float* v = reinterpret_cast<const float*>(a);
+            uint32_t h = 0;
+#pragma unroll
+            for (int g8 = 0; g8 < 4; ++g8) {
+              const float* u = v + g8 * 8;
+              const float gm = fmaxf(fmaxf(fmaxf(u[0], u[1]), fmaxf(u[2], u[3])), fmaxf(fmaxf(u[4], u[5]), fmaxf(u[6], u[7])));
+              h |= uint32_t(gm >= lo) << g8;
+            }
+            h = __reduce_or_sync(0xffffffffu, h);
+            uint32_t mc = 0, mb = 0;
+#pragma unroll
+            for (int g8 = 0; g8 < 4; ++g8) {
+              if (h & (1u << g8)) {
+                const float* u = v + g8 * 8;
+                const float4 n0 = reinterpret_cast<const float4*>(nrm + cc * 32 + g8 * 8)[0];
+                const float4 n1 = reinterpret_cast<const float4*>(nrm + cc * 32 + g8 * 8)[1];
+                const float nv[8] = {n0.x, n0.y, n0.z, n0.w, n1.x, n1.y, n1.z, n1.w};
+#pragma unroll
+                for (int jj = 0; jj < 8; ++jj) {
+                  const float m = e * nv[jj] + slack;
+                  const bool c = u[jj] >= t + m;
+                  const bool b = !c && u[jj] >= t - m;
+                  mc |= uint32_t(c) << (g8 * 8 + jj);
+                  mb |= uint32_t(b) << (g8 * 8 + jj);
+                }
+              }
+            }
+            const int lim = nvalid - cc * 32;
+            const uint32_t vm = lim >= 32 ? 0xffffffffu : (lim <= 0 ? 0u : ((1u << lim) - 1u));
+            cert[cc] = mc & vm;
+            bnd[cc] = mb & vm;
+          }
+          if (q < P.B) {
+            const int nc = __popc(cert[0]) + __popc(cert[1]), nb = __popc(bnd[0]) + __popc(bnd[1]);
+            if (nc) {
+              uint32_t pos = atomicAdd(scnt + q, (uint32_t)nc);
+#pragma unroll
+              for (int cc = 0; cc < 2; ++cc)
+                for (uint32_t m = cert[cc]; m; m &= m - 1, ++pos)
+                  if ((int64_t)pos < P.seg) cand_cta[int64_t(q) * P.cap + pos] = int32_t(row0 + cc * 32 + __ffs(m) - 1);
+            }
+            if (nb) {
+              uint32_t pos = atomicAdd(sbcnt + q, (uint32_t)nb);
+#pragma unroll
+              for (int cc = 0; cc < 2; ++cc)
+                for (uint32_t m = bnd[cc]; m; m &= m - 1, ++pos)
+                  if ((int64_t)pos < P.seg) band_cta[int64_t(q) * P.cap + pos] = int32_t(row0 + cc * 32 + __ffs(m) - 1);
+            }
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(tempty(buf));
+      }
+      mbar_arrive(empty_bar(stage));
+      if (++stage == NSTAGE) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  for (int q = threadIdx.x; q < P.B; q += blockDim.x) {
+    P.cta_counts[int64_t(q) * gridDim.x + blockIdx.x] = int32_t(scnt[q]);
+    P.cta_bcounts[int64_t(q) * gridDim.x + blockIdx.x] = int32_t(sbcnt[q]);
+  }
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
+}
+
+__global__ void seg_max_kernel(int64_t n, const int32_t* __restrict__ cnt, int* __restrict__ mx) {
+  int m = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    m = max(m, cnt[i]);
+  m = __reduce_max_sync(0xffffffffu, m);
+  if ((threadIdx.x & 31) == 0 && m > 0) atomicMax(mx, m);
+}
+
+// exact fp32 re-score of the undecided band (the sequential fmaf chain of filter_scan_kernel);
+// passers are appended after the query's certain passers (counts[b] = running total)
+__global__ void __launch_bounds__(256) recheck_band_kernel(int G, int64_t seg, int64_t cap_in, const int32_t* __restrict__ band,
+                                                           const int32_t* __restrict__ bcnt, const float* __restrict__ vf,
+                                                           const float* __restrict__ qf, const uint32_t* __restrict__ tkeys,
+                                                           int strict, int64_t cap_out, int32_t* __restrict__ cand,
+                                                           int64_t* __restrict__ counts) {
+  __shared__ float sq[64];
+  const int b = blockIdx.x;
+  if (threadIdx.x < 64) sq[threadIdx.x] = qf[int64_t(b) * 64 + threadIdx.x];
+  __syncthreads();
+  const uint32_t tk = tkeys[b];
+  for (int g = blockIdx.y; g < G; g += gridDim.y) {  // (query, group of CTA segments) per block
+    const int64_t n = imin64(bcnt[int64_t(b) * G + g], seg);
+    const int32_t* src = band + int64_t(b) * cap_in + int64_t(g) * seg;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+      const int32_t r = src[i];
+      const float4* v = reinterpret_cast<const float4*>(vf + int64_t(r) * 64);
+      float acc = 0.f;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const float4 x = __ldg(v + k);
+        acc = fmaf(x.x, sq[4 * k], acc);
+        acc = fmaf(x.y, sq[4 * k + 1], acc);
+        acc = fmaf(x.z, sq[4 * k + 2], acc);
+        acc = fmaf(x.w, sq[4 * k + 3], acc);
+      }
+      const uint32_t key = f32_key(acc);
+      if (strict ? key > tk : key >= tk) {
+        const int64_t pos = (int64_t)atomicAdd(reinterpret_cast<unsigned long long*>(counts + b), 1ull);
+        if (pos < cap_out) cand[int64_t(b) * cap_out + pos] = r;
+      }
+    }
+  }
+}
+}  // namespace s1bf
+
 bool s1_tc_supported(const molr_cache* c, int mode) {
   return c && mode != MOLR_S1_FLOAT && c->d1 == 64 && c->s1_codes && c->s1_chunk_mm && !getenv("MOLR_DISABLE_TC");
 }
@@ -790,6 +1145,92 @@ int s1_tc_scan(molr_ctx* ctx, int mode, const int8_t* codes, const float* scales
       MOLR_CUDA(cudaStreamSynchronize(s));
       if (hmx <= seg) break;
       seg = hmx;  // a private segment overflowed: rerun with the exact maximum
+    }
+  }
+  return MOLR_OK;
+}
+
+bool s1_bf_supported(const molr_cache* c, int mode) {
+  return c && mode == MOLR_S1_FLOAT && c->d1 == 64 && c->s1_f32 && c->X > 0 && !getenv("MOLR_DISABLE_TC") && !getenv("MOLR_S1_NO_BF");
+}
+
+static int s1_bf_build(molr_cache* c, cudaStream_t s) {
+  using namespace s1bf;
+  if (c->s1_bf_ready.load(std::memory_order_acquire)) return MOLR_OK;
+  std::lock_guard<std::mutex> g(c->seal_mu);
+  if (c->s1_bf_ready.load()) return MOLR_OK;
+  const int64_t xr = (c->X + NT - 1) / NT * NT;
+  if (!c->s1_bf) {
+    MOLR_CUDA(cudaMalloc(&c->s1_bf, size_t(xr) * 128));
+    MOLR_CUDA(cudaMalloc(&c->s1_bnorm, size_t(xr) * 4));
+    MOLR_CUDA(cudaMalloc(&c->s1_bnmax, size_t(xr / 32) * 4));
+    c->bytes += xr * 128 + xr * 4 + xr / 8;
+  }
+  build_kernel<<<c->ctx->num_sms * 8, 256, 0, s>>>(c->X, xr, c->s1_f32, c->s1_bf, c->s1_bnorm);
+  MOLR_LAUNCHED(c->ctx);
+  chunk_max_kernel<<<div_up(xr / 32, 256), 256, 0, s>>>(xr / 32, c->s1_bnorm, c->s1_bnmax);
+  MOLR_LAUNCHED(c->ctx);
+  MOLR_CUDA(cudaStreamSynchronize(s));
+  c->s1_bf_ready.store(1, std::memory_order_release);
+  return MOLR_OK;
+}
+
+// Filter every row of the float view against B queries: cand rows (B, cap) / counts (B,) exactly
+// as the fp32 filter scan would produce them (as a set).
+int s1_bf_scan(molr_ctx* ctx, const molr_cache* cc, int B, const float* q, const uint32_t* tkeys, int strict,
+               int64_t cap, int32_t* cand, int64_t* counts, cudaStream_t s) {
+  using namespace s1bf;
+  molr_cache* c = const_cast<molr_cache*>(cc);
+  MOLR_TRY(s1_bf_build(c, s));
+  const int64_t n = c->X;
+  if (n <= 0 || B <= 0) return MOLR_OK;
+  const int64_t ntiles = (n + NT - 1) / NT;
+  const int grid = (int)std::min<int64_t>(ntiles, ctx->num_sms);
+  int64_t seg = (cap / grid) + (cap / grid) / 3 + 64;
+  MOLR_CUDA(cudaFuncSetAttribute(bf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+  for (int b0 = 0; b0 < B; b0 += MAXQB * QB) {
+    const int Bc = std::min(B - b0, MAXQB * QB);
+    for (int attempt = 0; attempt < 2; ++attempt) {
+      Scratch priv, bpriv, ccount, bcount, mx;
+      Params P;
+      P.view = c->s1_bf;
+      P.nrm = c->s1_bnorm;
+      P.cmx = c->s1_bnmax;
+      P.n = n;
+      P.B = Bc;
+      P.q = q + int64_t(b0) * 64;
+      P.tkeys = tkeys + b0;
+      P.seg = seg;
+      P.cap = int64_t(grid) * seg;
+      MOLR_TRY(priv.alloc(size_t(Bc) * P.cap * 4, s));
+      MOLR_TRY(bpriv.alloc(size_t(Bc) * P.cap * 4, s));
+      MOLR_TRY(ccount.alloc(size_t(Bc) * grid * 4, s));
+      MOLR_TRY(bcount.alloc(size_t(Bc) * grid * 4, s));
+      MOLR_TRY(mx.alloc(4, s));
+      MOLR_CUDA(cudaMemsetAsync(mx.p, 0, 4, s));
+      P.cand = priv.as<int32_t>();
+      P.band = bpriv.as<int32_t>();
+      P.cta_counts = ccount.as<int32_t>();
+      P.cta_bcounts = bcount.as<int32_t>();
+      bf_kernel<<<grid, NTHREADS, SMEM_BYTES, s>>>(P);
+      MOLR_LAUNCHED(ctx);
+      s1tc::compact_segments_kernel<<<Bc, 256, 0, s>>>(grid, seg, P.cap, P.cand, P.cta_counts, cap,
+                                                       cand + int64_t(b0) * cap, counts + b0, mx.as<int>());
+      MOLR_LAUNCHED(ctx);
+      seg_max_kernel<<<div_up(int64_t(Bc) * grid, 256), 256, 0, s>>>(int64_t(Bc) * grid, P.cta_bcounts, mx.as<int>());
+      MOLR_LAUNCHED(ctx);
+      int hmx = 0;
+      MOLR_CUDA(cudaMemcpyAsync(&hmx, mx.p, 4, cudaMemcpyDeviceToHost, s));
+      MOLR_CUDA(cudaStreamSynchronize(s));
+      if (hmx > seg && attempt == 0) {
+        seg = hmx;  // a private segment overflowed: rerun with the exact maximum
+        continue;
+      }
+      const dim3 rg(Bc, std::max(1, std::min(grid, (4 * ctx->num_sms + Bc - 1) / Bc)));
+      recheck_band_kernel<<<rg, 256, 0, s>>>(grid, seg, P.cap, P.band, P.cta_bcounts, c->s1_f32, P.q, P.tkeys, strict,
+                                             cap, cand + int64_t(b0) * cap, counts + b0);
+      MOLR_LAUNCHED(ctx);
+      break;
     }
   }
   return MOLR_OK;

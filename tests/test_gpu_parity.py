@@ -576,6 +576,38 @@ def test_batched_stage1_small_batch_kernel(nb, monkeypatch):
             np.testing.assert_array_equal(x, y)
 
 
+@pytest.mark.parametrize("nb", [3, 300])
+def test_batched_float_view_tc_matches_fp32_scan(nb, monkeypatch):
+    """Float stage-1 view (quantized=False, the reference default) on the tensor cores: bf16 MMA
+    pre-test + exact fp32 re-check of the undecided band must give the SAME candidate sets as the
+    fp32 SIMT filter scan (identical counts, identical top-k), for both comparators and for an
+    exact threshold (lambda = X) and a sampled one; counts also match the oracle's NumPy h_indexer
+    up to fp32 summation-order near-ties."""
+    from paper_2306_04039_b200.engine import two_stage_top_k
+    from paper_2306_04039_b200.hindexer import HIndexerConfig
+
+    cache, syn, ue, feats = _synthetic_prod_cache(150_000, seed=41, n_users=nb)
+    gating, og = _prod_gating(syn)
+    uw = gating.user_net(feats)
+    X = cache.num_items
+    for comp in ("inclusive", "strict"):
+        for kw in ({"lam": X}, {"sample_ratio": 0.05}):
+            hcfg = HIndexerConfig(k_prime=1500, quantized=False, comparator=comp, **kw)
+            monkeypatch.delenv("MOLR_S1_NO_BF", raising=False)
+            a = two_stage_top_k(cache, gating, ue, uw, 20, hcfg, seed=3)
+            monkeypatch.setenv("MOLR_S1_NO_BF", "1")  # the fp32 SIMT filter scan
+            b = two_stage_top_k(cache, gating, ue, uw, 20, hcfg, seed=3)
+            monkeypatch.delenv("MOLR_S1_NO_BF")
+            np.testing.assert_array_equal(a[2], b[2])
+            np.testing.assert_array_equal(a[0], b[0])
+            np.testing.assert_array_equal(a[1], b[1])
+            if "lam" in kw:
+                for u in range(min(nb, 8)):
+                    c_ids, _, _ = O.h_indexer(cache.stage1_embs, ue[u].mean(axis=0), 1500, O.make_rng(0), lam=X,
+                                              comparator=comp)
+                    assert abs(int(a[2][u]) - c_ids.size) <= 2, (comp, u, a[2][u], c_ids.size)
+
+
 def test_batched_two_stage_recall_device_sample():
     """Device-drawn sample (lambda = 1% of X): candidate counts near K' and top-100 recall vs the
     oracle's exact MoL top-100 >= 0.99 (north-star bar), 100k items."""
