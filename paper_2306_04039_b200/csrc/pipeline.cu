@@ -237,6 +237,107 @@ int sample_threshold_tc(molr_ctx* ctx, int mode, const int8_t* scodes, const flo
   return nth_largest_rows(ctx, B, lam, ss.p, raw, lam, nullptr, 0, n_rank, tkey, s);
 }
 
+
+// Float view: score the sampled rows (v row in registers, the sequential fmaf chain of
+// scan_scores_kernel) and append the ascending keys of the scores >= t0[b] (pilot threshold).
+__global__ void __launch_bounds__(256) sample_keys_f32_kernel(int64_t n, const float* __restrict__ vf,
+                                                              const int64_t* __restrict__ rows_idx, int B,
+                                                              const float* __restrict__ qf, const uint32_t* __restrict__ t0,
+                                                              int64_t cap, uint32_t* __restrict__ keys,
+                                                              int64_t* __restrict__ counts) {
+  extern __shared__ __align__(16) unsigned char sq[];
+  float* q = reinterpret_cast<float*>(sq);
+  uint32_t* tk = reinterpret_cast<uint32_t*>(sq + size_t(B) * 256);
+  for (int i = threadIdx.x; i < B * 64; i += blockDim.x) q[i] = qf[i];
+  for (int i = threadIdx.x; i < B; i += blockDim.x) tk[i] = t0[i];
+  __syncthreads();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = rows_idx[i];
+    float v[64];
+    const float4* v4 = reinterpret_cast<const float4*>(vf + r * 64);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const float4 x = __ldg(v4 + k);
+      v[4 * k] = x.x, v[4 * k + 1] = x.y, v[4 * k + 2] = x.z, v[4 * k + 3] = x.w;
+    }
+    for (int b = 0; b < B; ++b) {
+      const float4* q4 = reinterpret_cast<const float4*>(q) + b * 16;
+      float acc = 0.f;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const float4 y = q4[k];
+        acc = fmaf(v[4 * k], y.x, acc);
+        acc = fmaf(v[4 * k + 1], y.y, acc);
+        acc = fmaf(v[4 * k + 2], y.z, acc);
+        acc = fmaf(v[4 * k + 3], y.w, acc);
+      }
+      const uint32_t key = f32_key(acc);
+      if (key >= tk[b]) {
+        const int64_t pos = (int64_t)atomicAdd(reinterpret_cast<unsigned long long*>(counts + b), 1ull);
+        if (pos < cap) keys[int64_t(b) * cap + pos] = key;
+      }
+    }
+  }
+}
+
+// The float view's sampled threshold with the pilot filter of sample_threshold_tc (exact: the
+// n-th largest passer key is the n-th largest sample score whenever >= n rows pass t0).
+int sample_threshold_f32(molr_ctx* ctx, const molr_cache* c, const int64_t* samp, int64_t lam, int B, const float* q,
+                         int64_t n_rank, Scratch& ss, uint32_t* tkey, cudaStream_t s) {
+  const double p = double(n_rank) / double(lam);
+  int64_t lam0 = (int64_t)std::ceil(16.0 / p);
+  lam0 = (lam0 + 255) / 256 * 256;
+  if (c->d1 == 64 && !getenv("MOLR_NO_PILOT") && lam0 * 4 <= lam) {
+    const double mu = double(lam0) * p;
+    int64_t n0 = std::min<int64_t>(lam0, (int64_t)std::ceil(mu + 6.0 * std::sqrt(mu) + 16.0));
+    if (const char* e = getenv("MOLR_PILOT_N0")) n0 = std::max<int64_t>(1, std::min<int64_t>(lam0, atoll(e)));
+    const double expect = double(lam) * double(n0) / double(lam0);
+    const int64_t cap = (int64_t)(2.0 * expect) + 2048;
+    Scratch pilot, t0, keys, counts, flag;
+    MOLR_TRY(pilot.alloc(size_t(B) * lam0 * 4, s));
+    MOLR_TRY(t0.alloc(size_t(B) * 4, s));
+    MOLR_TRY(keys.alloc(size_t(B) * cap * 4, s));
+    MOLR_TRY(counts.alloc(size_t(B) * 8, s));
+    MOLR_TRY(flag.alloc(sizeof(int) * 2, s));
+    {
+      KTimer t(ctx, "stage1_sample_scan", s, double(B) * lam);
+      MOLR_TRY(scan_scores(ctx, MOLR_S1_FLOAT, lam0, 64, c->s1_f32, nullptr, false, nullptr, nullptr, samp, B, q, nullptr,
+                           pilot.p, lam0, s));
+      MOLR_TRY(nth_largest_rows(ctx, B, lam0, pilot.p, false, lam0, nullptr, 0, n0, t0.as<uint32_t>(), s));
+      MOLR_CUDA(cudaMemsetAsync(counts.p, 0, size_t(B) * 8, s));
+      MOLR_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int) * 2, s));
+      const int bchunk = 128;  // 32 KB of queries per launch
+      for (int b0 = 0; b0 < B; b0 += bchunk) {
+        const int bb = std::min(bchunk, B - b0);
+        const size_t smem = size_t(bb) * 260;
+        const int blocks = (int)imin64(div_up(lam, 256), int64_t(ctx->num_sms) * 8);
+        sample_keys_f32_kernel<<<blocks, 256, smem, s>>>(lam, c->s1_f32, samp, bb, q + size_t(b0) * 64,
+                                                         t0.as<uint32_t>() + b0, cap, keys.as<uint32_t>() + size_t(b0) * cap,
+                                                         counts.as<int64_t>() + b0);
+        MOLR_LAUNCHED(ctx);
+      }
+    }
+    {
+      KTimer t(ctx, "select_nth", s, double(B) * expect);
+      MOLR_TRY(nth_largest_keys(ctx, B, cap, keys.as<uint32_t>(), counts.as<int64_t>(), n_rank, tkey, flag.as<int>(), s));
+      max_count_kernel<<<div_up(B, 256), 256, 0, s>>>(B, counts.as<int64_t>(), cap, flag.as<int>());
+      MOLR_LAUNCHED(ctx);
+    }
+    int hf = 0;
+    MOLR_CUDA(cudaMemcpyAsync(&hf, flag.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    MOLR_CUDA(cudaStreamSynchronize(s));
+    if (!hf) return MOLR_OK;
+  }
+  MOLR_TRY(ss.alloc(size_t(B) * lam * 4, s));
+  {
+    KTimer t(ctx, "stage1_sample_scan", s, double(B) * lam);
+    MOLR_TRY(scan_scores(ctx, MOLR_S1_FLOAT, lam, c->d1, c->s1_f32, nullptr, false, nullptr, nullptr, samp, B, q, nullptr,
+                         ss.p, lam, s));
+  }
+  KTimer t(ctx, "select_nth", s, double(B) * lam);
+  return nth_largest_rows(ctx, B, lam, ss.p, false, lam, nullptr, 0, n_rank, tkey, s);
+}
+
 }  // namespace molr
 
 using namespace molr;
@@ -476,13 +577,15 @@ int molr_two_stage_top_k(molr_ctx* ctx, const molr_cache* c, const molr_gating* 
       MOLR_LAUNCHED(ctx);
       MOLR_TRY(sample_threshold_tc(ctx, mode, scodes.as<int8_t>(), sscales.as<float>(), lam, B, qc.as<int8_t>(),
                                    n_rank, ss, tkey.as<uint32_t>(), s));
+    } else if (mode == MOLR_S1_FLOAT) {
+      MOLR_TRY(sample_threshold_f32(ctx, c, samp.as<int64_t>(), lam, B, q.as<float>(), n_rank, ss, tkey.as<uint32_t>(), s));
     } else {
       MOLR_TRY(ss.alloc(size_t(B) * lam * 4, s));
       KTimer t(ctx, "stage1_sample_scan", s, double(B) * lam);
       MOLR_TRY(scan_scores(ctx, mode, lam, c->d1, c->s1_f32, c->s1_codes, s1_interleaved(c->d1), c->s1_inv, c->s1_scales,
                            samp.as<int64_t>(), B, q.as<float>(), qc.as<int8_t>(), ss.p, lam, s));
     }
-    if (!use_tc) {
+    if (!use_tc && mode != MOLR_S1_FLOAT) {
       KTimer t(ctx, "select_nth", s, double(B) * lam);
       MOLR_TRY(nth_largest_rows(ctx, B, lam, ss.p, mode == MOLR_S1_INT8_RAW, lam, nullptr, 0, n_rank,
                                 tkey.as<uint32_t>(), s));

@@ -629,8 +629,9 @@ def test_batched_two_stage_recall_device_sample():
     assert np.mean(rec) >= 0.99
 
 
-@pytest.mark.parametrize("strict,raw", [(False, False), (True, False), (False, True)])
-def test_sample_threshold_pilot_exact(strict, raw, monkeypatch):
+@pytest.mark.parametrize("strict,raw,quantized", [(False, False, True), (True, False, True), (False, True, True),
+                                                  (False, False, False), (True, False, False)])
+def test_sample_threshold_pilot_exact(strict, raw, quantized, monkeypatch):
     """The pilot-filtered sample threshold (score a subsample, keep only sample rows above a low
     pilot threshold, select among them) must give the SAME threshold as scoring the whole sample:
     identical candidate counts and top-k for pilot / no pilot / forced fallback (pilot threshold
@@ -640,7 +641,7 @@ def test_sample_threshold_pilot_exact(strict, raw, monkeypatch):
 
     cache, syn, ue, feats = _synthetic_prod_cache(300_000, seed=17, n_users=200)
     gating, og = _prod_gating(syn)
-    hcfg = HIndexerConfig(k_prime=3000, sample_ratio=0.2, quantized=True,
+    hcfg = HIndexerConfig(k_prime=3000, sample_ratio=0.2, quantized=quantized,
                           comparator="strict" if strict else "inclusive", raw_int_ordering=raw)
     uw = gating.user_net(feats)
     runs = {}
