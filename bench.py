@@ -36,6 +36,10 @@ CONFIGS = {
     # X items, B queries per step, k, K', sample ratio r (lambda = r X)
     "100m": dict(X=100_000_000, B=1024, k=100, k_prime=100_000, ratio=0.01, label="100M-item synthetic corpus"),
     "10m": dict(X=10_000_000, B=1024, k=100, k_prime=100_000, ratio=0.01, label="10M-item synthetic corpus"),
+    # the reference's default stage-1 view (quantized=False): fp32 scores, filtered on the tensor
+    # cores with an exact fp32 re-check (K2f)
+    "10m_f32": dict(X=10_000_000, B=1024, k=100, k_prime=100_000, ratio=0.01, view="f32",
+                    label="10M-item synthetic corpus, float stage-1 view"),
     "books": dict(X=2_300_000, B=1024, k=100, k_prime=100_000, ratio=0.01, label="Amazon-Books-shaped 2.3M items"),
     # exact path (batch_score_all + mol_top_k over the whole corpus, mol.py:348-408): one step =
     # B users x all X items; the full ML-20M run is 138K users
@@ -195,7 +199,7 @@ def _cpu_worker(args):
     os.environ["OPENBLAS_NUM_THREADS"] = "1"
     import oracle as O
 
-    seed, reps, X1, k_prime, ratio, k = args
+    seed, reps, X1, k_prime, ratio, k, f32_view = args
     st = _CPU_STATE
     t1s, t2s = [], []
     for r in range(reps):
@@ -207,7 +211,8 @@ def _cpu_worker(args):
             t1s.append(0.0)
             t2s.append(time.perf_counter() - t0)
             continue
-        O.h_indexer(st["cache"].stage1_q, q1, max(1, k_prime * X1 // st["X"]), O.make_rng([9000, u]),
+        O.h_indexer(st["cache"].stage1_embs if f32_view else st["cache"].stage1_q, q1,
+                    max(1, k_prime * X1 // st["X"]), O.make_rng([9000, u]),
                     sample_ratio=ratio)
         t1 = time.perf_counter()
         O.mol_top_k(st["cache"], st["gating"], st["cand"], st["ue"][u], st["feats"][u], k)
@@ -257,7 +262,8 @@ def cpu_baseline(cfg, reps=2, procs=None, X1=1_000_000):
             pass
     t0 = time.perf_counter()
     with mp.get_context("fork").Pool(procs) as pool:
-        res = pool.map(_cpu_worker, [(i, reps, X1, cfg["k_prime"], cfg["ratio"], cfg["k"]) for i in range(procs)])
+        res = pool.map(_cpu_worker, [(i, reps, X1, cfg["k_prime"], cfg["ratio"], cfg["k"], cfg.get("view") == "f32")
+                                     for i in range(procs)])
     wall = time.perf_counter() - t0
     t1 = float(np.median([t for r in res for t in r[0]]))
     t2 = float(np.median([t for r in res for t in r[1]]))
@@ -268,7 +274,8 @@ def cpu_baseline(cfg, reps=2, procs=None, X1=1_000_000):
                            f"{cfg['X']:,} items = {t2:.2f} s per user per core; wall {wall:.1f} s"),
                 "s_per_query_per_core": t_query}
     return {"value": procs / t_query, "unit": "queries/s", "cores": procs, "kind": "port",
-            "sample": (f"oracle/ NumPy port, {procs} processes x {reps} queries: stage 1 (int8 h_indexer incl. "
+            "sample": (f"oracle/ NumPy port, {procs} processes x {reps} queries: stage 1 "
+                       f"({'float' if cfg.get('view') == 'f32' else 'int8'} h_indexer incl. "
                        f"rng.permutation) on a {X1:,}-row shard x {cfg['X'] // X1} (linear in X) = "
                        f"{t1 * cfg['X'] / X1:.2f} s + stage 2 mol_top_k over {ncand:,} candidates = {t2:.2f} s per "
                        f"query per core; wall {wall:.1f} s"),
@@ -359,7 +366,10 @@ def main():
 
     model = synthetic_model()
     t_build = time.perf_counter()
-    mcfg, cache = build_shard(model, X, lo, hi, seed=11, dev=dev, lib=lib, ctx=ctx)
+    f32_view = cfg.get("view") == "f32"
+    s1_mode = L.S1_FLOAT if f32_view else L.S1_INT8
+    mcfg, cache = build_shard(model, X, lo, hi, seed=11, dev=dev, lib=lib, ctx=ctx,
+                              storage=L.STORE_S1_F32 if f32_view else None)
     t_build = time.perf_counter() - t_build
     gating = GatingNetwork(Mlp(*model["user_net"]), Mlp(*model["item_net"]), Mlp(*model["cross_net"]))
     gh = _gating_handle(gating)
@@ -399,7 +409,7 @@ def main():
                 ids_d.add_(lo)
         else:
             L.call("molr_two_stage_top_k", ctx, cache.device_handle(), gh, B, K_U, ue_ptr, uw_d.data_ptr(), TAU,
-                   L.S1_INT8, kp_local, lam_local, 1000 + i, L.INCLUSIVE, k, lo, oi, osc, L.ptr(cand_h), sp)
+                   s1_mode, kp_local, lam_local, 1000 + i, L.INCLUSIVE, k, lo, oi, osc, L.ptr(cand_h), sp)
         if world > 1:
             all_gather(gat_ids, ids_d)
             all_gather(gat_sc, sc_d)
@@ -514,7 +524,7 @@ def main():
                    None, None, k, ids_d.data_ptr(), sc_d.data_ptr(), sp)
         else:
             L.call("molr_two_stage_top_k", ctx, cache.device_handle(), gh, 1, K_U, ue_d.data_ptr(), uw_d.data_ptr(),
-                   TAU, L.S1_INT8, kp_local, lam_local, 5 + i, L.INCLUSIVE, k, lo, ids_d.data_ptr(), sc_d.data_ptr(),
+                   TAU, s1_mode, kp_local, lam_local, 5 + i, L.INCLUSIVE, k, lo, ids_d.data_ptr(), sc_d.data_ptr(),
                    None, sp)
         t1.record(stream)
         torch.cuda.synchronize()
@@ -572,6 +582,12 @@ def main():
             r = {"kernel": name, "bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                  "frac": achieved / pk["hbm_gbs"], "traffic": None, "units_per_launch": units,
                  "per_unit": f"{PAIR_BYTES} B per (query, candidate) pair", "peak_src": pk["src"]}
+        elif name == "stage1_filter_bf16":
+            achieved = units * S1_OPS / per_launch_s / 1e12
+            r = {"kernel": name, "bound": "tensor", "achieved": achieved, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
+                 "frac": achieved / pk["bf16_tflops"], "traffic": None, "units_per_launch": units,
+                 "per_unit": f"{S1_OPS} bf16 flops per (query, row)", "peak_src": f"{pk['src']} bf16",
+                 "note": "bf16 pre-test + exact fp32 re-check of the undecided band (DESIGN.md K2f)"}
         elif name.startswith("stage1_filter"):
             achieved = units * S1_OPS / per_launch_s / 1e12
             peak_i8 = 2 * pk["bf16_tflops"]
@@ -596,11 +612,14 @@ def main():
     line = {
         "metric": metric, "value": value, "unit": "queries/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16+int8 (fp32 accumulate)",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "bf16+f32 (fp32 accumulate)" if f32_view else "bf16+int8 (fp32 accumulate)",
         "data": "synthetic (reference init convention model.py:121-163; bf16-representable item cache built on device)",
         "config": {"workload": cfg["label"], "items": X, "items_per_gpu": Xl, "batch": B, "k": k,
                    "k_prime": cfg["k_prime"], "k_prime_per_gpu": kp_local, "sample_ratio": cfg["ratio"],
-                   "lambda_per_gpu": lam_local, "stage1": None if exact else "int8 (bit-exact)",
+                   "lambda_per_gpu": lam_local,
+                   "stage1": None if exact else ("float view: bf16 tensor-core pre-test + exact fp32 re-check"
+                                                 if f32_view else "int8 (bit-exact)"),
                    "parallelism": f"item-shard x{world}",
                    "l2": ("item side L2-resident by design (exact path); user inputs fresh per step" if exact else
                           "inputs larger than L2 (corpus shard x 1.2 KB per item >> 126 MB)")},
