@@ -598,11 +598,12 @@ def main():
                  "note": "bound by the SIMT threshold test of every accumulator (~4.5 instr each), not the MMA"}
         else:
             return None
-        try:
-            with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-                r["traffic"] = json.load(f).get(name)
-        except Exception:
-            pass
+        if args.config == "100m" and world == 1:  # the committed capture is of the 100M N=1 step
+            try:
+                with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+                    r["traffic"] = json.load(f).get(name)
+            except Exception:
+                pass
         return r
 
     rooflines = [x for x in (roof_of(n, *v) for n, v in sorted(prof.items(), key=lambda kv: -kv[1][1])) if x]

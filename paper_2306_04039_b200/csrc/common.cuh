@@ -161,10 +161,12 @@ struct molr_cache {
   int32_t* s1_inv = nullptr;
   std::atomic<int> s1_sealed{0};
   std::mutex seal_mu;
-  // float view on the tensor cores (built lazily from s1_f32, d1 = 64): bf16(view) in the
-  // interleaved K-major layout (128 B rows, 256-row tiles), per-row ||v||_2 and per-32-row-chunk
-  // max of it, for the pre-test bound of the bf16 MMA against the fp32 score
-  __nv_bfloat16* s1_bf = nullptr;
+  // float view on the tensor cores (built lazily from s1_f32, d1 = 64): fp16(view / s1_hscale)
+  // (s1_hscale a power of two putting max|v| in [2^14, 2^15)) in the interleaved K-major layout
+  // (128 B rows, 256-row tiles), per-row ||v||_2 and per-32-row-chunk max of it, for the pre-test
+  // bound of the fp16 MMA against the fp32 score
+  __half* s1_bf = nullptr;
+  float s1_hscale = 1.f;
   float* s1_bnorm = nullptr;
   float* s1_bnmax = nullptr;
   std::atomic<int> s1_bf_ready{0};

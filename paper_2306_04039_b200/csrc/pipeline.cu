@@ -613,7 +613,6 @@ int molr_two_stage_top_k(molr_ctx* ctx, const molr_cache* c, const molr_gating* 
         return MOLR_OK;
       };
       if (s1_bf_supported(c, mode) && B >= 2) {  // (one query: the fp32 scan is already HBM-bound)
-        KTimer t(ctx, "stage1_filter_bf16", s, double(B) * X);
         MOLR_TRY(s1_bf_scan(ctx, c, B, q.as<float>(), tkey.as<uint32_t>(), comparator == MOLR_STRICT, cap,
                             cand.as<int32_t>(), counts.as<int64_t>(), s));
       } else if (use_tc) {

@@ -16,6 +16,8 @@
 // counters (no global atomics on the hot path); a compaction kernel concatenates the segments.
 //
 #include <algorithm>
+#include <cmath>
+#include <cstring>
 
 #include "kernels.cuh"
 #include "stage1.cuh"
@@ -709,23 +711,27 @@ __global__ void __launch_bounds__(256) compact_segments_kernel(int G, int64_t se
 //
 // The reference's float score is an fp32 dot; the product's fp32 definition is the sequential
 // fmaf chain of filter_scan_kernel / scan_scores_kernel (the sample threshold comes from it).
-// bf16(v) . bf16(q) with fp32 accumulation differs from it by at most
-//   |D - s| <= (2^-7 + 2^-16 + 2 * 64 * 2^-24) * sum|v_i q_i| <= EPS * ||v||_2 * ||q||_2
-// (bf16 round-to-nearest: relative error <= 2^-8 per operand; both fp32 accumulations), so per
-// (query, row) with m = EPS ||q|| ||v||:  D >= t + m  -> passes for certain;  D < t - m -> fails
+// Operands are fp16 after an exact power-of-two scaling (view: one global sv putting max|v| in
+// [2^14, 2^15); query: its own sq), so v = sv v' + dv with |dv| <= 2^-11 |v| + 2^-25 sv (the
+// second term for fp16 subnormals) and likewise for q.  With fp32 accumulation of the exact
+// fp16 products, D = sv sq sum v'q' differs from the fp32 score s by at most
+//   (2^-10 + 2^-22 + 2*64*2^-24) sum|v_i q_i| + 2^-24 (sv ||q||_1 + sq ||v||_1) (1 + 2^-10)
+//   <= EPS ||v||_2 ||q||_2 + 2^-21 (sv ||q||_2 + sq ||v||_2)      (||x||_1 <= 8 ||x||_2, d = 64)
+// so per (query, row) with that margin m:  D >= t + m  -> passes for certain;  D < t - m -> fails
 // for certain; otherwise the row is in the undecided band and is re-scored exactly in fp32 by
 // recheck_band_kernel.  The candidate SET equals the fp32 scan's bit for bit; only the order of
-// the list differs (certain passers in id order, then the re-checked band).
+// the list differs (certain passers in id order, then the re-checked band).  (A bf16 image would
+// make the band 8x wider: 2^-7 instead of 2^-10.)
 //
-// Layout: bf16 view in the interleaved K-major layout with 128 B rows (8-row groups of 1 KB),
+// Layout: the fp16 view in the interleaved K-major layout with 128 B rows (8-row groups of 1 KB),
 // 256-row tiles of 32 KB + 1 KB of row norms + 32 B of chunk max norms per stage; all B <= 1024
-// queries resident as bf16 (128 KB).  Per (tile, 128-query block): 4 x (M=128, N=256, K=16)
+// queries resident as fp16 (128 KB).  Per (tile, 128-query block): 4 x (M=128, N=256, K=16)
 // kind::f16 MMAs into one of two 256-column TMEM buffers; the epilogue is the int8 kernel's with
-// a float max tree and no scale.
+// a float max tree and no scale (thresholds and margins pre-divided by sv sq, exactly).
 namespace s1bf {
 using s1tc::smem_u32; using s1tc::mbar_init; using s1tc::mbar_arrive; using s1tc::mbar_arrive_expect_tx; using s1tc::mbar_wait;
 using s1tc::bulk_g2s; using s1tc::fence_async_smem; using s1tc::tc_fence_before; using s1tc::tc_fence_after; using s1tc::mma_commit;
-constexpr float EPS = 0.0079f;
+constexpr float EPS = 0.000992f;  // > 2^-10 + 2^-22 + 2^-17 (+0.5%)
 constexpr int NT = 256, QB = 128, MAXQB = 8, NSTAGE = 2, NBUF = 2, NEPI = 4;
 constexpr int SZ_TILE = NT * 128;
 constexpr int ST_NRM = SZ_TILE, ST_CMX = SZ_TILE + NT * 4;
@@ -736,13 +742,15 @@ constexpr int OFF_T = OFF_RING + NSTAGE * SZ_STAGE;
 constexpr int OFF_E = OFF_T + MAXQB * QB * 4;
 constexpr int OFF_CNT = OFF_E + MAXQB * QB * 4;
 constexpr int OFF_BCNT = OFF_CNT + MAXQB * QB * 4;
-constexpr int OFF_BAR = OFF_BCNT + MAXQB * QB * 4;
+constexpr int OFF_C = OFF_BCNT + MAXQB * QB * 4;
+constexpr int OFF_SQ = OFF_C + MAXQB * QB * 4;
+constexpr int OFF_BAR = OFF_SQ + MAXQB * QB * 4;
 constexpr int NBAR = 2 * NSTAGE + 2 * NBUF;
 constexpr int OFF_TMEM = OFF_BAR + NBAR * 8;
 constexpr int SMEM_BYTES = OFF_TMEM + 16;
 constexpr int NTHREADS = 64 + NEPI * 128;
 static_assert(SMEM_BYTES <= 232448, "shared memory");
-constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(NT >> 3) << 17) | (uint32_t(QB >> 4) << 24);
+constexpr uint32_t IDESC = (1u << 4) | (uint32_t(NT >> 3) << 17) | (uint32_t(QB >> 4) << 24);  // f16 x f16 -> f32
 
 __host__ __device__ __forceinline__ int64_t bf_offset(int64_t r, int k) {  // element offset of v[r][k]
   return ((r >> 3) << 9) + int64_t(k >> 3) * 64 + ((r & 7) << 3) + (k & 7);
@@ -760,17 +768,31 @@ __device__ __forceinline__ void mma_bf(uint32_t d_tmem, uint64_t a, uint64_t b, 
 }
 __device__ __forceinline__ float up_norm(float ss) { return sqrtf(ss) * (1.0f + 1e-6f) + 1e-30f; }
 
-// fp32 rows -> bf16 interleaved image + row norms (padding rows zero)
-__global__ void build_kernel(int64_t X, int64_t xr, const float* __restrict__ v, __nv_bfloat16* __restrict__ out,
+// power of two p with x / p in [2^14, 2^15) (1 for x == 0)
+__host__ __device__ __forceinline__ float h_scale(float x) {
+  if (!(x > 0.f)) return 1.f;
+  int e;
+  frexpf(x, &e);  // x = f 2^e, f in [0.5, 1)
+  return ldexpf(1.f, e - 15);
+}
+__global__ void absmax_kernel(int64_t n, const float* __restrict__ v, unsigned* __restrict__ out) {
+  float m = 0.f;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    m = fmaxf(m, fabsf(v[i]));
+  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(m));  // non-negative floats order as uints
+}
+// fp32 rows -> fp16(v / sv) interleaved image + row norms (padding rows zero)
+__global__ void build_kernel(int64_t X, int64_t xr, const float* __restrict__ v, float inv_sv, __half* __restrict__ out,
                              float* __restrict__ nrm) {
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < xr; r += (int64_t)gridDim.x * blockDim.x) {
     float ss = 0.f;
     for (int c = 0; c < 8; ++c) {
-      __align__(16) __nv_bfloat16 h[8];
+      __align__(16) __half h[8];
       for (int j = 0; j < 8; ++j) {
         const float x = r < X ? v[r * 64 + c * 8 + j] : 0.f;
         ss = fmaf(x, x, ss);
-        h[j] = __float2bfloat16_rn(x);
+        h[j] = __float2half_rn(x * inv_sv);  // exact power-of-two scaling, then one rounding
       }
       *reinterpret_cast<int4*>(out + bf_offset(r, c * 8)) = *reinterpret_cast<const int4*>(h);
     }
@@ -786,7 +808,8 @@ __global__ void chunk_max_kernel(int64_t nch, const float* __restrict__ nrm, flo
 }
 
 struct Params {
-  const __nv_bfloat16* view;
+  const __half* view;
+  float sv;               // the view's power-of-two scale
   const float* nrm;
   const float* cmx;
   int64_t n;
@@ -819,31 +842,44 @@ __global__ void __launch_bounds__(NTHREADS, 1) bf_kernel(Params P) {
   float* st_t = reinterpret_cast<float*>(sm + OFF_T);
   float* st_e = reinterpret_cast<float*>(sm + OFF_E);
 
-  // queries -> bf16 operand blocks (zero padded); per query threshold and EPS * ||q||
-  for (int i = threadIdx.x; i < nqb * QB * 8; i += blockDim.x) {
-    const int q = i >> 3, c = i & 7;
-    __align__(16) __nv_bfloat16 h[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) h[j] = __float2bfloat16_rn(q < P.B ? __ldg(P.q + int64_t(q) * 64 + c * 8 + j) : 0.f);
-    const int qb = q / QB, m = q % QB;
-    *reinterpret_cast<int4*>(sm + OFF_A + qb * 16384 + (m >> 3) * 1024 + c * 128 + (m & 7) * 16) =
-        *reinterpret_cast<const int4*>(h);
-  }
+  // per query: power-of-two scale sq, threshold t, margin factor e and constant margin c, all in
+  // units of sv * sq (t' = t / (sv sq), e' = (EPS ||q|| + 2^-21 sq) / (sv sq),
+  // c' = 2^-21 sv ||q|| / (sv sq)); then the queries -> fp16 operand blocks (zero padded)
+  float* st_c = reinterpret_cast<float*>(sm + OFF_C);
+  float* st_sq = reinterpret_cast<float*>(sm + OFF_SQ);
   for (int q = threadIdx.x; q < nqb * QB; q += blockDim.x) {
-    float t = 0.f, e = 0.f;
+    float t = 0.f, e = 0.f, c = 0.f, sq = 1.f;
     if (q < P.B) {
-      t = key_f32(__ldg(P.tkeys + q));
-      float ss = 0.f;
+      float ss = 0.f, mx = 0.f;
       for (int k = 0; k < 64; ++k) {
         const float x = __ldg(P.q + int64_t(q) * 64 + k);
         ss = fmaf(x, x, ss);
+        mx = fmaxf(mx, fabsf(x));
       }
-      e = EPS * up_norm(ss);
+      sq = h_scale(mx);
+      const float inv = 1.f / (P.sv * sq);  // exact (power of two)
+      const float nq = up_norm(ss);
+      t = key_f32(__ldg(P.tkeys + q)) * inv;
+      e = (EPS * nq + 4.8e-7f * sq) * inv;  // 4.8e-7 = 2^-21 (1 + 0.7%)
+      c = 4.8e-7f * P.sv * nq * inv;
     }
     st_t[q] = t;
     st_e[q] = e;
+    st_c[q] = c;
+    st_sq[q] = sq;
     scnt[q] = 0;
     sbcnt[q] = 0;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nqb * QB * 8; i += blockDim.x) {
+    const int q = i >> 3, c = i & 7;
+    const float inv_sq = 1.f / st_sq[q];
+    __align__(16) __half h[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) h[j] = __float2half_rn(q < P.B ? __ldg(P.q + int64_t(q) * 64 + c * 8 + j) * inv_sq : 0.f);
+    const int qb = q / QB, m = q % QB;
+    *reinterpret_cast<int4*>(sm + OFF_A + qb * 16384 + (m >> 3) * 1024 + c * 128 + (m & 7) * 16) =
+        *reinterpret_cast<const int4*>(h);
   }
   if (threadIdx.x == 0) {
     for (int s = 0; s < NSTAGE; ++s) {
@@ -934,7 +970,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) bf_kernel(Params P) {
         tc_fence_after();
         if (qb * QB + quarter * 32 < P.B) {
           const float t = st_t[q], e = st_e[q];
-          const float slack = fabsf(t) * 1e-6f + 1e-30f;
+          const float slack = st_c[q] + fabsf(t) * 1e-6f + 1e-30f;
           uint32_t cert[2], bnd[2];
           uint32_t ra[32], rb[32];
           TMEM_LD32(tm, ra);
@@ -1166,7 +1202,21 @@ static int s1_bf_build(molr_cache* c, cudaStream_t s) {
     MOLR_CUDA(cudaMalloc(&c->s1_bnmax, size_t(xr / 32) * 4));
     c->bytes += xr * 128 + xr * 4 + xr / 8;
   }
-  build_kernel<<<c->ctx->num_sms * 8, 256, 0, s>>>(c->X, xr, c->s1_f32, c->s1_bf, c->s1_bnorm);
+  {
+    Scratch mx;
+    MOLR_TRY(mx.alloc(4, s));
+    MOLR_CUDA(cudaMemsetAsync(mx.p, 0, 4, s));
+    absmax_kernel<<<c->ctx->num_sms * 8, 256, 0, s>>>(c->X * 64, c->s1_f32, mx.as<unsigned>());
+    MOLR_LAUNCHED(c->ctx);
+    unsigned hm = 0;
+    MOLR_CUDA(cudaMemcpyAsync(&hm, mx.p, 4, cudaMemcpyDeviceToHost, s));
+    MOLR_CUDA(cudaStreamSynchronize(s));
+    float m;
+    memcpy(&m, &hm, 4);
+    if (!std::isfinite(m)) MOLR_FAIL(MOLR_ERR_INVALID, "float stage-1 view holds a non-finite value");
+    c->s1_hscale = h_scale(m);
+  }
+  build_kernel<<<c->ctx->num_sms * 8, 256, 0, s>>>(c->X, xr, c->s1_f32, 1.f / c->s1_hscale, c->s1_bf, c->s1_bnorm);
   MOLR_LAUNCHED(c->ctx);
   chunk_max_kernel<<<div_up(xr / 32, 256), 256, 0, s>>>(xr / 32, c->s1_bnorm, c->s1_bnmax);
   MOLR_LAUNCHED(c->ctx);
@@ -1194,6 +1244,7 @@ int s1_bf_scan(molr_ctx* ctx, const molr_cache* cc, int B, const float* q, const
       Scratch priv, bpriv, ccount, bcount, mx;
       Params P;
       P.view = c->s1_bf;
+      P.sv = c->s1_hscale;
       P.nrm = c->s1_bnorm;
       P.cmx = c->s1_bnmax;
       P.n = n;
@@ -1212,13 +1263,17 @@ int s1_bf_scan(molr_ctx* ctx, const molr_cache* cc, int B, const float* q, const
       P.band = bpriv.as<int32_t>();
       P.cta_counts = ccount.as<int32_t>();
       P.cta_bcounts = bcount.as<int32_t>();
-      bf_kernel<<<grid, NTHREADS, SMEM_BYTES, s>>>(P);
-      MOLR_LAUNCHED(ctx);
-      s1tc::compact_segments_kernel<<<Bc, 256, 0, s>>>(grid, seg, P.cap, P.cand, P.cta_counts, cap,
-                                                       cand + int64_t(b0) * cap, counts + b0, mx.as<int>());
-      MOLR_LAUNCHED(ctx);
-      seg_max_kernel<<<div_up(int64_t(Bc) * grid, 256), 256, 0, s>>>(int64_t(Bc) * grid, P.cta_bcounts, mx.as<int>());
-      MOLR_LAUNCHED(ctx);
+      {
+        KTimer t(ctx, "stage1_filter_bf16", s, double(Bc) * n);
+        bf_kernel<<<grid, NTHREADS, SMEM_BYTES, s>>>(P);
+        MOLR_LAUNCHED(ctx);
+        s1tc::compact_segments_kernel<<<Bc, 256, 0, s>>>(grid, seg, P.cap, P.cand, P.cta_counts, cap,
+                                                         cand + int64_t(b0) * cap, counts + b0, mx.as<int>());
+        MOLR_LAUNCHED(ctx);
+        seg_max_kernel<<<div_up(int64_t(Bc) * grid, 256), 256, 0, s>>>(int64_t(Bc) * grid, P.cta_bcounts,
+                                                                        mx.as<int>());
+        MOLR_LAUNCHED(ctx);
+      }
       int hmx = 0;
       MOLR_CUDA(cudaMemcpyAsync(&hmx, mx.p, 4, cudaMemcpyDeviceToHost, s));
       MOLR_CUDA(cudaStreamSynchronize(s));
@@ -1227,6 +1282,7 @@ int s1_bf_scan(molr_ctx* ctx, const molr_cache* cc, int B, const float* q, const
         continue;
       }
       const dim3 rg(Bc, std::max(1, std::min(grid, (4 * ctx->num_sms + Bc - 1) / Bc)));
+      KTimer t(ctx, "stage1_band_recheck", s, double(Bc));
       recheck_band_kernel<<<rg, 256, 0, s>>>(grid, seg, P.cap, P.band, P.cta_bcounts, c->s1_f32, P.q, P.tkeys, strict,
                                              cap, cand + int64_t(b0) * cap, counts + b0);
       MOLR_LAUNCHED(ctx);

@@ -15,7 +15,7 @@ X = int(sys.argv[1]) if len(sys.argv) > 1 else 10_000_000
 cfg, cache = Bm.build_shard(model, X, 0, X, seed=11, dev=dev, lib=lib, ctx=ctx, storage=L.STORE_S1_F32 | L.STORE_S1_INT8)
 gh = _gating_handle(GatingNetwork(Mlp(*model['user_net']), Mlp(*model['item_net']), Mlp(*model['cross_net'])))
 W = {k: [torch.from_numpy(a).to(dev) for a in v] for k, v in model.items()}
-kp = max(1000, X // 1000)
+kp = int(sys.argv[2]) if len(sys.argv) > 2 else max(1000, X // 1000)
 for B, modes in ((1, ("bf", "simt", "int8")), (64, ("bf", "simt", "int8")), (1024, ("bf", "simt", "int8"))):
     feats_h, feats_d = Bm.make_queries(model, B, 1, dev)
     ue = torch.empty((B, 8, 64), device=dev); uw = torch.empty((B, 64), device=dev)
