@@ -582,12 +582,12 @@ def main():
             r = {"kernel": name, "bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                  "frac": achieved / pk["hbm_gbs"], "traffic": None, "units_per_launch": units,
                  "per_unit": f"{PAIR_BYTES} B per (query, candidate) pair", "peak_src": pk["src"]}
-        elif name == "stage1_filter_bf16":
+        elif name == "stage1_filter_f16":
             achieved = units * S1_OPS / per_launch_s / 1e12
             r = {"kernel": name, "bound": "tensor", "achieved": achieved, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
                  "frac": achieved / pk["bf16_tflops"], "traffic": None, "units_per_launch": units,
-                 "per_unit": f"{S1_OPS} bf16 flops per (query, row)", "peak_src": f"{pk['src']} bf16",
-                 "note": "bf16 pre-test + exact fp32 re-check of the undecided band (DESIGN.md K2f)"}
+                 "per_unit": f"{S1_OPS} fp16 flops per (query, row)", "peak_src": f"{pk['src']} bf16 (= fp16 dense rate)",
+                 "note": "fp16 pre-test + exact fp32 re-check of the undecided band (DESIGN.md K2f)"}
         elif name.startswith("stage1_filter"):
             achieved = units * S1_OPS / per_launch_s / 1e12
             peak_i8 = 2 * pk["bf16_tflops"]
@@ -619,7 +619,7 @@ def main():
         "config": {"workload": cfg["label"], "items": X, "items_per_gpu": Xl, "batch": B, "k": k,
                    "k_prime": cfg["k_prime"], "k_prime_per_gpu": kp_local, "sample_ratio": cfg["ratio"],
                    "lambda_per_gpu": lam_local,
-                   "stage1": None if exact else ("float view: bf16 tensor-core pre-test + exact fp32 re-check"
+                   "stage1": None if exact else ("float view: fp16 tensor-core pre-test + exact fp32 re-check"
                                                  if f32_view else "int8 (bit-exact)"),
                    "parallelism": f"item-shard x{world}",
                    "l2": ("item side L2-resident by design (exact path); user inputs fresh per step" if exact else

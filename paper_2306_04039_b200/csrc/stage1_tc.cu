@@ -1264,7 +1264,7 @@ int s1_bf_scan(molr_ctx* ctx, const molr_cache* cc, int B, const float* q, const
       P.cta_counts = ccount.as<int32_t>();
       P.cta_bcounts = bcount.as<int32_t>();
       {
-        KTimer t(ctx, "stage1_filter_bf16", s, double(Bc) * n);
+        KTimer t(ctx, "stage1_filter_f16", s, double(Bc) * n);
         bf_kernel<<<grid, NTHREADS, SMEM_BYTES, s>>>(P);
         MOLR_LAUNCHED(ctx);
         s1tc::compact_segments_kernel<<<Bc, 256, 0, s>>>(grid, seg, P.cap, P.cand, P.cta_counts, cap,
