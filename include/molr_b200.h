@@ -225,6 +225,31 @@ int molr_two_stage_top_k(molr_ctx* ctx, const molr_cache* cache, const molr_gati
                          int64_t id_offset, int64_t* out_ids, float* out_scores,
                          int64_t* out_cand, void* stream);
 
+/* ---- sharded retrieval with the single-device threshold (SURVEY §8(e) "single-GPU-equivalent
+ * threshold") --------------------------------------------------------------------------------
+ * A shard holding global rows [row_lo, row_lo + X_shard) of an X_global corpus:
+ * 1. molr_sample_top_keys: draws the SAME global sample as a single device (seeded Feistel prefix
+ *    of lam rows of X_global, hindexer.py:125), scores the rows that fall in this shard and writes
+ *    each query's n_keep largest ascending-order score keys (f32_key / i32_key; padded with 0).
+ * 2. the caller all-gathers the (B, n_keep) keys of the P shards into (B, P*n_keep) rows and
+ *    molr_select_nth_keys picks the n-th largest per row: n = max(1, round(k'*lam/X_global)) gives
+ *    exactly the single-device threshold (hindexer.py:131; the n-th largest of the union of every
+ *    shard's top n is the n-th largest of the whole sample).
+ * 3. molr_two_stage_top_k_at filters this shard with those thresholds (keys), scores the passers
+ *    by MoL and returns the shard's top-k with global ids and its passer counts; no corpus
+ *    fallback (the caller falls back when the GLOBAL count is < k, engine.py:134-135, by calling
+ *    it again with the key below every score: f32_key(-inf) = 0x007FFFFF, or 0 for raw int32).  cap_hint sizes the candidate buffer. */
+int molr_sample_top_keys(molr_ctx* ctx, const molr_cache* cache, int B, int k_u, const float* user_embs,
+                         int mode, int64_t X_global, int64_t row_lo, int64_t lam, uint64_t seed,
+                         int64_t n_keep, uint32_t* out_keys, void* stream);
+int molr_select_nth_keys(molr_ctx* ctx, int B, int64_t m, const uint32_t* keys, int64_t n,
+                         uint32_t* out_keys, void* stream);
+int molr_two_stage_top_k_at(molr_ctx* ctx, const molr_cache* cache, const molr_gating* g, int B,
+                            int k_u, const float* user_embs, const float* uw, float tau, int mode,
+                            int64_t cap_hint, const uint32_t* tkeys, int comparator, int k,
+                            int64_t id_offset, int64_t* out_ids, float* out_scores,
+                            int64_t* out_cand, void* stream);
+
 /* ---- multi-GPU merge (C1): P ranks' (B,k) lists (already all-gathered, rank-major) ------- */
 int molr_merge_top_k(molr_ctx* ctx, int P, int B, int k_in, const int64_t* ids,
                      const float* scores, int k, int64_t* out_ids, float* out_scores,

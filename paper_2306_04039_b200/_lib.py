@@ -74,6 +74,9 @@ SIGNATURES = {
     "molr_index_select": [P, P, L, P, P],
     "molr_two_stage_top_k": [P, P, P, I, I, P, P, F, I, L, L, U64, I, I, L, P, P, P, P],
     "molr_merge_top_k": [P, I, I, I, P, P, I, P, P, P],
+    "molr_sample_top_keys": [P, P, I, I, P, I, L, L, L, U64, L, P, P],
+    "molr_select_nth_keys": [P, I, L, P, L, P, P],
+    "molr_two_stage_top_k_at": [P, P, P, I, I, P, P, F, I, L, P, I, I, L, P, P, P, P],
 }
 _RESTYPES = {"molr_last_error": C.c_char_p, "molr_version": C.c_char_p, "molr_ctx_launch_count": C.c_int64}
 

@@ -338,6 +338,47 @@ int sample_threshold_f32(molr_ctx* ctx, const molr_cache* c, const int64_t* samp
   return nth_largest_rows(ctx, B, lam, ss.p, false, lam, nullptr, 0, n_rank, tkey, s);
 }
 
+
+// global sample rows inside [lo, hi) -> local row ids (order irrelevant: only the top keys matter)
+__global__ void shard_rows_kernel(int64_t lam, const int64_t* __restrict__ samp, int64_t lo, int64_t hi,
+                                  int64_t* __restrict__ loc, unsigned long long* __restrict__ cnt) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < lam; j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = samp[j];
+    if (r >= lo && r < hi) loc[atomicAdd(cnt, 1ull)] = r - lo;
+  }
+}
+
+// per query: the nk largest score keys (the nk-th largest is t[b]: every key > t plus copies of t),
+// padded with 0 (below every real key) up to n_keep
+__global__ void __launch_bounds__(256) top_keys_kernel(int64_t m, const void* __restrict__ sc, int is_int,
+                                                      const uint32_t* __restrict__ t, int64_t nk, int64_t n_keep,
+                                                      uint32_t* __restrict__ out) {
+  __shared__ unsigned long long n_gt;
+  const int b = blockIdx.x;
+  if (threadIdx.x == 0) n_gt = 0;
+  __syncthreads();
+  uint32_t* o = out + int64_t(b) * n_keep;
+  const uint32_t tb = nk > 0 ? t[b] : 0u;
+  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
+    const int64_t idx = int64_t(b) * m + i;
+    const uint32_t key = is_int ? i32_key(reinterpret_cast<const int32_t*>(sc)[idx])
+                                : f32_key(reinterpret_cast<const float*>(sc)[idx]);
+    if (key > tb) {
+      const unsigned long long p = atomicAdd(&n_gt, 1ull);
+      if ((int64_t)p < nk) o[p] = key;
+    }
+  }
+  __syncthreads();
+  const int64_t filled = (int64_t)n_gt < nk ? (int64_t)n_gt : nk;
+  for (int64_t i = filled + threadIdx.x; i < n_keep; i += blockDim.x)
+    o[i] = i < nk ? tb : 0u;
+}
+
+__global__ void fill_i64_kernel(int n, int64_t v, int64_t* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = v;
+}
+
 }  // namespace molr
 
 using namespace molr;
@@ -503,19 +544,24 @@ int molr_index_select(molr_ctx* ctx, const molr_cache* c, int64_t n, const int64
 //  4. scan + threshold filter, passers appended per query                      hindexer.py:155,159-163
 //  5. MoL scoring of each query's passers; fallback to the corpus if < k      engine.py:134-137
 //  6. top-k by (score desc, id asc)                                            mol.py:407
-int molr_two_stage_top_k(molr_ctx* ctx, const molr_cache* c, const molr_gating* g, int B, int k_u, const float* ue,
-                         const float* uw, float tau, int mode, int64_t k_prime, int64_t lam, uint64_t seed,
-                         int comparator, int k, int64_t id_offset, int64_t* out_ids, float* out_scores,
-                         int64_t* out_cand, void* stream) {
+// tkeys_in != null: the per-query thresholds are given (molr_two_stage_top_k_at) and steps 2-3
+// are skipped; no_fallback: queries with < k passers keep their short lists (the caller decides
+// the fallback from the global counts).
+static int two_stage_impl(molr_ctx* ctx, const molr_cache* c, const molr_gating* g, int B, int k_u, const float* ue,
+                          const float* uw, float tau, int mode, int64_t k_prime, int64_t lam, uint64_t seed,
+                          int comparator, int k, int64_t id_offset, int64_t* out_ids, float* out_scores,
+                          int64_t* out_cand, void* stream, const uint32_t* tkeys_in, bool no_fallback) {
   if (!ctx) MOLR_FAIL(MOLR_ERR_INVALID, "null ctx");
   MOLR_TRY(mol_common_checks(c, g, k_u));
   MOLR_TRY(check_view(c, mode));
   if (c->d1 != c->d) MOLR_FAIL(MOLR_ERR_DIMENSION, "stage-1 dim %d != d %d", c->d1, c->d);
   if (k_prime < 1) MOLR_FAIL(MOLR_ERR_INVALID, "k_prime must be >= 1");
-  if (k_prime > c->X) MOLR_FAIL(MOLR_ERR_OUT_OF_RANGE, "k_prime %lld exceeds corpus %lld", (long long)k_prime,
-                                (long long)c->X);
-  if (lam < 1 || lam > c->X) MOLR_FAIL(MOLR_ERR_OUT_OF_RANGE, "lambda %lld outside [1, %lld]", (long long)lam,
-                                       (long long)c->X);
+  if (!tkeys_in) {
+    if (k_prime > c->X) MOLR_FAIL(MOLR_ERR_OUT_OF_RANGE, "k_prime %lld exceeds corpus %lld", (long long)k_prime,
+                                  (long long)c->X);
+    if (lam < 1 || lam > c->X) MOLR_FAIL(MOLR_ERR_OUT_OF_RANGE, "lambda %lld outside [1, %lld]", (long long)lam,
+                                         (long long)c->X);
+  }
   if (k < 1) MOLR_FAIL(MOLR_ERR_OUT_OF_RANGE, "k=%d", k);
   if (mode != MOLR_S1_FLOAT && (c->d1 % 16) != 0) MOLR_FAIL(MOLR_ERR_DIMENSION, "int8 batched scan needs d1%%16==0");
   MOLR_CUDA(cudaSetDevice(ctx->device));
@@ -539,7 +585,7 @@ int molr_two_stage_top_k(molr_ctx* ctx, const molr_cache* c, const molr_gating* 
   segs.X = X;
   Scratch cand, counts, sb, se;
   std::vector<int64_t> hcnt(B, X);
-  if (k_prime < X) {
+  if (k_prime < X || tkeys_in) {
     // 1. queries
     Scratch q, qc, qs;
     MOLR_TRY(q.alloc(size_t(B) * c->d * 4, s));
@@ -550,6 +596,11 @@ int molr_two_stage_top_k(molr_ctx* ctx, const molr_cache* c, const molr_gating* 
       MOLR_TRY(qs.alloc(size_t(B) * 4, s));
       MOLR_TRY(prepare_queries(ctx, mode, B, c->d1, q.as<float>(), qc.as<int8_t>(), qs.as<float>(), s));
     }
+    Scratch ss, tkey;
+    MOLR_TRY(tkey.alloc(size_t(B) * 4, s));
+    if (tkeys_in) {
+      MOLR_CUDA(cudaMemcpyAsync(tkey.p, tkeys_in, size_t(B) * 4, cudaMemcpyDefault, s));
+    } else {
     // 2. sample
     int bits = 2;
     while ((int64_t(1) << bits) < X) bits += 2;
@@ -561,8 +612,6 @@ int molr_two_stage_top_k(molr_ctx* ctx, const molr_cache* c, const molr_gating* 
     // 3. sample scores [B][lam] then n-th largest per query
     const double nr = std::nearbyint(double(k_prime * lam) / double(X));  // Python round(): half-even
     const int64_t n_rank = std::max<int64_t>(1, (int64_t)nr);
-    Scratch ss, tkey;
-    MOLR_TRY(tkey.alloc(size_t(B) * 4, s));
     const bool use_tc = s1_tc_supported(c, mode);
     if (use_tc) {
       // gather the sample rows into a contiguous operand, then the tensor-core scan writes scores
@@ -590,6 +639,8 @@ int molr_two_stage_top_k(molr_ctx* ctx, const molr_cache* c, const molr_gating* 
       MOLR_TRY(nth_largest_rows(ctx, B, lam, ss.p, mode == MOLR_S1_INT8_RAW, lam, nullptr, 0, n_rank,
                                 tkey.as<uint32_t>(), s));
     }
+    }  // thresholds
+    const bool use_tc = s1_tc_supported(c, mode);
     // 4. filter scan with capacity; retry once with the exact maximum if it overflowed
     int64_t cap = imin64(X, k_prime + k_prime / 4 + 1024);
     MOLR_TRY(counts.alloc(size_t(B) * 8, s));
@@ -642,7 +693,7 @@ int molr_two_stage_top_k(molr_ctx* ctx, const molr_cache* c, const molr_gating* 
     segs.ids = cand.as<int32_t>();
     // 5. MoL over passers; queries with < k passers fall back to the whole corpus (engine.py:134-135)
     std::vector<int> fallback;
-    for (int b = 0; b < B; ++b)
+    for (int b = 0; b < B && !no_fallback; ++b)
       if (hcnt[b] < kk) fallback.push_back(b);
     int64_t cand_total = int64_t(B) * cap;
     double pairs = 0;
@@ -703,6 +754,123 @@ int molr_two_stage_top_k(molr_ctx* ctx, const molr_cache* c, const molr_gating* 
   if (out_cand) MOLR_CUDA(cudaMemcpyAsync(oc.dptr, hcnt.data(), size_t(B) * 8, cudaMemcpyDefault, s));
   MOLR_CUDA(cudaStreamSynchronize(s));  // hcnt lives on this stack frame
   return finish_outputs(s, {&oi, &os, &oc});
+}
+
+int molr_two_stage_top_k(molr_ctx* ctx, const molr_cache* c, const molr_gating* g, int B, int k_u, const float* ue,
+                         const float* uw, float tau, int mode, int64_t k_prime, int64_t lam, uint64_t seed,
+                         int comparator, int k, int64_t id_offset, int64_t* out_ids, float* out_scores,
+                         int64_t* out_cand, void* stream) {
+  return two_stage_impl(ctx, c, g, B, k_u, ue, uw, tau, mode, k_prime, lam, seed, comparator, k, id_offset, out_ids,
+                        out_scores, out_cand, stream, nullptr, false);
+}
+
+int molr_two_stage_top_k_at(molr_ctx* ctx, const molr_cache* c, const molr_gating* g, int B, int k_u, const float* ue,
+                            const float* uw, float tau, int mode, int64_t cap_hint, const uint32_t* tkeys,
+                            int comparator, int k, int64_t id_offset, int64_t* out_ids, float* out_scores,
+                            int64_t* out_cand, void* stream) {
+  if (!tkeys) MOLR_FAIL(MOLR_ERR_INVALID, "null thresholds");
+  return two_stage_impl(ctx, c, g, B, k_u, ue, uw, tau, mode, std::max<int64_t>(1, std::min<int64_t>(cap_hint, c ? c->X : 1)),
+                        1, 0, comparator, k, id_offset, out_ids, out_scores, out_cand, stream, tkeys, true);
+}
+
+int molr_sample_top_keys(molr_ctx* ctx, const molr_cache* c, int B, int k_u, const float* ue, int mode,
+                         int64_t X_global, int64_t row_lo, int64_t lam, uint64_t seed, int64_t n_keep,
+                         uint32_t* out_keys, void* stream) {
+  if (!ctx || !c) MOLR_FAIL(MOLR_ERR_INVALID, "null ctx/cache");
+  MOLR_TRY(check_view(c, mode));
+  if (c->d1 != c->d) MOLR_FAIL(MOLR_ERR_DIMENSION, "stage-1 dim %d != d %d", c->d1, c->d);
+  if (X_global < c->X || row_lo < 0 || row_lo + c->X > X_global)
+    MOLR_FAIL(MOLR_ERR_OUT_OF_RANGE, "shard [%lld, %lld) outside the corpus [0, %lld)", (long long)row_lo,
+              (long long)(row_lo + c->X), (long long)X_global);
+  if (lam < 1 || lam > X_global) MOLR_FAIL(MOLR_ERR_OUT_OF_RANGE, "lambda %lld outside [1, %lld]", (long long)lam,
+                                           (long long)X_global);
+  if (n_keep < 1) MOLR_FAIL(MOLR_ERR_OUT_OF_RANGE, "n_keep=%lld", (long long)n_keep);
+  MOLR_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t s = pick_stream(ctx, stream);
+  if (B <= 0) return MOLR_OK;
+  WorkspaceScope ws(ctx, s);
+  In iue;
+  MOLR_TRY(iue.stage(ue, size_t(B) * k_u * c->d * 4, s));
+  Out ok;
+  MOLR_TRY(ok.stage(out_keys, size_t(B) * n_keep * 4, s));
+  Scratch q, qc, qs;
+  MOLR_TRY(q.alloc(size_t(B) * c->d * 4, s));
+  s1_query_kernel<<<div_up(int64_t(B) * c->d, 256), 256, 0, s>>>(B, k_u, c->d, iue.as<float>(), q.as<float>());
+  MOLR_LAUNCHED(ctx);
+  if (mode != MOLR_S1_FLOAT) {
+    MOLR_TRY(qc.alloc(size_t(B) * c->d1, s));
+    MOLR_TRY(qs.alloc(size_t(B) * 4, s));
+    MOLR_TRY(prepare_queries(ctx, mode, B, c->d1, q.as<float>(), qc.as<int8_t>(), qs.as<float>(), s));
+  }
+  // the global sample (same Feistel permutation prefix as a single device), restricted to this shard
+  int bits = 2;
+  while ((int64_t(1) << bits) < X_global) bits += 2;
+  Scratch samp, loc, cnt;
+  MOLR_TRY(samp.alloc(size_t(lam) * 8, s));
+  MOLR_TRY(loc.alloc(size_t(lam) * 8, s));
+  MOLR_TRY(cnt.alloc(8, s));
+  feistel_sample_kernel<<<std::min(div_up(lam, 256), ctx->num_sms * 8), 256, 0, s>>>(X_global, lam, seed, bits / 2,
+                                                                                     samp.as<int64_t>());
+  MOLR_LAUNCHED(ctx);
+  MOLR_CUDA(cudaMemsetAsync(cnt.p, 0, 8, s));
+  shard_rows_kernel<<<std::min(div_up(lam, 256), ctx->num_sms * 8), 256, 0, s>>>(lam, samp.as<int64_t>(), row_lo,
+                                                                                 row_lo + c->X, loc.as<int64_t>(),
+                                                                                 cnt.as<unsigned long long>());
+  MOLR_LAUNCHED(ctx);
+  unsigned long long hm = 0;
+  MOLR_CUDA(cudaMemcpyAsync(&hm, cnt.p, 8, cudaMemcpyDeviceToHost, s));
+  MOLR_CUDA(cudaStreamSynchronize(s));
+  const int64_t m = (int64_t)hm;
+  const int64_t nk = std::min<int64_t>(n_keep, m);
+  Scratch ss, tk;
+  MOLR_TRY(tk.alloc(size_t(B) * 4, s));
+  if (m > 0) {
+    MOLR_TRY(ss.alloc(size_t(B) * m * 4, s));
+    if (s1_tc_supported(c, mode)) {
+      const int64_t lp = (m + 255) / 256 * 256;
+      Scratch scodes, sscales;
+      MOLR_TRY(scodes.alloc(size_t(lp) * 64, s));
+      MOLR_TRY(sscales.alloc(size_t(lp) * 4, s));
+      MOLR_CUDA(cudaMemsetAsync(scodes.p, 0, size_t(lp) * 64, s));
+      MOLR_CUDA(cudaMemsetAsync(sscales.p, 0, size_t(lp) * 4, s));
+      MOLR_TRY(s1_seal(const_cast<molr_cache*>(c), s));
+      gather_sample_kernel<<<std::min(div_up(m * 4, 256), ctx->num_sms * 8), 256, 0, s>>>(
+          c->s1_codes, c->s1_scales, c->s1_inv, loc.as<int64_t>(), m, scodes.as<int8_t>(), sscales.as<float>());
+      MOLR_LAUNCHED(ctx);
+      MOLR_TRY(s1_tc_scan(ctx, mode, scodes.as<int8_t>(), sscales.as<float>(), nullptr, nullptr, m, B, qc.as<int8_t>(),
+                          nullptr, 0, 0, nullptr, nullptr, ss.p, m, s));
+    } else {
+      if (mode != MOLR_S1_FLOAT && c->s1_codes) MOLR_TRY(s1_seal(const_cast<molr_cache*>(c), s));
+      MOLR_TRY(scan_scores(ctx, mode, m, c->d1, c->s1_f32, c->s1_codes, s1_interleaved(c->d1), c->s1_inv, c->s1_scales,
+                           loc.as<int64_t>(), B, q.as<float>(), qc.as<int8_t>(), ss.p, m, s));
+    }
+    MOLR_TRY(nth_largest_rows(ctx, B, m, ss.p, mode == MOLR_S1_INT8_RAW, m, nullptr, 0, nk, tk.as<uint32_t>(), s));
+  }
+  top_keys_kernel<<<B, 256, 0, s>>>(m, ss.p, mode == MOLR_S1_INT8_RAW, tk.as<uint32_t>(), nk, n_keep, ok.as<uint32_t>());
+  MOLR_LAUNCHED(ctx);
+  MOLR_CUDA(cudaStreamSynchronize(s));
+  return finish_outputs(s, {&ok});
+}
+
+int molr_select_nth_keys(molr_ctx* ctx, int B, int64_t m, const uint32_t* keys, int64_t n, uint32_t* out_keys,
+                         void* stream) {
+  if (!ctx) MOLR_FAIL(MOLR_ERR_INVALID, "null ctx");
+  if (n < 1 || n > m) MOLR_FAIL(MOLR_ERR_OUT_OF_RANGE, "n=%lld outside [1, %lld]", (long long)n, (long long)m);
+  MOLR_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t s = pick_stream(ctx, stream);
+  if (B <= 0) return MOLR_OK;
+  WorkspaceScope ws(ctx, s);
+  In ik;
+  MOLR_TRY(ik.stage(keys, size_t(B) * m * 4, s));
+  Out ok;
+  MOLR_TRY(ok.stage(out_keys, size_t(B) * 4, s));
+  Scratch counts;
+  MOLR_TRY(counts.alloc(size_t(B) * 8, s));
+  fill_i64_kernel<<<div_up(B, 256), 256, 0, s>>>(B, m, counts.as<int64_t>());
+  MOLR_LAUNCHED(ctx);
+  MOLR_TRY(nth_largest_keys(ctx, B, m, ik.as<uint32_t>(), counts.as<int64_t>(), n, ok.as<uint32_t>(), nullptr, s));
+  MOLR_CUDA(cudaStreamSynchronize(s));
+  return finish_outputs(s, {&ok});
 }
 
 }  // extern "C"

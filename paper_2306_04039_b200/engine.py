@@ -182,6 +182,66 @@ class BatchedRetrievalEngine:
         return batch_mol_top_k(self.cache, self.gating, user_embs, user_feats, min(k, self.num_items))
 
 
+def two_stage_top_k_sharded(cache, gating: GatingNetwork, user_embs, uw, k: int, hconfig: HIndexerConfig, *,
+                            X_global: int, row_lo: int, exchange, seed: int = 0):
+    """Two-stage top-k over one shard (global rows [row_lo, row_lo + cache.num_items)) that returns
+    EXACTLY the single-device result of `two_stage_top_k` over the whole X_global corpus (SURVEY
+    §8(e), "single-GPU-equivalent threshold"): every shard scores its part of the same global
+    sample, the shards exchange each query's top n sample-score keys, and the n-th largest of that
+    union is the single-device threshold (hindexer.py:131).  The fallback to the corpus
+    (engine.py:134-135) is decided on the GLOBAL passer count.
+
+    `exchange(a)` all-gathers a NumPy array over the shards and returns the rank-major stack
+    (P, *a.shape) — e.g. torch.distributed.all_gather, or a list of in-process shards in tests.
+    Returns (ids (B,k) global, scores (B,k), global candidate counts (B,)), identical on every
+    shard."""
+    B, k_u = int(user_embs.shape[0]), int(user_embs.shape[1])
+    Xs = cache.num_items
+    ue = L.f32(np.asarray(user_embs))
+    uwf = L.f32(np.asarray(uw))
+    mode = _mode(hconfig)
+    lam = hconfig.resolve_lambda(X_global)  # raises OutOfRangeError for K' > X like the reference
+    kp = int(hconfig.k_prime)
+    # the key below every score: f32_key(-inf) (scaled / float views) or i32_key(INT32_MIN) (raw)
+    pass_all = 0 if mode == L.S1_INT8_RAW else 0x007FFFFF
+    if kp >= X_global:
+        tkeys = np.full(B, pass_all, dtype=np.uint32)  # every row passes (hindexer.py:151-154)
+    else:
+        n_rank = max(1, round(kp * lam / X_global))  # Python round(): half-even, as hindexer.py:131
+        keys = np.empty((B, n_rank), dtype=np.uint32)
+        L.call("molr_sample_top_keys", L.ctx(), cache.device_handle(), B, k_u, L.ptr(ue), mode, int(X_global),
+               int(row_lo), int(lam), int(seed) & (2**64 - 1), int(n_rank), L.ptr(keys), None)
+        allk = np.asarray(exchange(keys))  # (P, B, n_rank)
+        rows = np.ascontiguousarray(allk.transpose(1, 0, 2).reshape(B, -1))
+        tkeys = np.empty(B, dtype=np.uint32)
+        L.call("molr_select_nth_keys", L.ctx(), B, rows.shape[1], L.ptr(rows), int(n_rank), L.ptr(tkeys), None)
+    comp = L.STRICT if hconfig.comparator == "strict" else L.INCLUSIVE
+    cap_hint = max(1, min(Xs, -(-kp * Xs // X_global)))
+
+    def run(sel, tk, cap):
+        ids = np.empty((len(sel), k), dtype=np.int64)
+        sc = np.empty((len(sel), k), dtype=np.float32)
+        cnt = np.empty(len(sel), dtype=np.int64)
+        ue_s = np.ascontiguousarray(ue[sel])  # (named: the buffers must outlive the call)
+        uw_s = np.ascontiguousarray(uwf[sel])
+        tk_s = np.ascontiguousarray(tk, dtype=np.uint32)
+        L.call("molr_two_stage_top_k_at", L.ctx(), cache.device_handle(), _gating_handle(gating), len(sel), k_u,
+               L.ptr(ue_s), L.ptr(uw_s), float(cache.config.tau), mode, int(cap), L.ptr(tk_s), comp, int(k),
+               int(row_lo), L.ptr(ids), L.ptr(sc), L.ptr(cnt), None)
+        return ids, sc, cnt
+
+    allq = np.arange(B)
+    ids, sc, cnt = run(allq, tkeys, cap_hint)
+    gcnt = np.asarray(exchange(cnt)).sum(axis=0)
+    short = np.nonzero(gcnt < min(k, X_global))[0]
+    if short.size:  # fewer than k candidates in the whole corpus: score every row (engine.py:134-135)
+        fi, fs, _ = run(short, np.full(short.size, pass_all, dtype=np.uint32), Xs)
+        ids[short], sc[short] = fi, fs
+        gcnt[short] = X_global
+    out_i, out_s = merge_top_k(np.asarray(exchange(ids)), np.asarray(exchange(sc)), k)
+    return out_i, out_s, gcnt
+
+
 def merge_top_k(ids, scores, k: int):
     """Merge P rank-major (P,B,k_in) per-shard top-k lists into the global top-k (C1 merge)."""
     ids = np.ascontiguousarray(ids, dtype=np.int64)

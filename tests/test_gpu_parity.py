@@ -608,6 +608,74 @@ def test_batched_float_view_tc_matches_fp32_scan(nb, monkeypatch):
                     assert abs(int(a[2][u]) - c_ids.size) <= 2, (comp, u, a[2][u], c_ids.size)
 
 
+def _run_shards(fn, P):
+    """Run fn(rank, exchange) for P in-process shards on threads, with a barrier all-gather."""
+    import threading
+
+    bar = threading.Barrier(P)
+    slots = [None] * P
+    out = [None] * P
+    err = []
+
+    def exchange_for(r):
+        def ex(a):
+            slots[r] = np.array(a, copy=True)
+            bar.wait()
+            res = np.stack(slots)
+            bar.wait()
+            return res
+        return ex
+
+    def body(r):
+        try:
+            out[r] = fn(r, exchange_for(r))
+        except BaseException as e:  # keep the other shards from hanging
+            err.append(e)
+            bar.abort()
+
+    th = [threading.Thread(target=body, args=(r,)) for r in range(P)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    if err:
+        raise err[0]
+    return out
+
+
+@pytest.mark.parametrize("quantized,comp,kp", [(True, "inclusive", 2000), (True, "strict", 2000),
+                                               (False, "inclusive", 2000), (True, "inclusive", 5)])
+def test_sharded_global_threshold_equals_single_device(quantized, comp, kp):
+    """Item-range shards with the single-device-equivalent threshold: three uneven
+    shards exchanging their top sample keys return EXACTLY the single-device two_stage_top_k result
+    (ids, scores, candidate counts), int8 and float views, both comparators, and the global
+    fallback to the whole corpus when K' < k."""
+    from paper_2306_04039_b200.engine import two_stage_top_k, two_stage_top_k_sharded
+    from paper_2306_04039_b200.hindexer import HIndexerConfig
+    from paper_2306_04039_b200.mol import ItemCache
+    from paper_2306_04039_b200.quant import QuantizedRows
+
+    cache, syn, ue, feats = _synthetic_prod_cache(90_001, seed=51, n_users=40)
+    gating, og = _prod_gating(syn)
+    uw = gating.user_net(feats)
+    X = cache.num_items
+    hcfg = HIndexerConfig(k_prime=kp, sample_ratio=0.05, quantized=quantized, comparator=comp)
+    ref = two_stage_top_k(cache, gating, ue, uw, 20, hcfg, seed=7)
+    cuts = [0, 20_000, 61_111, X]
+    shards = []
+    for lo, hi in zip(cuts[:-1], cuts[1:]):
+        q = cache.stage1_q
+        shards.append(ItemCache(config=cache.config, item_embs=cache.item_embs[lo:hi],
+                                item_gate_pre=cache.item_gate_pre[lo:hi], stage1_embs=cache.stage1_embs[lo:hi],
+                                stage1_q=QuantizedRows(q.codes[lo:hi], q.scales[lo:hi])))
+    res = _run_shards(lambda r, ex: two_stage_top_k_sharded(shards[r], gating, ue, uw, 20, hcfg, X_global=X,
+                                                            row_lo=cuts[r], exchange=ex, seed=7), 3)
+    for ids, sc, cnt in res:
+        np.testing.assert_array_equal(cnt, ref[2])
+        np.testing.assert_array_equal(ids, ref[0])
+        np.testing.assert_array_equal(sc, ref[1])
+
+
 def test_batched_two_stage_recall_device_sample():
     """Device-drawn sample (lambda = 1% of X): candidate counts near K' and top-100 recall vs the
     oracle's exact MoL top-100 >= 0.99 (north-star bar), 100k items."""
