@@ -318,6 +318,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--recall-queries", type=int, default=8)
+    ap.add_argument("--local-threshold", action="store_true",
+                    help="N>1: per-shard K'/N and lambda/N thresholds instead of the single-device threshold")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if args.items:
@@ -363,6 +365,12 @@ def main():
     exact = cfg.get("exact", False)
     kp_local = None if exact else local_k_prime(cfg["k_prime"], world)
     lam_local = None if exact else local_lambda(Xl, sample_ratio=cfg["ratio"])
+    # N>1 default: the single-device threshold (every shard scores its part of the same global
+    # sample, the shards all-gather each query's top n sample keys, the n-th largest of the union is
+    # the 1-GPU threshold), so the N-GPU result equals the 1-GPU result bit for bit
+    global_thr = world > 1 and not exact and not args.local_threshold
+    lam_g = None if exact else local_lambda(X, sample_ratio=cfg["ratio"])
+    n_rank = None if exact else max(1, round(cfg["k_prime"] * lam_g / X))
 
     model = synthetic_model()
     t_build = time.perf_counter()
@@ -386,6 +394,11 @@ def main():
     gat_sc = torch.empty((world, B, k), dtype=torch.float32, device=dev)
     out_ids = torch.empty((B, k), dtype=torch.int64, device=dev)
     out_sc = torch.empty((B, k), dtype=torch.float32, device=dev)
+    if global_thr:
+        keys_d = torch.empty((B, n_rank), dtype=torch.int32, device=dev)
+        gat_keys = torch.empty((world, B, n_rank), dtype=torch.int32, device=dev)
+        tk_d = torch.empty((B,), dtype=torch.int32, device=dev)
+        cnt_t = torch.empty((B,), dtype=torch.int64, device=dev)
     stream = torch.cuda.current_stream()
     sp = stream.cuda_stream
 
@@ -407,6 +420,27 @@ def main():
                    oi, osc, sp)
             if world > 1:
                 ids_d.add_(lo)
+        elif global_thr:
+            L.call("molr_sample_top_keys", ctx, cache.device_handle(), B, K_U, ue_ptr, s1_mode, X, lo, lam_g, 1000 + i,
+                   n_rank, keys_d.data_ptr(), sp)
+            all_gather(gat_keys, keys_d)
+            rows = gat_keys.permute(1, 0, 2).reshape(B, world * n_rank).contiguous()
+            L.call("molr_select_nth_keys", ctx, B, world * n_rank, rows.data_ptr(), n_rank, tk_d.data_ptr(), sp)
+            L.call("molr_two_stage_top_k_at", ctx, cache.device_handle(), gh, B, K_U, ue_ptr, uw_d.data_ptr(), TAU,
+                   s1_mode, kp_local, tk_d.data_ptr(), L.INCLUSIVE, k, lo, oi, osc, L.ptr(cand_h), sp)
+            cnt_t.copy_(torch.from_numpy(cand_h))
+            all_reduce_sum(cnt_t)
+            short = torch.nonzero(cnt_t < min(k, X)).flatten().tolist()
+            if short:  # fewer than k candidates in the whole corpus: every row (engine.py:134-135)
+                sel = torch.tensor(short, device=dev)
+                ue_s, uw_s = ue_d[sel].contiguous(), uw_d[sel].contiguous()
+                tk_s = torch.full((len(short),), 0x007FFFFF, dtype=torch.int32, device=dev)
+                fi = torch.empty((len(short), k), dtype=torch.int64, device=dev)
+                fs = torch.empty((len(short), k), dtype=torch.float32, device=dev)
+                L.call("molr_two_stage_top_k_at", ctx, cache.device_handle(), gh, len(short), K_U, ue_s.data_ptr(),
+                       uw_s.data_ptr(), TAU, s1_mode, Xl, tk_s.data_ptr(), L.INCLUSIVE, k, lo, fi.data_ptr(),
+                       fs.data_ptr(), None, sp)
+                ids_d[sel], sc_d[sel] = fi, fs
         else:
             L.call("molr_two_stage_top_k", ctx, cache.device_handle(), gh, B, K_U, ue_ptr, uw_d.data_ptr(), TAU,
                    s1_mode, kp_local, lam_local, 1000 + i, L.INCLUSIVE, k, lo, oi, osc, L.ptr(cand_h), sp)
@@ -425,6 +459,14 @@ def main():
             out.copy_(torch.stack(parts).to(out.device))
         else:
             dist.all_gather_into_tensor(out, inp)
+
+    def all_reduce_sum(t):
+        if share:
+            c = t.cpu()
+            dist.all_reduce(c)
+            t.copy_(c)
+        else:
+            dist.all_reduce(t)
 
     def all_reduce_max(t):
         if share:
@@ -532,7 +574,13 @@ def main():
 
     # ---------------- recall vs the exact MoL top-k (GPU exact path, parity-tested vs the oracle) ----
     R = min(args.recall_queries, B)
-    res_i, _ = step(0, feats_d.data_ptr())
+    res_i, res_s = step(0, feats_d.data_ptr())
+    torch.cuda.synchronize()
+    # digest of the whole batch's top-k (ids + score bits): with the single-device threshold the
+    # N-GPU digest equals the 1-GPU digest
+    import hashlib
+
+    digest = hashlib.sha1(res_i.cpu().numpy().tobytes() + res_s.cpu().numpy().tobytes()).hexdigest()[:16]
     two = res_i[:R].cpu().numpy()
     ex_i = torch.empty((R, k), dtype=torch.int64, device=dev)
     ex_s = torch.empty((R, k), dtype=torch.float32, device=dev)
@@ -622,10 +670,12 @@ def main():
                    "stage1": None if exact else ("float view: fp16 tensor-core pre-test + exact fp32 re-check"
                                                  if f32_view else "int8 (bit-exact)"),
                    "parallelism": f"item-shard x{world}",
+                   "threshold": None if exact else ("single-device (global sample, top-n key all-gather)"
+                                                    if (global_thr or world == 1) else "per-shard (K'/N, lambda/N)"),
                    "l2": ("item side L2-resident by design (exact path); user inputs fresh per step" if exact else
                           "inputs larger than L2 (corpus shard x 1.2 KB per item >> 126 MB)")},
         "p50_batch_latency_ms": float(np.median(step_ms)), "step_ms": [round(x, 3) for x in step_ms], "step_host_ms": host_ms, "p50_single_query_latency_ms": float(np.median(lat)),
-        "recall_at_k_vs_exact_mol": recall, "recall_queries": R,
+        "recall_at_k_vs_exact_mol": recall, "result_digest_step0": digest, "recall_queries": R,
         "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "step_ms": [round(x, 3) for x in e2e_step_ms]},
         "gpu_launches": int(launches), "roofline": roof, "rooflines": rooflines, "kernels": kernels,
