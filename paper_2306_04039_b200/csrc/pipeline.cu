@@ -300,12 +300,25 @@ int sample_threshold_f32(molr_ctx* ctx, const molr_cache* c, const int64_t* samp
     MOLR_TRY(counts.alloc(size_t(B) * 8, s));
     MOLR_TRY(flag.alloc(sizeof(int) * 2, s));
     {
-      KTimer t(ctx, "stage1_sample_scan", s, double(B) * lam);
+      KTimer t(ctx, "stage1_sample_pilot", s, double(B) * lam0);
       MOLR_TRY(scan_scores(ctx, MOLR_S1_FLOAT, lam0, 64, c->s1_f32, nullptr, false, nullptr, nullptr, samp, B, q, nullptr,
                            pilot.p, lam0, s));
       MOLR_TRY(nth_largest_rows(ctx, B, lam0, pilot.p, false, lam0, nullptr, 0, n0, t0.as<uint32_t>(), s));
       MOLR_CUDA(cudaMemsetAsync(counts.p, 0, size_t(B) * 8, s));
       MOLR_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int) * 2, s));
+    }
+    if (s1_bf_supported(c, MOLR_S1_FLOAT) && B >= 2) {
+      // the sampled rows' fp16 image through the tensor-core filter (>= t0, exact fp32 re-check),
+      // then the exact fp32 keys of the passers
+      Scratch f32r, himg, hn, hc, pids;
+      F16View V;
+      MOLR_TRY(s1_f16_image(ctx, c, samp, lam, f32r, himg, hn, hc, &V, s));
+      MOLR_TRY(pids.alloc(size_t(B) * cap * 4, s));
+      MOLR_TRY(s1_f16_filter(ctx, V, B, q, t0.as<uint32_t>(), 0, cap, pids.as<int32_t>(), counts.as<int64_t>(), s,
+                             "stage1_sample_scan_f16"));
+      MOLR_TRY(s1_passer_keys(ctx, B, cap, pids.as<int32_t>(), counts.as<int64_t>(), V.f32, q, keys.as<uint32_t>(), s));
+    } else {
+      KTimer t(ctx, "stage1_sample_scan", s, double(B) * lam);
       const int bchunk = 128;  // 32 KB of queries per launch
       for (int b0 = 0; b0 < B; b0 += bchunk) {
         const int bb = std::min(bchunk, B - b0);

@@ -26,6 +26,20 @@ int s1_seal(molr_cache* c, cudaStream_t s);
 // float view (MOLR_S1_FLOAT) on the tensor cores: bf16 MMA pre-test + exact fp32 re-check of the
 // band the bf16 rounding cannot decide (same candidate set as the fp32 scan)
 bool s1_bf_supported(const molr_cache* c, int mode);
+struct F16View {  // fp16 image of an fp32 row matrix (d = 64) for s1_f16_filter
+  const __half* h;
+  const float* nrm;  // per-row ||v||_2 (rounded up)
+  const float* cmx;  // per-32-row max of nrm
+  float sv;          // power-of-two scale of the image
+  const float* f32;  // the fp32 rows (exact re-check)
+  int64_t n;
+};
+int s1_f16_filter(molr_ctx* ctx, const F16View& V, int B, const float* q, const uint32_t* tkeys, int strict,
+                  int64_t cap, int32_t* cand, int64_t* counts, cudaStream_t s, const char* timer);
+int s1_f16_image(molr_ctx* ctx, const molr_cache* c, const int64_t* rows, int64_t n, Scratch& f32, Scratch& h,
+                 Scratch& nrm, Scratch& cmx, F16View* out, cudaStream_t s);
+int s1_passer_keys(molr_ctx* ctx, int B, int64_t cap, const int32_t* ids, const int64_t* counts, const float* vf,
+                   const float* q, uint32_t* keys, cudaStream_t s);
 int s1_bf_scan(molr_ctx* ctx, const molr_cache* c, int B, const float* q, const uint32_t* tkeys, int strict,
                int64_t cap, int32_t* cand, int64_t* counts, cudaStream_t s);
 int int_to_float_inplace(molr_ctx* ctx, int32_t* p, int64_t n, cudaStream_t s);

@@ -1093,6 +1093,16 @@ __global__ void __launch_bounds__(256) recheck_band_kernel(int G, int64_t seg, i
     }
   }
 }
+__global__ void gather_f32_rows_kernel(int64_t n, int64_t np, const float* __restrict__ vf, const int64_t* __restrict__ rows,
+                                       float* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < np * 16; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i >> 4;
+    const int c = int(i & 15);
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (r < n) v = __ldg(reinterpret_cast<const float4*>(vf + rows[r] * 64) + c);
+    reinterpret_cast<float4*>(out + r * 64)[c] = v;
+  }
+}
 }  // namespace s1bf
 
 bool s1_tc_supported(const molr_cache* c, int mode) {
@@ -1225,14 +1235,12 @@ static int s1_bf_build(molr_cache* c, cudaStream_t s) {
   return MOLR_OK;
 }
 
-// Filter every row of the float view against B queries: cand rows (B, cap) / counts (B,) exactly
-// as the fp32 filter scan would produce them (as a set).
-int s1_bf_scan(molr_ctx* ctx, const molr_cache* cc, int B, const float* q, const uint32_t* tkeys, int strict,
-               int64_t cap, int32_t* cand, int64_t* counts, cudaStream_t s) {
+// Filter every row of an fp16 view image against B queries: cand rows (B, cap) / counts (B,)
+// exactly as the fp32 filter scan would produce them (as a set).
+int s1_f16_filter(molr_ctx* ctx, const F16View& V, int B, const float* q, const uint32_t* tkeys, int strict,
+                  int64_t cap, int32_t* cand, int64_t* counts, cudaStream_t s, const char* timer) {
   using namespace s1bf;
-  molr_cache* c = const_cast<molr_cache*>(cc);
-  MOLR_TRY(s1_bf_build(c, s));
-  const int64_t n = c->X;
+  const int64_t n = V.n;
   if (n <= 0 || B <= 0) return MOLR_OK;
   const int64_t ntiles = (n + NT - 1) / NT;
   const int grid = (int)std::min<int64_t>(ntiles, ctx->num_sms);
@@ -1243,10 +1251,10 @@ int s1_bf_scan(molr_ctx* ctx, const molr_cache* cc, int B, const float* q, const
     for (int attempt = 0; attempt < 2; ++attempt) {
       Scratch priv, bpriv, ccount, bcount, mx;
       Params P;
-      P.view = c->s1_bf;
-      P.sv = c->s1_hscale;
-      P.nrm = c->s1_bnorm;
-      P.cmx = c->s1_bnmax;
+      P.view = V.h;
+      P.sv = V.sv;
+      P.nrm = V.nrm;
+      P.cmx = V.cmx;
       P.n = n;
       P.B = Bc;
       P.q = q + int64_t(b0) * 64;
@@ -1264,7 +1272,7 @@ int s1_bf_scan(molr_ctx* ctx, const molr_cache* cc, int B, const float* q, const
       P.cta_counts = ccount.as<int32_t>();
       P.cta_bcounts = bcount.as<int32_t>();
       {
-        KTimer t(ctx, "stage1_filter_f16", s, double(Bc) * n);
+        KTimer t(ctx, timer, s, double(Bc) * n);
         bf_kernel<<<grid, NTHREADS, SMEM_BYTES, s>>>(P);
         MOLR_LAUNCHED(ctx);
         s1tc::compact_segments_kernel<<<Bc, 256, 0, s>>>(grid, seg, P.cap, P.cand, P.cta_counts, cap,
@@ -1283,12 +1291,74 @@ int s1_bf_scan(molr_ctx* ctx, const molr_cache* cc, int B, const float* q, const
       }
       const dim3 rg(Bc, std::max(1, std::min(grid, (4 * ctx->num_sms + Bc - 1) / Bc)));
       KTimer t(ctx, "stage1_band_recheck", s, double(Bc));
-      recheck_band_kernel<<<rg, 256, 0, s>>>(grid, seg, P.cap, P.band, P.cta_bcounts, c->s1_f32, P.q, P.tkeys, strict,
+      recheck_band_kernel<<<rg, 256, 0, s>>>(grid, seg, P.cap, P.band, P.cta_bcounts, V.f32, P.q, P.tkeys, strict,
                                              cap, cand + int64_t(b0) * cap, counts + b0);
       MOLR_LAUNCHED(ctx);
       break;
     }
   }
+  return MOLR_OK;
+}
+
+int s1_bf_scan(molr_ctx* ctx, const molr_cache* cc, int B, const float* q, const uint32_t* tkeys, int strict,
+               int64_t cap, int32_t* cand, int64_t* counts, cudaStream_t s) {
+  molr_cache* c = const_cast<molr_cache*>(cc);
+  MOLR_TRY(s1_bf_build(c, s));
+  F16View V{c->s1_bf, c->s1_bnorm, c->s1_bnmax, c->s1_hscale, c->s1_f32, c->X};
+  return s1_f16_filter(ctx, V, B, q, tkeys, strict, cap, cand, counts, s, "stage1_filter_f16");
+}
+
+// fp16 image of `n` gathered fp32 rows (the sampled rows of the float view), at the view's scale
+int s1_f16_image(molr_ctx* ctx, const molr_cache* cc, const int64_t* rows, int64_t n, Scratch& f32, Scratch& h,
+                 Scratch& nrm, Scratch& cmx, F16View* out, cudaStream_t s) {
+  using namespace s1bf;
+  molr_cache* c = const_cast<molr_cache*>(cc);
+  MOLR_TRY(s1_bf_build(c, s));  // (the view's scale)
+  const int64_t np = (n + NT - 1) / NT * NT;
+  MOLR_TRY(f32.alloc(size_t(np) * 256, s));
+  MOLR_TRY(h.alloc(size_t(np) * 128, s));
+  MOLR_TRY(nrm.alloc(size_t(np) * 4, s));
+  MOLR_TRY(cmx.alloc(size_t(np / 32) * 4, s));
+  gather_f32_rows_kernel<<<ctx->num_sms * 8, 256, 0, s>>>(n, np, c->s1_f32, rows, f32.as<float>());
+  MOLR_LAUNCHED(ctx);
+  build_kernel<<<ctx->num_sms * 8, 256, 0, s>>>(n, np, f32.as<float>(), 1.f / c->s1_hscale, h.as<__half>(),
+                                                nrm.as<float>());
+  MOLR_LAUNCHED(ctx);
+  chunk_max_kernel<<<div_up(np / 32, 256), 256, 0, s>>>(np / 32, nrm.as<float>(), cmx.as<float>());
+  MOLR_LAUNCHED(ctx);
+  *out = F16View{h.as<__half>(), nrm.as<float>(), cmx.as<float>(), c->s1_hscale, f32.as<float>(), n};
+  return MOLR_OK;
+}
+
+// keys[b, j] = f32_key(exact fp32 score of row rows_f32[ids[b, j]]) for the j < min(counts[b], cap)
+__global__ void passer_keys_kernel(int B, int64_t cap, const int32_t* __restrict__ ids, const int64_t* __restrict__ counts,
+                                   const float* __restrict__ vf, const float* __restrict__ qf, uint32_t* __restrict__ keys) {
+  __shared__ float sq[64];
+  const int b = blockIdx.x;
+  if (threadIdx.x < 64) sq[threadIdx.x] = qf[int64_t(b) * 64 + threadIdx.x];
+  __syncthreads();
+  const int64_t n = imin64(counts[b], cap);
+  for (int64_t i = blockIdx.y * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.y * blockDim.x) {
+    const float4* v = reinterpret_cast<const float4*>(vf + int64_t(ids[int64_t(b) * cap + i]) * 64);
+    float acc = 0.f;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const float4 x = __ldg(v + k);
+      acc = fmaf(x.x, sq[4 * k], acc);
+      acc = fmaf(x.y, sq[4 * k + 1], acc);
+      acc = fmaf(x.z, sq[4 * k + 2], acc);
+      acc = fmaf(x.w, sq[4 * k + 3], acc);
+    }
+    keys[int64_t(b) * cap + i] = f32_key(acc);
+  }
+}
+
+int s1_passer_keys(molr_ctx* ctx, int B, int64_t cap, const int32_t* ids, const int64_t* counts, const float* vf,
+                   const float* q, uint32_t* keys, cudaStream_t s) {
+  if (B <= 0) return MOLR_OK;
+  passer_keys_kernel<<<dim3(B, std::max(1, std::min(8, (2 * ctx->num_sms + B - 1) / B))), 256, 0, s>>>(
+      B, cap, ids, counts, vf, q, keys);
+  MOLR_LAUNCHED(ctx);
   return MOLR_OK;
 }
 
