@@ -40,6 +40,8 @@ CONFIGS = {
     # cores with an exact fp32 re-check (K2f)
     "10m_f32": dict(X=10_000_000, B=1024, k=100, k_prime=100_000, ratio=0.01, view="f32",
                     label="10M-item synthetic corpus, float stage-1 view"),
+    "100m_f32": dict(X=100_000_000, B=1024, k=100, k_prime=100_000, ratio=0.01, view="f32",
+                     label="100M-item synthetic corpus, float stage-1 view"),
     "books": dict(X=2_300_000, B=1024, k=100, k_prime=100_000, ratio=0.01, label="Amazon-Books-shaped 2.3M items"),
     # exact path (batch_score_all + mol_top_k over the whole corpus, mol.py:348-408): one step =
     # B users x all X items; the full ML-20M run is 138K users
