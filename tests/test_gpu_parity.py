@@ -676,6 +676,54 @@ def test_sharded_global_threshold_equals_single_device(quantized, comp, kp):
         np.testing.assert_array_equal(sc, ref[1])
 
 
+@pytest.mark.parametrize("X", [300, 4099])
+def test_stage1_tc_paths_edge_cases(X, monkeypatch):
+    """Tiny / ragged corpora through the small-batch int8 kernel, the 128-query int8 kernel and the
+    fp16 float-view kernel: duplicated rows (exact ties at the threshold), an all-zero stage-1 row,
+    an all-zero query and lambda = X (exact threshold); candidate counts and top-k must equal the
+    SIMT scans' (MOLR_DISABLE_TC / MOLR_S1_NO_BF) and the oracle's counts."""
+    from paper_2306_04039_b200.engine import two_stage_top_k
+    from paper_2306_04039_b200.hindexer import HIndexerConfig
+    from paper_2306_04039_b200.mol import ItemCache
+    from paper_2306_04039_b200.quant import quantize_rowwise
+
+    cache, syn, ue, feats = _synthetic_prod_cache(X, seed=61, n_users=40)
+    gating, og = _prod_gating(syn)
+    embs = cache.item_embs.copy()
+    gp = cache.item_gate_pre.copy()
+    embs[1::7] = embs[0]  # duplicated items -> tied stage-1 and MoL scores
+    gp[1::7] = gp[0]
+    embs[5] = 0.0  # an all-zero stage-1 row
+    s1 = embs.mean(axis=1).astype(np.float32)
+    cache = ItemCache(config=cache.config, item_embs=embs, item_gate_pre=gp, stage1_embs=s1,
+                      stage1_q=quantize_rowwise(s1))
+    ue = ue.copy()
+    ue[3] = 0.0  # an all-zero stage-1 query (every score 0: everything ties)
+    uw = gating.user_net(feats)
+    q = O.Quant(cache.stage1_q.codes, cache.stage1_q.scales)
+    kp = max(25, X // 20)
+    for nb in (5, 40):  # small-batch kernel / 128-query kernel (and the float kernel for both)
+        for quantized in (True, False):
+            for comp in ("inclusive", "strict"):
+                hcfg = HIndexerConfig(k_prime=kp, lam=X, quantized=quantized, comparator=comp)
+                env = "MOLR_DISABLE_TC" if quantized else "MOLR_S1_NO_BF"
+                monkeypatch.delenv(env, raising=False)
+                a = two_stage_top_k(cache, gating, ue[:nb], uw[:nb], 10, hcfg, seed=2)
+                monkeypatch.setenv(env, "1")
+                b = two_stage_top_k(cache, gating, ue[:nb], uw[:nb], 10, hcfg, seed=2)
+                monkeypatch.delenv(env)
+                np.testing.assert_array_equal(a[2], b[2])
+                np.testing.assert_array_equal(a[0], b[0])
+                if quantized:  # (MOLR_DISABLE_TC also swaps the MoL kernel: scores within tolerance)
+                    np.testing.assert_allclose(a[1], b[1], rtol=1e-3, atol=1e-6)
+                    for u in range(nb):
+                        c_ids, _, _ = O.h_indexer(q, ue[u].mean(axis=0), kp, O.make_rng(0), lam=X, comparator=comp)
+                        want = X if c_ids.size < 10 else c_ids.size  # (corpus fallback below k)
+                        assert a[2][u] == want, (nb, comp, u, a[2][u], c_ids.size)
+                else:
+                    np.testing.assert_array_equal(a[1], b[1])
+
+
 def test_batched_two_stage_recall_device_sample():
     """Device-drawn sample (lambda = 1% of X): candidate counts near K' and top-100 recall vs the
     oracle's exact MoL top-100 >= 0.99 (north-star bar), 100k items."""
