@@ -387,6 +387,30 @@ __global__ void __launch_bounds__(256) top_keys_kernel(int64_t m, const void* __
     o[i] = i < nk ? tb : 0u;
 }
 
+// the same from a list of ascending keys per query (row b: keys[b*cap, b*cap + min(counts[b], cap)))
+__global__ void __launch_bounds__(256) top_keys_list_kernel(int64_t cap, const uint32_t* __restrict__ keys,
+                                                           const int64_t* __restrict__ counts,
+                                                           const uint32_t* __restrict__ t, int64_t nk, int64_t n_keep,
+                                                           uint32_t* __restrict__ out) {
+  __shared__ unsigned long long n_gt;
+  const int b = blockIdx.x;
+  if (threadIdx.x == 0) n_gt = 0;
+  __syncthreads();
+  uint32_t* o = out + int64_t(b) * n_keep;
+  const uint32_t tb = t[b];
+  const int64_t m = counts[b] < cap ? counts[b] : cap;
+  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
+    const uint32_t key = keys[int64_t(b) * cap + i];
+    if (key > tb) {
+      const unsigned long long p = atomicAdd(&n_gt, 1ull);
+      if ((int64_t)p < nk) o[p] = key;
+    }
+  }
+  __syncthreads();
+  const int64_t filled = (int64_t)n_gt < nk ? (int64_t)n_gt : nk;
+  for (int64_t i = filled + threadIdx.x; i < n_keep; i += blockDim.x) o[i] = i < nk ? tb : 0u;
+}
+
 __global__ void fill_i64_kernel(int n, int64_t v, int64_t* __restrict__ out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[i] = v;
@@ -838,7 +862,6 @@ int molr_sample_top_keys(molr_ctx* ctx, const molr_cache* c, int B, int k_u, con
   Scratch ss, tk;
   MOLR_TRY(tk.alloc(size_t(B) * 4, s));
   if (m > 0) {
-    MOLR_TRY(ss.alloc(size_t(B) * m * 4, s));
     if (s1_tc_supported(c, mode)) {
       const int64_t lp = (m + 255) / 256 * 256;
       Scratch scodes, sscales;
@@ -850,9 +873,53 @@ int molr_sample_top_keys(molr_ctx* ctx, const molr_cache* c, int B, int k_u, con
       gather_sample_kernel<<<std::min(div_up(m * 4, 256), ctx->num_sms * 8), 256, 0, s>>>(
           c->s1_codes, c->s1_scales, c->s1_inv, loc.as<int64_t>(), m, scodes.as<int8_t>(), sscales.as<float>());
       MOLR_LAUNCHED(ctx);
+      // pilot (as sample_threshold_tc): a low threshold t0 from the first lam0 local sample rows, the
+      // fused filter keeps the keys >= t0, and the nk-th largest of those is the shard's nk-th
+      // largest whenever >= nk rows passed; otherwise the full score matrix below
+      const double p = double(nk) / double(m);
+      int64_t lam0 = ((int64_t)std::ceil(16.0 / p) + 255) / 256 * 256;
+      if (!getenv("MOLR_NO_PILOT") && lam0 * 4 <= m) {
+        const double mu = double(lam0) * p;
+        const int64_t n0 = std::min<int64_t>(lam0, (int64_t)std::ceil(mu + 6.0 * std::sqrt(mu) + 16.0));
+        const int64_t cap = (int64_t)(2.0 * double(m) * double(n0) / double(lam0)) + 2048;
+        const int64_t lp = (m + 255) / 256 * 256;
+        Scratch pilot, t0, keys, counts, flag, mm;
+        MOLR_TRY(pilot.alloc(size_t(B) * lam0 * 4, s));
+        MOLR_TRY(t0.alloc(size_t(B) * 4, s));
+        MOLR_TRY(keys.alloc(size_t(B) * cap * 4, s));
+        MOLR_TRY(counts.alloc(size_t(B) * 8, s));
+        MOLR_TRY(flag.alloc(sizeof(int) * 2, s));
+        MOLR_TRY(mm.alloc(size_t(lp / 32) * sizeof(float2), s));
+        MOLR_TRY(s1_tc_scan(ctx, mode, scodes.as<int8_t>(), sscales.as<float>(), nullptr, nullptr, lam0, B,
+                            qc.as<int8_t>(), nullptr, 0, 0, nullptr, nullptr, pilot.p, lam0, s));
+        MOLR_TRY(nth_largest_rows(ctx, B, lam0, pilot.p, mode == MOLR_S1_INT8_RAW, lam0, nullptr, 0, n0,
+                                  t0.as<uint32_t>(), s));
+        MOLR_TRY(chunk_minmax(ctx, sscales.as<float>(), 0, lp / 32, mm.as<float2>(), s));
+        MOLR_CUDA(cudaMemsetAsync(counts.p, 0, size_t(B) * 8, s));
+        MOLR_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int) * 2, s));
+        MOLR_TRY(s1_tc_scan(ctx, mode, scodes.as<int8_t>(), sscales.as<float>(), mm.as<float2>(), nullptr, m, B,
+                            qc.as<int8_t>(), t0.as<uint32_t>(), 0, cap, keys.as<int32_t>(), counts.as<int64_t>(), nullptr,
+                            0, s, /*emit_keys=*/true));
+        MOLR_TRY(nth_largest_keys(ctx, B, cap, keys.as<uint32_t>(), counts.as<int64_t>(), nk, tk.as<uint32_t>(),
+                                  flag.as<int>(), s));
+        max_count_kernel<<<div_up(B, 256), 256, 0, s>>>(B, counts.as<int64_t>(), cap, flag.as<int>());
+        MOLR_LAUNCHED(ctx);
+        int hf = 0;
+        MOLR_CUDA(cudaMemcpyAsync(&hf, flag.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+        MOLR_CUDA(cudaStreamSynchronize(s));
+        if (!hf) {
+          top_keys_list_kernel<<<B, 256, 0, s>>>(cap, keys.as<uint32_t>(), counts.as<int64_t>(), tk.as<uint32_t>(), nk,
+                                                 n_keep, ok.as<uint32_t>());
+          MOLR_LAUNCHED(ctx);
+          MOLR_CUDA(cudaStreamSynchronize(s));
+          return finish_outputs(s, {&ok});
+        }
+      }
+      MOLR_TRY(ss.alloc(size_t(B) * m * 4, s));
       MOLR_TRY(s1_tc_scan(ctx, mode, scodes.as<int8_t>(), sscales.as<float>(), nullptr, nullptr, m, B, qc.as<int8_t>(),
                           nullptr, 0, 0, nullptr, nullptr, ss.p, m, s));
     } else {
+      MOLR_TRY(ss.alloc(size_t(B) * m * 4, s));
       if (mode != MOLR_S1_FLOAT && c->s1_codes) MOLR_TRY(s1_seal(const_cast<molr_cache*>(c), s));
       MOLR_TRY(scan_scores(ctx, mode, m, c->d1, c->s1_f32, c->s1_codes, s1_interleaved(c->d1), c->s1_inv, c->s1_scales,
                            loc.as<int64_t>(), B, q.as<float>(), qc.as<int8_t>(), ss.p, m, s));
