@@ -307,7 +307,7 @@ int sample_threshold_f32(molr_ctx* ctx, const molr_cache* c, const int64_t* samp
       MOLR_CUDA(cudaMemsetAsync(counts.p, 0, size_t(B) * 8, s));
       MOLR_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int) * 2, s));
     }
-    if (s1_bf_supported(c, MOLR_S1_FLOAT) && B >= 2) {
+    if (s1_bf_supported(c, MOLR_S1_FLOAT)) {
       // the sampled rows' fp16 image through the tensor-core filter (>= t0, exact fp32 re-check),
       // then the exact fp32 keys of the passers
       Scratch f32r, himg, hn, hc, pids;
@@ -700,7 +700,7 @@ static int two_stage_impl(molr_ctx* ctx, const molr_cache* c, const molr_gating*
         }
         return MOLR_OK;
       };
-      if (s1_bf_supported(c, mode) && B >= 2) {  // (one query: the fp32 scan is already HBM-bound)
+      if (s1_bf_supported(c, mode)) {
         MOLR_TRY(s1_bf_scan(ctx, c, B, q.as<float>(), tkey.as<uint32_t>(), comparator == MOLR_STRICT, cap,
                             cand.as<int32_t>(), counts.as<int64_t>(), s));
       } else if (use_tc) {

@@ -1050,6 +1050,248 @@ __global__ void __launch_bounds__(NTHREADS, 1) bf_kernel(Params P) {
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
 }
 
+// Small batches (B <= 32) of the float view: items in M, queries in N (as s1tc::s1_small_kernel).
+// Per 256-row tile two M=128 x N=SBQ x K=64 fp16 MMA groups (4 x K=16 each) into one of 8 TMEM
+// buffers; every epilogue thread owns one item row and classifies its 16 query columns as
+// certain / band / fail with the row's own norm (no chunk pre-test needed: one row per thread).
+constexpr int SS_NSTAGE = 4;
+constexpr int SS_STAGE = SZ_TILE + NT * 4;  // fp16 tile + row norms (33 KB)
+constexpr int SS_OFF_Q = 0;                 // <= 32 x 128 B queries
+constexpr int SS_OFF_RING = 4096;
+constexpr int SS_OFF_T = SS_OFF_RING + SS_NSTAGE * SS_STAGE;
+constexpr int SS_OFF_E = SS_OFF_T + 128;
+constexpr int SS_OFF_S = SS_OFF_E + 128;
+constexpr int SS_OFF_SQ = SS_OFF_S + 128;
+constexpr int SS_OFF_CNT = SS_OFF_SQ + 128;
+constexpr int SS_OFF_BCNT = SS_OFF_CNT + 128;
+constexpr int SS_OFF_BAR = SS_OFF_BCNT + 128;
+constexpr int SS_OFF_TMEM = SS_OFF_BAR + (2 * SS_NSTAGE + 16) * 8;
+constexpr int SS_SMEM = SS_OFF_TMEM + 16;
+template <int SBQ>
+constexpr uint32_t idesc_h_s() {
+  return (1u << 4) | (uint32_t(SBQ >> 3) << 17) | (uint32_t(128 >> 4) << 24);
+}
+template <int SBQ>
+__device__ __forceinline__ void mma_h_s(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc_h_s<SBQ>()), "r"(accum)
+      : "memory");
+}
+#define TMEM_LD16H(taddr, r)                                                                                         \
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];" \
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),       \
+                 "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])   \
+               : "r"(taddr))
+#define TMEM_WAIT16H(r)                                                                                              \
+  asm volatile("tcgen05.wait::ld.sync.aligned;"                                                                      \
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),     \
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15])  \
+               :                                                                                                     \
+               : "memory")
+
+template <int SBQ>
+__global__ void __launch_bounds__(NTHREADS, 1) bf_small_kernel(Params P) {
+  constexpr bool SPLIT_T = SBQ == 16;        // warp halves take alternate tiles (else split the queries)
+  constexpr int QW = 16;
+  constexpr int NB = 8;
+  constexpr uint32_t TCOLS = NB * 2 * SBQ;
+  constexpr int NARRIVE = SPLIT_T ? NEPI * 64 : NEPI * 128;
+  extern __shared__ __align__(1024) uint8_t sm[];
+  const uint32_t sbase = smem_u32(sm);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t ntiles = (P.n + NT - 1) / NT;
+  const int64_t tile_lo = (int64_t(blockIdx.x) * ntiles) / gridDim.x;
+  const int64_t tile_hi = (int64_t(blockIdx.x + 1) * ntiles) / gridDim.x;
+  auto bar = [&](int i) { return sbase + SS_OFF_BAR + 8 * i; };
+  auto full_bar = [&](int s) { return bar(s); };
+  auto empty_bar = [&](int s) { return bar(SS_NSTAGE + s); };
+  auto tfull = [&](int e) { return bar(2 * SS_NSTAGE + e); };
+  auto tempty = [&](int e) { return bar(2 * SS_NSTAGE + 8 + e); };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + SS_OFF_TMEM);
+  uint32_t* scnt = reinterpret_cast<uint32_t*>(sm + SS_OFF_CNT);
+  uint32_t* sbcnt = reinterpret_cast<uint32_t*>(sm + SS_OFF_BCNT);
+  float* st_t = reinterpret_cast<float*>(sm + SS_OFF_T);
+  float* st_e = reinterpret_cast<float*>(sm + SS_OFF_E);
+  float* st_s = reinterpret_cast<float*>(sm + SS_OFF_S);
+  float* st_sq = reinterpret_cast<float*>(sm + SS_OFF_SQ);
+
+  if (threadIdx.x < SBQ) {  // per query (as bf_kernel): scale, threshold, margin factor, constant slack
+    const int q = threadIdx.x;
+    float t = 0.f, e = 0.f, c = 0.f, sq = 1.f;
+    if (q < P.B) {
+      float ss = 0.f, mx = 0.f;
+      for (int k = 0; k < 64; ++k) {
+        const float x = __ldg(P.q + int64_t(q) * 64 + k);
+        ss = fmaf(x, x, ss);
+        mx = fmaxf(mx, fabsf(x));
+      }
+      sq = h_scale(mx);
+      const float inv = 1.f / (P.sv * sq);
+      const float nq = up_norm(ss);
+      t = key_f32(__ldg(P.tkeys + q)) * inv;
+      e = (EPS * nq + 4.8e-7f * sq) * inv;
+      c = 4.8e-7f * P.sv * nq * inv;
+    }
+    st_t[q] = t;
+    st_e[q] = e;
+    st_s[q] = c + fabsf(t) * 1e-6f + 1e-30f;
+    st_sq[q] = sq;
+    scnt[q] = 0;
+    sbcnt[q] = 0;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < SBQ * 8; i += blockDim.x) {
+    const int q = i >> 3, c = i & 7;
+    const float inv_sq = 1.f / st_sq[q];
+    __align__(16) __half h[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) h[j] = __float2half_rn(q < P.B ? __ldg(P.q + int64_t(q) * 64 + c * 8 + j) * inv_sq : 0.f);
+    *reinterpret_cast<int4*>(sm + SS_OFF_Q + (q >> 3) * 1024 + c * 128 + (q & 7) * 16) = *reinterpret_cast<const int4*>(h);
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < SS_NSTAGE; ++s) {
+      mbar_init(full_bar(s), 1);
+      mbar_init(empty_bar(s), 1 + NARRIVE);
+    }
+    for (int e = 0; e < NB; ++e) {
+      mbar_init(tfull(e), 1);
+      mbar_init(tempty(e), NARRIVE);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)), "r"(TCOLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t tile = tile_lo; tile < tile_hi; ++tile) {
+        mbar_wait(empty_bar(stage), phase ^ 1);
+        const uint32_t st = sbase + SS_OFF_RING + stage * SS_STAGE;
+        mbar_arrive_expect_tx(full_bar(stage), SZ_TILE + NT * 4);
+        bulk_g2s(st, P.view + tile * (NT * 64), SZ_TILE, full_bar(stage));
+        bulk_g2s(st + SZ_TILE, P.nrm + tile * NT, NT * 4, full_bar(stage));
+        if (++stage == SS_NSTAGE) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      uint32_t jc = 0;
+      const uint32_t at = sbase + SS_OFF_Q;
+      for (int64_t tile = tile_lo; tile < tile_hi; ++tile, ++jc) {
+        mbar_wait(full_bar(stage), phase);
+        const int buf = int(jc % NB);
+        mbar_wait(tempty(buf), ((jc / NB) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t bt = sbase + SS_OFF_RING + stage * SS_STAGE;
+#pragma unroll
+        for (int mb = 0; mb < 2; ++mb)  // item rows [128 mb, +128) -> columns [SBQ mb, +SBQ)
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            mma_h_s<SBQ>(tmem_base + buf * 2 * SBQ + mb * SBQ, desc_bf(bt + mb * 16384 + k * 256), desc_bf(at + k * 256),
+                         k > 0);
+        mma_commit(tfull(buf));
+        mma_commit(empty_bar(stage));
+        if (++stage == SS_NSTAGE) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    const int w = (warp - 2) >> 2;
+    const int quarter = warp & 3;
+    const int mb = w & 1, qh = w >> 1;
+    const int r = mb * 128 + quarter * 32 + lane;
+    const int qo = SPLIT_T ? 0 : QW * qh;
+    const int nq = min(QW, P.B - qo);
+    float tv[QW], ev[QW], sv[QW];
+#pragma unroll
+    for (int j = 0; j < QW; ++j) tv[j] = st_t[qo + j], ev[j] = st_e[qo + j], sv[j] = st_s[qo + j];
+    int stage = 0;
+    uint32_t phase = 0;
+    int64_t jc = 0;
+    int32_t* cand_cta = P.cand + int64_t(blockIdx.x) * P.seg;
+    int32_t* band_cta = P.band + int64_t(blockIdx.x) * P.seg;
+    for (int64_t tile = tile_lo; tile < tile_hi; ++tile, ++jc) {
+      const int buf = int(jc % NB);
+      if (SPLIT_T && int(jc & 1) != qh) {
+        if (++stage == SS_NSTAGE) {
+          stage = 0;
+          phase ^= 1;
+        }
+        continue;
+      }
+      mbar_wait(full_bar(stage), phase);
+      mbar_wait(tfull(buf), uint32_t((jc / NB) & 1));
+      tc_fence_after();
+      if (nq > 0) {
+        const float nv = reinterpret_cast<const float*>(sm + SS_OFF_RING + stage * SS_STAGE + SZ_TILE)[r];
+        const bool valid = tile * NT + r < P.n;
+        uint32_t a[16];
+        TMEM_LD16H(tmem_base + buf * 2 * SBQ + mb * SBQ + qo + ((uint32_t)(quarter * 32) << 16), a);
+        TMEM_WAIT16H(a);
+        uint32_t mc = 0, mbd = 0;
+#pragma unroll
+        for (int j = 0; j < QW; ++j) {
+          const float d = __uint_as_float(a[j]);
+          const float m = fmaf(ev[j], nv, sv[j]);
+          const bool c = d >= tv[j] + m;
+          const bool b = !c && d >= tv[j] - m;
+          mc |= uint32_t(c && j < nq) << j;
+          mbd |= uint32_t(b && j < nq) << j;
+        }
+        if (!valid) mc = mbd = 0;
+        if (__any_sync(0xffffffffu, (mc | mbd) != 0)) {
+          const int32_t id = int32_t(tile * NT + r);
+          for (uint32_t m2 = mc; m2; m2 &= m2 - 1) {
+            const int q = qo + __ffs(m2) - 1;
+            const uint32_t pos = atomicAdd(scnt + q, 1u);
+            if ((int64_t)pos < P.seg) cand_cta[int64_t(q) * P.cap + pos] = id;
+          }
+          for (uint32_t m2 = mbd; m2; m2 &= m2 - 1) {
+            const int q = qo + __ffs(m2) - 1;
+            const uint32_t pos = atomicAdd(sbcnt + q, 1u);
+            if ((int64_t)pos < P.seg) band_cta[int64_t(q) * P.cap + pos] = id;
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(tempty(buf));
+      mbar_arrive(empty_bar(stage));
+      if (++stage == SS_NSTAGE) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  for (int q = threadIdx.x; q < P.B; q += blockDim.x) {
+    P.cta_counts[int64_t(q) * gridDim.x + blockIdx.x] = int32_t(scnt[q]);
+    P.cta_bcounts[int64_t(q) * gridDim.x + blockIdx.x] = int32_t(sbcnt[q]);
+  }
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TCOLS));
+}
+
 __global__ void seg_max_kernel(int64_t n, const int32_t* __restrict__ cnt, int* __restrict__ mx) {
   int m = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -1273,7 +1515,13 @@ int s1_f16_filter(molr_ctx* ctx, const F16View& V, int B, const float* q, const 
       P.cta_bcounts = bcount.as<int32_t>();
       {
         KTimer t(ctx, timer, s, double(Bc) * n);
-        bf_kernel<<<grid, NTHREADS, SMEM_BYTES, s>>>(P);
+        if (Bc <= 32 && !getenv("MOLR_S1_NO_SMALL")) {  // items-in-M variant for small batches
+          auto kern = Bc <= 16 ? bf_small_kernel<16> : bf_small_kernel<32>;
+          MOLR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SS_SMEM));
+          kern<<<grid, NTHREADS, SS_SMEM, s>>>(P);
+        } else {
+          bf_kernel<<<grid, NTHREADS, SMEM_BYTES, s>>>(P);
+        }
         MOLR_LAUNCHED(ctx);
         s1tc::compact_segments_kernel<<<Bc, 256, 0, s>>>(grid, seg, P.cap, P.cand, P.cta_counts, cap,
                                                          cand + int64_t(b0) * cap, counts + b0, mx.as<int>());

@@ -576,7 +576,7 @@ def test_batched_stage1_small_batch_kernel(nb, monkeypatch):
             np.testing.assert_array_equal(x, y)
 
 
-@pytest.mark.parametrize("nb", [3, 300])
+@pytest.mark.parametrize("nb", [1, 3, 17, 300])
 def test_batched_float_view_tc_matches_fp32_scan(nb, monkeypatch):
     """Float stage-1 view (quantized=False, the reference default) on the tensor cores: bf16 MMA
     pre-test + exact fp32 re-check of the undecided band must give the SAME candidate sets as the
