@@ -691,11 +691,13 @@ __global__ void __launch_bounds__(256) compact_segments_kernel(int G, int64_t se
       mx = max(mx, c);
     }
     pre[G] = acc;
-    counts[b] = acc;
-    if (mx > 0) atomicMax(max_cta, mx);
+    if (blockIdx.y == 0) {
+      counts[b] = acc;
+      if (mx > 0) atomicMax(max_cta, mx);
+    }
   }
   __syncthreads();
-  for (int g = 0; g < G; ++g) {
+  for (int g = blockIdx.y; g < G; g += gridDim.y) {  // (query, group of segments) per block
     const int64_t n = imin64(pre[g + 1] - pre[g], seg);
     const int32_t* s = src + int64_t(b) * cap_in + int64_t(g) * seg;
     int32_t* d = dst + int64_t(b) * cap_out + pre[g];
@@ -704,6 +706,10 @@ __global__ void __launch_bounds__(256) compact_segments_kernel(int G, int64_t se
   }
 }
 
+// blocks per query for compact_segments_kernel: enough to cover the SMs for small batches
+inline unsigned compact_split(const molr_ctx* ctx, int Bc, int G) {
+  return (unsigned)std::max(1, std::min(G, (2 * ctx->num_sms + Bc - 1) / Bc));
+}
 }  // namespace s1tc
 
 // ---------------------------------------------------------------------------------------------
@@ -1425,8 +1431,8 @@ int s1_tc_scan(molr_ctx* ctx, int mode, const int8_t* codes, const float* scales
         }
       }
       if (!filter) break;
-      compact_segments_kernel<<<Bc, 256, 0, s>>>(grid, seg, P.cap, P.cand, P.cta_counts, cap, cand + int64_t(b0) * cap,
-                                                 counts + b0, mx.as<int>());
+      compact_segments_kernel<<<dim3(Bc, compact_split(ctx, Bc, grid)), 256, 0, s>>>(
+          grid, seg, P.cap, P.cand, P.cta_counts, cap, cand + int64_t(b0) * cap, counts + b0, mx.as<int>());
       MOLR_LAUNCHED(ctx);
       int hmx = 0;
       MOLR_CUDA(cudaMemcpyAsync(&hmx, mx.p, 4, cudaMemcpyDeviceToHost, s));
@@ -1523,8 +1529,8 @@ int s1_f16_filter(molr_ctx* ctx, const F16View& V, int B, const float* q, const 
           bf_kernel<<<grid, NTHREADS, SMEM_BYTES, s>>>(P);
         }
         MOLR_LAUNCHED(ctx);
-        s1tc::compact_segments_kernel<<<Bc, 256, 0, s>>>(grid, seg, P.cap, P.cand, P.cta_counts, cap,
-                                                         cand + int64_t(b0) * cap, counts + b0, mx.as<int>());
+        s1tc::compact_segments_kernel<<<dim3(Bc, s1tc::compact_split(ctx, Bc, grid)), 256, 0, s>>>(
+            grid, seg, P.cap, P.cand, P.cta_counts, cap, cand + int64_t(b0) * cap, counts + b0, mx.as<int>());
         MOLR_LAUNCHED(ctx);
         seg_max_kernel<<<div_up(int64_t(Bc) * grid, 256), 256, 0, s>>>(int64_t(Bc) * grid, P.cta_bcounts,
                                                                         mx.as<int>());
