@@ -995,24 +995,22 @@ __global__ void __launch_bounds__(NTHREADS, 1) bf_kernel(Params P) {
               h |= uint32_t(gm >= lo) << g8;
             }
             h = __reduce_or_sync(0xffffffffu, h);
-            uint32_t mc = 0, mb = 0;
+            // in a hit group: certain above the chunk's upper bound, band between the two bounds
+            // (the chunk's max row norm for both: two compares per element)
+            const float hi = t + (e * cmx[cc] + slack);
+            uint32_t mc = 0, ml = 0;
 #pragma unroll
             for (int g8 = 0; g8 < 4; ++g8) {
               if (h & (1u << g8)) {
                 const float* u = v + g8 * 8;
-                const float4 n0 = reinterpret_cast<const float4*>(nrm + cc * 32 + g8 * 8)[0];
-                const float4 n1 = reinterpret_cast<const float4*>(nrm + cc * 32 + g8 * 8)[1];
-                const float nv[8] = {n0.x, n0.y, n0.z, n0.w, n1.x, n1.y, n1.z, n1.w};
 #pragma unroll
                 for (int jj = 0; jj < 8; ++jj) {
-                  const float m = e * nv[jj] + slack;
-                  const bool c = u[jj] >= t + m;
-                  const bool b = !c && u[jj] >= t - m;
-                  mc |= uint32_t(c) << (g8 * 8 + jj);
-                  mb |= uint32_t(b) << (g8 * 8 + jj);
+                  mc |= uint32_t(u[jj] >= hi) << (g8 * 8 + jj);
+                  ml |= uint32_t(u[jj] >= lo) << (g8 * 8 + jj);
                 }
               }
             }
+            const uint32_t mb = ml & ~mc;
             const int lim = nvalid - cc * 32;
             const uint32_t vm = lim >= 32 ? 0xffffffffu : (lim <= 0 ? 0u : ((1u << lim) - 1u));
             cert[cc] = mc & vm;
