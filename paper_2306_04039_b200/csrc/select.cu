@@ -129,6 +129,11 @@ segmented_topk_kernel(int B, const int64_t* __restrict__ begin, const int64_t* _
   const float* sc = begin ? scores + seg0 : scores + int64_t(b) * dense_ld;
   const Id* id = ids ? ids + seg0 : nullptr;
   const int kk = (int)imin64(k, n);
+  // a segment shorter than k: the tail is "no entry" (id -1, score -inf; merge_topk drops it)
+  for (int i = max(kk, 0) + threadIdx.x; i < k; i += blockDim.x) {
+    out_ids[int64_t(b) * k + i] = -1;
+    out_scores[int64_t(b) * k + i] = -INFINITY;
+  }
   if (kk <= 0) return;
   auto idof = [&](int64_t i) -> uint32_t { return id ? (uint32_t)id[i] : (uint32_t)i; };
   // ---- fast path: sampled bound + one filtering pass ----------------------------------------

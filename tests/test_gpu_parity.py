@@ -724,6 +724,38 @@ def test_stage1_tc_paths_edge_cases(X, monkeypatch):
                     np.testing.assert_array_equal(a[1], b[1])
 
 
+def test_two_stage_at_short_lists_are_padded():
+    """molr_two_stage_top_k_at keeps short candidate lists (no corpus fallback): the tail of a list
+    shorter than k must be "no entry" (id -1, score -inf), never uninitialised memory (the merge
+    drops such entries; a garbage tail once won the merge of a sharded query)."""
+    from paper_2306_04039_b200 import _lib as L
+    from paper_2306_04039_b200.mol import _gating_handle
+
+    cache, syn, ue, feats = _synthetic_prod_cache(30_000, seed=71, n_users=24)
+    gating, og = _prod_gating(syn)
+    uw = L.f32(gating.user_net(feats))
+    ue = L.f32(ue)
+    B, k = ue.shape[0], 50
+    # thresholds at each query's 10th-largest int8 score -> ~10 passers < k
+    q = O.Quant(cache.stage1_q.codes, cache.stage1_q.scales)
+    tk = np.empty(B, dtype=np.uint32)
+    for u in range(B):
+        sc = O.stage1_scores(q, ue[u].mean(axis=0))
+        tk[u] = np.float32(np.sort(sc)[-10]).view(np.uint32) | np.uint32(0x80000000) if np.sort(sc)[-10] >= 0 \
+            else ~np.float32(np.sort(sc)[-10]).view(np.uint32)
+    for rep in range(3):
+        ids = np.full((B, k), 12345, dtype=np.int64)
+        scs = np.full((B, k), 7.0, dtype=np.float32)
+        cnt = np.empty(B, dtype=np.int64)
+        L.call("molr_two_stage_top_k_at", L.ctx(), cache.device_handle(), _gating_handle(gating), B, 8, L.ptr(ue),
+               L.ptr(uw), 20.0, L.S1_INT8, 1000, L.ptr(tk), L.INCLUSIVE, k, 0, L.ptr(ids), L.ptr(scs), L.ptr(cnt), None)
+        for u in range(B):
+            c = int(cnt[u])
+            assert 10 <= c < k, c
+            assert np.all(ids[u, :c] >= 0) and np.all(np.isfinite(scs[u, :c]))
+            assert np.all(ids[u, c:] == -1) and np.all(scs[u, c:] == -np.inf), (u, c, ids[u, c:c + 3])
+
+
 def test_batched_two_stage_recall_device_sample():
     """Device-drawn sample (lambda = 1% of X): candidate counts near K' and top-100 recall vs the
     oracle's exact MoL top-100 >= 0.99 (north-star bar), 100k items."""
