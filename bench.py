@@ -486,6 +486,11 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    # the exact path's item side (27K x 1.15 KB) fits the 126 MB L2: flush it between timed steps
+    # by writing a buffer larger than L2 (outside the per-step events); the other configs' inputs
+    # are larger than L2
+    l2_flush = torch.empty(64 << 20, dtype=torch.float32, device=dev) if exact else None
+
     # ---------------- device-resident timing (value) ----------------
     prof_range = os.environ.get("MOLR_PROFILE_RANGE") == "1"  # ncu --profile-from-start off
     with Clocks(local) as clk:  # sampling starts before the warm-up (nvidia-smi start-up stalls the GPU)
@@ -496,6 +501,7 @@ def main():
         L.set_profiling(True, local)
         launches0 = L.launch_count(local)
         evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+        starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
         if prof_range:
             torch.cuda.profiler.start()
         barrier()
@@ -504,6 +510,9 @@ def main():
         last = {}
         host_ms = []
         for i in range(args.steps):
+            if l2_flush is not None:  # (untimed) evict the L2-resident item side between steps
+                l2_flush.zero_()
+            starts[i].record(stream)
             t_host = time.perf_counter()
             step(args.warmup + i, feats_d.data_ptr())
             evs[i + 1].record(stream)
@@ -521,8 +530,8 @@ def main():
     L.set_profiling(False, local)
     launches = L.launch_count(local) - launches0
     prof = L.prof_read(local)
-    step_ms = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
-    total_ms = evs[0].elapsed_time(evs[-1])
+    step_ms = [starts[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
+    total_ms = sum(step_ms) if l2_flush is not None else evs[0].elapsed_time(evs[-1])
     if world > 1:
         tt = torch.tensor([total_ms], device=dev)
         all_reduce_max(tt)
@@ -541,13 +550,17 @@ def main():
         step(i, feats_pin.data_ptr(), (host_ids, host_sc))
     barrier()
     eev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    est = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     eev[0].record(stream)
     for i in range(args.steps):
+        if l2_flush is not None:
+            l2_flush.zero_()
+        est[i].record(stream)
         step(args.warmup + i, feats_pin.data_ptr(), (host_ids, host_sc))
         eev[i + 1].record(stream)
     barrier()
-    e2e_ms = eev[0].elapsed_time(eev[-1])
-    e2e_step_ms = [eev[i].elapsed_time(eev[i + 1]) for i in range(args.steps)]
+    e2e_step_ms = [est[i].elapsed_time(eev[i + 1]) for i in range(args.steps)]
+    e2e_ms = sum(e2e_step_ms) if l2_flush is not None else eev[0].elapsed_time(eev[-1])
     if world > 1:
         tt = torch.tensor([e2e_ms], device=dev)
         all_reduce_max(tt)
@@ -676,7 +689,8 @@ def main():
                    "parallelism": f"item-shard x{world}",
                    "threshold": None if exact else ("single-device (global sample, top-n key all-gather)"
                                                     if (global_thr or world == 1) else "per-shard (K'/N, lambda/N)"),
-                   "l2": ("item side L2-resident by design (exact path); user inputs fresh per step" if exact else
+                   "l2": ("L2 flushed between timed steps (256 MB write outside the step events); the item side "
+                          "fits L2 within a step" if exact else
                           "inputs larger than L2 (corpus shard x 1.2 KB per item >> 126 MB)")},
         "p50_batch_latency_ms": float(np.median(step_ms)), "step_ms": [round(x, 3) for x in step_ms], "step_host_ms": host_ms, "p50_single_query_latency_ms": float(np.median(lat)),
         "recall_at_k_vs_exact_mol": recall, "result_digest_step0": digest, "recall_queries": R,
