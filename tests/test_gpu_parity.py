@@ -756,6 +756,42 @@ def test_two_stage_at_short_lists_are_padded():
             assert np.all(ids[u, c:] == -1) and np.all(scs[u, c:] == -np.inf), (u, c, ids[u, c:c + 3])
 
 
+def test_sharded_entry_points_validate():
+    """The sharded entry points fail loudly on bad arguments (reference error classes): a shard
+    outside the corpus, lambda outside [1, X], n outside [1, m], a null threshold array; and
+    two_stage_top_k_sharded raises OutOfRangeError for K' > X like h_indexer (hindexer.py:60-61)."""
+    from paper_2306_04039_b200 import _lib as L
+    from paper_2306_04039_b200.engine import _mode, two_stage_top_k_sharded
+    from paper_2306_04039_b200.errors import OutOfRangeError
+    from paper_2306_04039_b200.hindexer import HIndexerConfig
+    from paper_2306_04039_b200.mol import _gating_handle
+
+    cache, syn, ue, feats = _synthetic_prod_cache(2_000, seed=81, n_users=4)
+    gating, og = _prod_gating(syn)
+    ue = L.f32(ue)
+    keys = np.empty((4, 8), dtype=np.uint32)
+    h = HIndexerConfig(k_prime=100, sample_ratio=0.1, quantized=True)
+    with pytest.raises(OutOfRangeError):  # shard [1500, 3500) outside a 3000-row corpus
+        L.call("molr_sample_top_keys", L.ctx(), cache.device_handle(), 4, 8, L.ptr(ue), _mode(h), 3000, 1500, 100, 1, 8,
+               L.ptr(keys), None)
+    with pytest.raises(OutOfRangeError):  # lambda > X
+        L.call("molr_sample_top_keys", L.ctx(), cache.device_handle(), 4, 8, L.ptr(ue), _mode(h), 2000, 0, 5000, 1, 8,
+               L.ptr(keys), None)
+    out = np.empty(4, dtype=np.uint32)
+    with pytest.raises(OutOfRangeError):  # n > m
+        L.call("molr_select_nth_keys", L.ctx(), 4, 8, L.ptr(keys), 9, L.ptr(out), None)
+    ids = np.empty((4, 5), dtype=np.int64)
+    sc = np.empty((4, 5), dtype=np.float32)
+    with pytest.raises(Exception):  # null thresholds
+        L.call("molr_two_stage_top_k_at", L.ctx(), cache.device_handle(), _gating_handle(gating), 4, 8, L.ptr(ue),
+               L.ptr(L.f32(gating.user_net(feats))), 20.0, _mode(h), 100, None, L.INCLUSIVE, 5, 0, L.ptr(ids), L.ptr(sc),
+               None, None)
+    with pytest.raises(OutOfRangeError):
+        two_stage_top_k_sharded(cache, gating, ue, gating.user_net(feats), 5,
+                                HIndexerConfig(k_prime=5000, sample_ratio=0.1, quantized=True), X_global=2000, row_lo=0,
+                                exchange=lambda a: np.asarray(a)[None])
+
+
 def test_batched_two_stage_recall_device_sample():
     """Device-drawn sample (lambda = 1% of X): candidate counts near K' and top-100 recall vs the
     oracle's exact MoL top-100 >= 0.99 (north-star bar), 100k items."""
