@@ -1352,7 +1352,8 @@ __global__ void gather_f32_rows_kernel(int64_t n, int64_t np, const float* __res
 }  // namespace s1bf
 
 bool s1_tc_supported(const molr_cache* c, int mode) {
-  return c && mode != MOLR_S1_FLOAT && c->d1 == 64 && c->s1_codes && c->s1_chunk_mm && !getenv("MOLR_DISABLE_TC");
+  return c && mode != MOLR_S1_FLOAT && c->d1 == 64 && c->s1_codes && c->s1_chunk_mm && !getenv("MOLR_DISABLE_TC") &&
+         !getenv("MOLR_S1_NO_TC");
 }
 
 // Scan rows [0, n) of an interleaved code matrix against B queries (chunks of 1024 per launch).

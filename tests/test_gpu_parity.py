@@ -792,6 +792,26 @@ def test_sharded_entry_points_validate():
                                 exchange=lambda a: np.asarray(a)[None])
 
 
+def test_batched_two_stage_more_than_1024_queries(monkeypatch):
+    """B = 1100 > 1024 (two query chunks per scan, the second a small-batch chunk) through the int8
+    and the float tensor-core filters: counts and top-k identical to the SIMT scans."""
+    from paper_2306_04039_b200.engine import two_stage_top_k
+    from paper_2306_04039_b200.hindexer import HIndexerConfig
+
+    cache, syn, ue, feats = _synthetic_prod_cache(20_000, seed=91, n_users=1100)
+    gating, og = _prod_gating(syn)
+    uw = gating.user_net(feats)
+    for quantized, env in ((True, "MOLR_S1_NO_TC"), (False, "MOLR_S1_NO_BF")):  # (filter-only switches)
+        hcfg = HIndexerConfig(k_prime=400, sample_ratio=0.1, quantized=quantized)
+        monkeypatch.delenv(env, raising=False)
+        a = two_stage_top_k(cache, gating, ue, uw, 10, hcfg, seed=4)
+        monkeypatch.setenv(env, "1")
+        b = two_stage_top_k(cache, gating, ue, uw, 10, hcfg, seed=4)
+        monkeypatch.delenv(env)
+        np.testing.assert_array_equal(a[2], b[2])
+        np.testing.assert_array_equal(a[0], b[0])
+
+
 def test_batched_two_stage_recall_device_sample():
     """Device-drawn sample (lambda = 1% of X): candidate counts near K' and top-100 recall vs the
     oracle's exact MoL top-100 >= 0.99 (north-star bar), 100k items."""
