@@ -15,10 +15,10 @@ from tests.test_gpu_parity import _prod_gating, _synthetic_prod_cache  # noqa: E
 # SAN_NEW_ONLY=1: only the round-1 additions (small-batch, float view, sharded) on a smaller corpus
 # (racecheck is slow on the shared-memory-heavy kernels)
 NEW_ONLY = os.environ.get("SAN_NEW_ONLY") == "1"
-cache, syn, ue, feats = _synthetic_prod_cache(8_000 if NEW_ONLY else 40_000, seed=3, n_users=40)
+cache, syn, ue, feats = _synthetic_prod_cache(int(os.environ.get("SAN_X", 8_000)) if NEW_ONLY else 40_000, seed=3, n_users=40)
 gating, _ = _prod_gating(syn)
 uw = gating.user_net(feats)
-KP = 400 if NEW_ONLY else 2000
+KP = max(30, cache.num_items // 20) if NEW_ONLY else 2000
 ids, sc, cand = two_stage_top_k(cache, gating, ue, uw, 20, HIndexerConfig(k_prime=KP, sample_ratio=0.2, quantized=True),
                                 seed=1)
 c2 = np.zeros(1, dtype=np.int64)
