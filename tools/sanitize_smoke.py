@@ -42,7 +42,7 @@ from paper_2306_04039_b200.quant import QuantizedRows  # noqa: E402
 from tests.test_gpu_parity import _run_shards  # noqa: E402
 
 X = cache.num_items
-cuts = [0, X // 2 - 777, X]
+cuts = [0, X // 2 - X // 10, X]
 q = cache.stage1_q
 shards = [ItemCache(config=cache.config, item_embs=cache.item_embs[lo:hi], item_gate_pre=cache.item_gate_pre[lo:hi],
                     stage1_embs=cache.stage1_embs[lo:hi], stage1_q=QuantizedRows(q.codes[lo:hi], q.scales[lo:hi]))
