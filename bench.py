@@ -47,7 +47,13 @@ CONFIGS = {
     # B users x all X items; the full ML-20M run is 138K users
     "ml20m": dict(X=27_000, B=1024, k=100, k_prime=None, ratio=None, exact=True, users=138_000,
                   label="ML-20M-shaped synthetic: 27K items, exact MoL top-100"),
+    # BASELINE configs[0]: one step = every user of the ML-1M shape against the whole corpus
+    "ml1m": dict(X=3_706, B=6_040, k=200, k_prime=None, ratio=None, exact=True, users=6_040,
+                 label="ML-1M-shaped synthetic: 6,040 users x 3,706 items, exact MoL top-200"),
 }
+# queries checked against the CPU oracle (oracle/molr_oracle.c) after the timed region: exhaustive
+# oracle top-k for ORACLE_Q[config] queries (all users for ML-1M), oracle scores of the returned items
+ORACLE_Q = {"100m": 2, "100m_f32": 2, "10m": 8, "10m_f32": 8, "books": 16, "ml20m": 64, "ml1m": 6_040}
 K_U = K_X = 8
 D = 64
 G = 64
@@ -285,6 +291,45 @@ def cpu_baseline(cfg, reps=2, procs=None, X1=1_000_000):
 
 
 # ------------------------------------------------------------------------------------------
+# parity against the CPU oracle at the bench's own config (outside the timed region)
+# ------------------------------------------------------------------------------------------
+def oracle_parity(cfg, model, cache, ue, feats, ids, scores, q_exact, q_scores=8):
+    """Compare the step's top-k (ids/scores, host (B,k)) with the C restatement of the reference's
+    scorer (oracle/molr_oracle.c, pinned to reference goldens): the oracle's exhaustive top-k
+    (RetrievalEngine.full_top_k, engine.py:140-147) of the first q_exact queries, streamed from the
+    device cache in chunks (read back exactly), and the oracle's scores of the returned items of
+    the first q_scores queries (score_candidates, mol.py:329-345)."""
+    import oracle as O
+    from oracle import c_oracle as CO
+
+    t0 = time.perf_counter()
+    k = ids.shape[1]
+    X = cache.num_items
+    uw = O.mlp(O.MlpW(*model["user_net"]), feats).astype(np.float32)
+    cross = CO.Net(*model["cross_net"])
+    q = min(q_exact, ids.shape[0])
+    chunk = max(1, min(1 << 20, (1 << 28) // max(q, 1)))
+    ex_i, ex_s = CO.exact_top_k_streamed(cache.read, X, ue[:q], uw[:q], cross, TAU, k, chunk=chunk)
+    recall = float(np.mean([len(set(ids[b].tolist()) & set(ex_i[b].tolist())) / k for b in range(q)]))
+    identical = int(sum(ids[b].tolist() == ex_i[b].tolist() for b in range(q)))
+    # oracle scores of the returned items
+    qs = min(max(q_scores, q if cfg.get("exact") else 0), ids.shape[0], 64)
+    uniq = np.unique(ids[:qs])
+    rows = {int(i): cache.read(int(i), 1) for i in uniq}
+    e = np.concatenate([rows[int(i)][0] for i in uniq])
+    g = np.concatenate([rows[int(i)][1] for i in uniq])
+    pos = {int(i): j for j, i in enumerate(uniq)}
+    lists = [np.array([pos[int(i)] for i in ids[b]]) for b in range(qs)]
+    ref = CO.score_candidates(e, g, ue[:qs], uw[:qs], cross, TAU, lists)
+    err = max(float(np.abs(scores[b] - ref[b]).max()) for b in range(qs))
+    viol = int(sum((~O.score_close(scores[b], ref[b])).sum() for b in range(qs)))
+    return {"recall_vs_oracle": recall, "oracle_queries": q, "lists_identical_to_oracle": identical,
+            "max_abs_score_err": err, "score_tolerance": "1e-3*|s| + 1e-6", "score_violations": viol,
+            "score_queries": qs, "oracle": "oracle/molr_oracle.c (C restatement of mol.py:139-205, 329-408)",
+            "oracle_threads": CO.num_threads(), "seconds": round(time.perf_counter() - t0, 1)}
+
+
+# ------------------------------------------------------------------------------------------
 def metric_name(name, cfg):
     if name == "100m":
         return "MoL+h-indexer top-100 queries/sec over 100M items"  # BASELINE.json's headline metric
@@ -319,6 +364,7 @@ def main():
     ap.add_argument("--items", type=int, default=0, help="override corpus size (debug)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-oracle", action="store_true", help="skip the CPU-oracle parity check")
     ap.add_argument("--recall-queries", type=int, default=8)
     ap.add_argument("--global-threshold", action="store_true",
                     help="N>1: the single-device threshold (exchange of each query's top sample keys) instead "
@@ -616,6 +662,15 @@ def main():
     ex_np = ex_i.cpu().numpy()
     recall = float(np.mean([len(set(two[r]) & set(ex_np[r])) / k for r in range(R)]))
 
+    # ---------------- parity against the CPU oracle (1 GPU: the whole corpus is local) ----------------
+    parity = None
+    if world == 1 and not args.no_oracle and rank == 0:
+        try:
+            parity = oracle_parity(cfg, model, cache, ue_d.cpu().numpy(), feats_h, res_i.cpu().numpy(),
+                                   res_s.cpu().numpy(), ORACLE_Q.get(args.config, 2))
+        except Exception as e:  # keep the GPU line
+            parity = {"error": repr(e)}
+
     if rank != 0:
         if world > 1:
             dist.barrier()
@@ -694,6 +749,7 @@ def main():
                           "inputs larger than L2 (corpus shard x 1.2 KB per item >> 126 MB)")},
         "p50_batch_latency_ms": float(np.median(step_ms)), "step_ms": [round(x, 3) for x in step_ms], "step_host_ms": host_ms, "p50_single_query_latency_ms": float(np.median(lat)),
         "recall_at_k_vs_exact_mol": recall, "result_digest_step0": digest, "recall_queries": R,
+        "oracle_parity": parity,
         "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "step_ms": [round(x, 3) for x in e2e_step_ms]},
         "gpu_launches": int(launches), "roofline": roof, "rooflines": rooflines, "kernels": kernels,

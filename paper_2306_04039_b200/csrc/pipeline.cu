@@ -505,6 +505,18 @@ int molr_mol_top_k(molr_ctx* ctx, const molr_cache* c, const molr_gating* g, int
     }
   } else if (k < 1 || k > c->X) {
     MOLR_FAIL(MOLR_ERR_OUT_OF_RANGE, "k=%d outside [1, %lld]", k, (long long)c->X);
+  } else {
+    // whole-corpus ranking materialises a (users x X) f32 score block: bound it (4 GB) by running
+    // the users in chunks (100M items x 1024 users would otherwise need 400 GB)
+    const int64_t per = std::max<int64_t>(1, (int64_t(1) << 30) / std::max<int64_t>(c->X, 1));
+    if (B > per) {
+      for (int64_t b0 = 0; b0 < B; b0 += per) {
+        const int nb = int(std::min<int64_t>(per, B - b0));
+        MOLR_TRY(molr_mol_top_k(ctx, c, g, nb, k_u, ue + b0 * k_u * c->d, uw + b0 * c->G, tau, nullptr, nullptr, k,
+                                out_ids + b0 * k, out_scores + b0 * k, stream));
+      }
+      return MOLR_OK;
+    }
   }
   Scratch sc;
   MOLR_TRY(sc.alloc(size_t(total) * 4, s));

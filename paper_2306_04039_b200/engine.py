@@ -13,7 +13,8 @@ import numpy as np
 
 from paper_2306_04039_b200 import _lib as L
 from paper_2306_04039_b200.hindexer import HIndexerConfig
-from paper_2306_04039_b200.mol import GatingNetwork, _gating_handle
+from paper_2306_04039_b200.errors import DimensionMismatchError
+from paper_2306_04039_b200.mol import GatingNetwork, _gating_handle, cache_handle
 
 
 def _mode(h: HIndexerConfig) -> int:
@@ -22,22 +23,49 @@ def _mode(h: HIndexerConfig) -> int:
     return L.S1_FLOAT
 
 
+def _host_or_f32_tensor(a, name):
+    """Host inputs become contiguous float32 NumPy arrays; device tensors must already be float32
+    and contiguous (their data pointer is read as such by the C-ABI)."""
+    if hasattr(a, "data_ptr") and not isinstance(a, np.ndarray):
+        if str(getattr(a, "dtype", "")) not in ("torch.float32", "float32"):
+            raise DimensionMismatchError(f"{name}: device tensors must be float32, got {a.dtype}")
+        if hasattr(a, "is_contiguous") and not a.is_contiguous():
+            raise DimensionMismatchError(f"{name}: device tensors must be contiguous")
+        return a
+    return L.f32(np.asarray(a))
+
+
+def check_batch(cache, gating, user_embs, uw, *, uw_name="uw"):
+    """Validate a batch before raw pointers cross the C-ABI: user_embs (B, k_u, d) with
+    k_u * k_x = G = the cross net's width, and the gating rows (B, G) — user_net outputs, or raw
+    user features (B, d_u) when uw_name == "user_feats".  Returns (user_embs, uw) as float32."""
+    ue = _host_or_f32_tensor(user_embs, "user_embs")
+    w = _host_or_f32_tensor(uw, uw_name)
+    cfg = cache.config
+    shape = tuple(int(x) for x in ue.shape)
+    if len(shape) != 3 or shape[2] != cfg.d or shape[1] * cfg.k_x != gating.cross_net.in_dim:
+        raise DimensionMismatchError(
+            f"user_embs {shape} vs (B, k_u, {cfg.d}) with k_u * {cfg.k_x} = {gating.cross_net.in_dim}")
+    want = gating.user_net.in_dim if uw_name == "user_feats" else gating.cross_net.out_dim
+    if tuple(int(x) for x in w.shape) != (shape[0], want):
+        raise DimensionMismatchError(f"{uw_name} {tuple(w.shape)} vs ({shape[0]}, {want})")
+    return ue, w
+
+
 def two_stage_top_k(cache, gating: GatingNetwork, user_embs, uw, k: int, hconfig: HIndexerConfig, *, seed: int = 0,
                     id_offset: int = 0, out_ids=None, out_scores=None, out_cand=None, stream=None):
     """Device-resident batched two-stage top-k.  `user_embs` (B,k_u,d) and `uw` (B,G) may be host
     NumPy arrays or device tensors (anything with data_ptr()); outputs likewise.  Returns
     (ids (B,k) int64, scores (B,k) f32, candidate counts (B,) int64)."""
+    user_embs, uw = check_batch(cache, gating, user_embs, uw)
     B, k_u = int(user_embs.shape[0]), int(user_embs.shape[1])
     X = cache.num_items
     lam = hconfig.resolve_lambda(X)
-    if isinstance(user_embs, np.ndarray):
-        user_embs = L.f32(user_embs)
-        uw = L.f32(uw)
     if out_ids is None:
         out_ids = np.empty((B, k), dtype=np.int64)
         out_scores = np.empty((B, k), dtype=np.float32)
         out_cand = np.empty(B, dtype=np.int64)
-    L.call("molr_two_stage_top_k", L.ctx(), cache.device_handle(), _gating_handle(gating), B, k_u, L.ptr(user_embs),
+    L.call("molr_two_stage_top_k", L.ctx(), cache_handle(cache), _gating_handle(gating), B, k_u, L.ptr(user_embs),
            L.ptr(uw), float(cache.config.tau), _mode(hconfig), int(hconfig.k_prime), int(lam), int(seed) & (2**64 - 1),
            L.STRICT if hconfig.comparator == "strict" else L.INCLUSIVE, int(k), int(id_offset), L.ptr(out_ids),
            L.ptr(out_scores), L.ptr(out_cand), L.ptr(stream))
@@ -76,8 +104,15 @@ class RetrievalEngine:
         return int(getattr(self.params, "n_users", np.asarray(self.params.user_table).shape[0]))
 
     def query_state(self, user_id: int):
-        """user_forward (model.py:203-208): device query prep of one user."""
-        from paper_2306_04039_b200.errors import OutOfRangeError
+        """user_forward (model.py:203-208): the user tower is the caller's model code, not the MoL /
+        h-indexer path, so it is evaluated exactly as the reference evaluates it (NumPy:
+        silu(x @ w1 + b1) @ w2 -> reshape -> row L2 norm, model.py:179-191, mol.py:84-85,
+        numerics.py:41-50): the stage-1 query (mean of the components) and its int8 codes are then
+        bit-identical to the reference engine's, so the drop-in returns the reference's candidates.
+        The batched engine below runs the device query prep (molr_query_prep) instead."""
+        from scipy.special import expit
+
+        from paper_2306_04039_b200.errors import OutOfRangeError, ZeroNormError
         from paper_2306_04039_b200.mol import QueryState
 
         if not 0 <= user_id < self.num_users:
@@ -85,8 +120,17 @@ class RetrievalEngine:
         if getattr(self.params, "compression", None) is not None:
             raise ValueError("user-side compression maps are outside the B200 path (SURVEY.md §2)")
         feats = np.asarray(self.params.user_table)[user_id]
-        ue, _ = query_prep(self.params.user_proj, self.params.gating.user_net, feats[None, :], self.config)
-        return QueryState(user_embs=ue[0], gate_features=feats)
+        p = self.params.user_proj
+        x = feats[None, :]
+        hid = x @ np.asarray(p.w1) + np.asarray(p.b1)
+        raw = (hid * expit(hid)) @ np.asarray(p.w2)
+        embs = raw.reshape(1, self.config.k_u, self.config.d)
+        if self.config.l2_normalized:
+            norms = np.linalg.norm(embs, axis=-1, keepdims=True)
+            if np.any(norms <= 1e-12):
+                raise ZeroNormError("at least one row has norm <= eps")
+            embs = embs / norms.astype(embs.dtype)
+        return QueryState(user_embs=embs[0], gate_features=feats)
 
     def query(self, user_id: int, k: int, k_prime: int | None = None):
         """First-stage candidates, then exact MoL top-k (engine.py:117-138)."""
@@ -160,6 +204,7 @@ class BatchedRetrievalEngine:
         from dataclasses import replace
 
         h = self.hconfig if k_prime is None else replace(self.hconfig, k_prime=k_prime)
+        check_batch(self.cache, self.gating, user_embs, user_feats, uw_name="user_feats")
         uw = self.gating.user_net(np.asarray(user_feats))
         ids, sc, cand = two_stage_top_k(self.cache, self.gating, user_embs, uw, k, h,
                                         seed=self.seed if seed is None else seed)
@@ -209,7 +254,7 @@ def two_stage_top_k_sharded(cache, gating: GatingNetwork, user_embs, uw, k: int,
     else:
         n_rank = max(1, round(kp * lam / X_global))  # Python round(): half-even, as hindexer.py:131
         keys = np.empty((B, n_rank), dtype=np.uint32)
-        L.call("molr_sample_top_keys", L.ctx(), cache.device_handle(), B, k_u, L.ptr(ue), mode, int(X_global),
+        L.call("molr_sample_top_keys", L.ctx(), cache_handle(cache), B, k_u, L.ptr(ue), mode, int(X_global),
                int(row_lo), int(lam), int(seed) & (2**64 - 1), int(n_rank), L.ptr(keys), None)
         allk = np.asarray(exchange(keys))  # (P, B, n_rank)
         rows = np.ascontiguousarray(allk.transpose(1, 0, 2).reshape(B, -1))
@@ -225,7 +270,7 @@ def two_stage_top_k_sharded(cache, gating: GatingNetwork, user_embs, uw, k: int,
         ue_s = np.ascontiguousarray(ue[sel])  # (named: the buffers must outlive the call)
         uw_s = np.ascontiguousarray(uwf[sel])
         tk_s = np.ascontiguousarray(tk, dtype=np.uint32)
-        L.call("molr_two_stage_top_k_at", L.ctx(), cache.device_handle(), _gating_handle(gating), len(sel), k_u,
+        L.call("molr_two_stage_top_k_at", L.ctx(), cache_handle(cache), _gating_handle(gating), len(sel), k_u,
                L.ptr(ue_s), L.ptr(uw_s), float(cache.config.tau), mode, int(cap), L.ptr(tk_s), comp, int(k),
                int(row_lo), L.ptr(ids), L.ptr(sc), L.ptr(cnt), None)
         return ids, sc, cnt

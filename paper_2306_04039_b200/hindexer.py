@@ -9,7 +9,6 @@ from __future__ import annotations
 
 import ctypes as C
 import threading
-import weakref
 from dataclasses import dataclass, replace
 from typing import Optional, Union
 
@@ -17,7 +16,7 @@ import numpy as np
 
 from paper_2306_04039_b200 import _lib as L
 from paper_2306_04039_b200.errors import CapacityError, DimensionMismatchError, OutOfRangeError
-from paper_2306_04039_b200.mol import ItemCache, _upload_cache
+from paper_2306_04039_b200.mol import ItemCache, cache_handle, device_copy
 from paper_2306_04039_b200.quant import QuantizedRows
 
 Stage1View = Union[np.ndarray, QuantizedRows]
@@ -91,39 +90,34 @@ def nth_largest(values, n: int) -> float:
     return float(out.value)
 
 
+def _is_quant(view) -> bool:
+    """A quantized stage-1 view: this package's QuantizedRows, the reference's molr.quant.QuantizedRows,
+    or anything else carrying int8 .codes and per-row .scales (duck-typed, quant.py:20-46)."""
+    return isinstance(view, QuantizedRows) or (hasattr(view, "codes") and hasattr(view, "scales"))
+
+
 def _view_size_dim(view: Stage1View):
-    if isinstance(view, QuantizedRows):
-        return view.codes.shape
+    if _is_quant(view):
+        codes = np.asarray(view.codes)
+        if codes.ndim != 2 or np.asarray(view.scales).shape != (codes.shape[0],):
+            raise DimensionMismatchError(f"codes {codes.shape} need one scale per row")
+        return codes.shape
     view = np.asarray(view)
     if view.ndim != 2:
         raise DimensionMismatchError(f"stage-1 view must be 2-D, got {view.shape}")
     return view.shape
 
 
-# ---- device copies of stage-1 views, keyed by the view object (weakly) ----------------------
-_views_lock = threading.Lock()
-_views: dict = {}
-
-
 def _device_view(view: Stage1View) -> int:
-    key = id(view)
-    with _views_lock:
-        ent = _views.get(key)
-        if ent is not None and ent[0]() is view:
-            return ent[1].value
-    if isinstance(view, QuantizedRows):
-        n, d = view.codes.shape
-        h = _upload_stage1(n, d, None, view)
-    else:
-        v = np.asarray(view)
-        h = _upload_stage1(v.shape[0], v.shape[1], v, None)
-    with _views_lock:
-        try:
-            ref = weakref.ref(view, lambda _r, k=key: _views.pop(k, None))
-        except TypeError:  # object without weakref support: keep for this call only
-            return _keep_alive(h)
-        _views[key] = (ref, h)
-    return h.value
+    """Device copy of a stage-1 view, uploaded once per view object (mol.device_copy: weakly keyed,
+    host arrays frozen, re-uploaded when the object's arrays change)."""
+    if _is_quant(view):
+        n, d = np.asarray(view.codes).shape
+        return device_copy(view, (view.codes, view.scales), lambda: _upload_stage1(n, d, None, view))
+    if isinstance(view, np.ndarray):
+        return device_copy(view, (view,), lambda: _upload_stage1(view.shape[0], view.shape[1], view, None))
+    v = np.asarray(view)  # a list or other array-like: this call only
+    return _keep_alive(_upload_stage1(v.shape[0], v.shape[1], v, None))
 
 
 _tmp = threading.local()
@@ -147,7 +141,7 @@ def _upload_stage1(n: int, d: int, s1, q) -> L.Handle:
 
 
 def _mode(view, raw_int_ordering: bool) -> int:
-    if isinstance(view, QuantizedRows):
+    if _is_quant(view):
         return L.S1_INT8_RAW if raw_int_ordering else L.S1_INT8
     return L.S1_FLOAT
 
@@ -237,7 +231,7 @@ def index_select(cache: ItemCache, indices) -> ItemCache:
     cfg = cache.config
     n = indices.size
     out = C.c_void_p()
-    L.call("molr_index_select", L.ctx(), cache.device_handle(), n, L.ptr(indices), C.byref(out))
+    L.call("molr_index_select", L.ctx(), cache_handle(cache), n, L.ptr(indices), C.byref(out))
     h = L.Handle(out.value, "molr_cache_destroy")
     embs = np.empty((n, cfg.k_x, cfg.d), dtype=np.float32)
     gp = np.empty((n, cfg.num_logits), dtype=np.float32)
@@ -247,6 +241,9 @@ def index_select(cache: ItemCache, indices) -> ItemCache:
         codes = np.empty((n, cache.stage1_q.codes.shape[1]), dtype=np.int8)
         scales = np.empty(n, dtype=np.float32)
     L.call("molr_cache_read", h.value, 0, n, L.ptr(embs), L.ptr(gp), L.ptr(s1), L.ptr(codes), L.ptr(scales), None)
+    for a in (embs, gp, s1, codes, scales):  # the device copy mirrors them: immutable (mol.py:218)
+        if a is not None:
+            a.flags.writeable = False
     q = QuantizedRows(codes=codes, scales=scales) if codes is not None else None
     res = ItemCache(config=cfg, item_embs=embs, item_gate_pre=gp, stage1_embs=s1, stage1_q=q)
     res._dev = h
@@ -270,4 +267,3 @@ __all__ = [
     "HIndexerConfig", "CandidateSet", "nth_largest", "stage1_scores", "estimate_threshold", "h_indexer",
     "exact_top_k", "index_select", "stage1_view", "with_k_prime", "n_rank", "Stage1View",
 ]
-_ = _upload_cache

@@ -16,6 +16,7 @@ from __future__ import annotations
 import ctypes as C
 import hashlib
 import threading
+import weakref
 from dataclasses import dataclass, field
 from typing import Optional, Sequence
 
@@ -233,7 +234,6 @@ class ItemCache:
     stage1_embs: np.ndarray  # (X, d')
     stage1_q: Optional[QuantizedRows] = None
     _dev: Optional[L.Handle] = field(default=None, init=False, repr=False, compare=False)
-    _dev_lock: threading.Lock = field(default_factory=threading.Lock, init=False, repr=False, compare=False)
 
     def __post_init__(self):
         x = self.item_embs.shape[0]
@@ -267,13 +267,84 @@ class ItemCache:
         return snapshot.load_item_cache(path)
 
     def device_handle(self) -> int:
-        """molr_cache* of this snapshot (uploaded on first use)."""
-        if self._dev is None:
-            with self._dev_lock:
-                if self._dev is None:
-                    self._dev = _upload_cache(self.config, self.item_embs, self.item_gate_pre, self.stage1_embs,
-                                              self.stage1_q)
-        return self._dev.value
+        """molr_cache* of this snapshot (uploaded on first use; see cache_handle)."""
+        return cache_handle(self)
+
+
+# ---- device copies of host-side snapshots --------------------------------------------------------
+# Any ItemCache-shaped object (this module's ItemCache, the reference's molr.mol.ItemCache, anything
+# with config / item_embs / item_gate_pre / stage1_embs / stage1_q) and any stage-1 view (a 2-D
+# array, or any object with .codes / .scales) is uploaded once and kept, weakly keyed by the object,
+# for as long as the object lives.  The reference documents both as immutable (mol.py:218,
+# quant.py:22): the uploaded host arrays are marked read-only, so an in-place edit fails loudly
+# instead of being served a stale device copy, and each use checks a fingerprint (array identity,
+# buffer, layout and 4,096 sampled elements) so arrays swapped into the object are re-uploaded.
+_copies_lock = threading.Lock()
+_copies: dict = {}
+
+
+def _fingerprint(arrays) -> tuple:
+    fp = []
+    for a in arrays:
+        if a is None:
+            fp.append(None)
+            continue
+        if isinstance(a, np.ndarray) and a.flags.writeable:
+            try:
+                a.flags.writeable = False
+            except ValueError:  # a view of a buffer we may not freeze: the fingerprint still guards
+                pass
+        arr = np.asarray(a)
+        n = arr.size
+        sample = arr.flat[np.linspace(0, n - 1, num=min(n, 4096)).astype(np.int64)].tobytes() if n else b""
+        fp.append((id(a), arr.__array_interface__["data"][0], arr.shape, arr.strides, arr.dtype.str,
+                   hashlib.blake2b(sample, digest_size=8).digest()))
+    return tuple(fp)
+
+
+def device_copy(obj, arrays, upload) -> int:
+    """Handle value of the device copy of `obj` (whose content is `arrays`), created by
+    `upload() -> L.Handle` on first use or when the content changed."""
+    fp = _fingerprint(arrays)
+    key = (L.device_index(), id(obj))
+    with _copies_lock:
+        ent = _copies.get(key)
+        if ent is not None and ent[0]() is obj and ent[1] == fp:
+            return ent[2].value
+    h = upload()
+    with _copies_lock:
+        try:
+            ref = weakref.ref(obj, lambda _r, k=key: _copies.pop(k, None))
+        except TypeError:  # no weakref support: keep the copy for this thread's current call only
+            _tmp.h = h
+            return h.value
+        _copies[key] = (ref, fp, h)
+    return h.value
+
+
+_tmp = threading.local()
+
+
+def _quant_arrays(q):
+    return (None, None) if q is None else (q.codes, q.scales)
+
+
+def cache_handle(cache) -> int:
+    """molr_cache* for any cache the scoring / retrieval functions accept: a DeviceItemCache (or
+    anything else exposing device_handle()), this module's ItemCache, or any ItemCache-shaped
+    object such as the reference's molr.mol.ItemCache (duck-typed, uploaded once)."""
+    if not isinstance(cache, ItemCache) and hasattr(cache, "device_handle"):
+        return cache.device_handle()
+    pre = getattr(cache, "_dev", None)
+    if isinstance(pre, L.Handle):  # built on the device (index_select): the host arrays mirror it
+        return pre.value
+    for f in ("config", "item_embs", "item_gate_pre", "stage1_embs"):
+        if not hasattr(cache, f):
+            raise TypeError(f"{type(cache).__name__} is not an ItemCache (no .{f})")
+    q = getattr(cache, "stage1_q", None)
+    arrays = (cache.item_embs, cache.item_gate_pre, cache.stage1_embs) + _quant_arrays(q)
+    return device_copy(cache, arrays, lambda: _upload_cache(cache.config, cache.item_embs, cache.item_gate_pre,
+                                                           cache.stage1_embs, q))
 
 
 def _upload_cache(cfg: MoLConfig, embs, gp, s1, q: Optional[QuantizedRows]) -> L.Handle:
@@ -311,6 +382,15 @@ class DeviceItemCache:
         """Fill rows [row0, row0+n) from host arrays or device tensors (data pointers)."""
         L.call("molr_cache_fill", self._dev.value, row0, n, L.ptr(item_embs), L.ptr(item_gate_pre),
                L.ptr(stage1_embs), L.ptr(stage1_codes), L.ptr(stage1_scales), L.ptr(stream))
+
+    def read(self, row0: int, n: int):
+        """Rows [row0, row0+n) back to the host as the reference's f32 ItemCache fields:
+        (item_embs (n,k_x,d), item_gate_pre (n,G)) — exact (bf16 storage widens losslessly)."""
+        cfg = self.config
+        embs = np.empty((n, cfg.k_x, cfg.d), dtype=np.float32)
+        gp = np.empty((n, cfg.num_logits), dtype=np.float32)
+        L.call("molr_cache_read", self._dev.value, int(row0), int(n), L.ptr(embs), L.ptr(gp), None, None, None, None)
+        return embs, gp
 
     @property
     def num_items(self) -> int:
@@ -386,6 +466,18 @@ def build_device_item_cache(item_table, item_proj: Mlp, item_net: Mlp, config: M
     return dev
 
 
+def _check_users(cache, gating, user_embs, user_feats) -> None:
+    """(U, k_u, d) user components and (U, d_u) gating features consistent with the cache and nets,
+    checked before their pointers cross the C-ABI (which reads U * G floats of user_net output)."""
+    cfg = cache.config
+    if user_embs.ndim != 3 or user_embs.shape[2] != cfg.d or user_embs.shape[1] * cfg.k_x != gating.cross_net.in_dim:
+        raise DimensionMismatchError(f"user_embs {user_embs.shape} vs (U, k_u, {cfg.d}) with k_u * {cfg.k_x} = "
+                                     f"{gating.cross_net.in_dim}")
+    if user_feats.shape != (user_embs.shape[0], gating.user_net.in_dim):
+        raise DimensionMismatchError(f"user_feats {user_feats.shape} vs ({user_embs.shape[0]}, "
+                                     f"{gating.user_net.in_dim})")
+
+
 def _validate_candidates(cache, candidate_ids) -> np.ndarray:
     ids = np.asarray(candidate_ids, dtype=np.int64).reshape(-1)
     if ids.size == 0:
@@ -413,7 +505,7 @@ def score_candidates(cache, gating: GatingNetwork, candidate_ids, query: QuerySt
     ue, uw = _query_arrays(cache, query, gating)
     out = np.empty(ids.size, dtype=np.float32)
     offs = np.array([0, ids.size], dtype=np.int64)
-    L.call("molr_score", L.ctx(), cache.device_handle(), _gating_handle(gating), 1, ue.shape[0], L.ptr(ue),
+    L.call("molr_score", L.ctx(), cache_handle(cache), _gating_handle(gating), 1, ue.shape[0], L.ptr(ue),
            L.ptr(uw), float(cache.config.tau), L.ptr(offs), L.ptr(ids), L.ptr(out), None)
     return out.astype(_out_dtype(query.user_embs, np.float32), copy=False)
 
@@ -430,6 +522,7 @@ def batch_score_all(cache, gating: GatingNetwork, user_embs, user_feats, *, pair
     cfg = cache.config
     if user_embs.ndim != 3 or user_embs.shape[2] != cfg.d:
         raise DimensionMismatchError(f"user_embs {user_embs.shape} vs d {cfg.d}")
+    _check_users(cache, gating, user_embs, user_feats)
     out = np.empty((U, X), dtype=np.float32)
     if U == 0 or X == 0:
         return out
@@ -439,7 +532,7 @@ def batch_score_all(cache, gating: GatingNetwork, user_embs, user_feats, *, pair
     gh = _gating_handle(gating)
     for lo in range(0, U, per):
         hi = min(lo + per, U)
-        L.call("molr_score", L.ctx(), cache.device_handle(), gh, hi - lo, ue.shape[1], L.ptr(ue[lo:hi]),
+        L.call("molr_score", L.ctx(), cache_handle(cache), gh, hi - lo, ue.shape[1], L.ptr(ue[lo:hi]),
                L.ptr(uw_all[lo:hi]), float(cfg.tau), None, None, L.ptr(out[lo:hi]), None)
     return out
 
@@ -457,7 +550,7 @@ def mol_top_k(cache, gating: GatingNetwork, candidate_ids: Sequence[int] | np.nd
     out_ids = np.empty(k, dtype=np.int64)
     out_sc = np.empty(k, dtype=np.float32)
     offs = np.array([0, ids.size], dtype=np.int64)
-    L.call("molr_mol_top_k", L.ctx(), cache.device_handle(), _gating_handle(gating), 1, ue.shape[0], L.ptr(ue),
+    L.call("molr_mol_top_k", L.ctx(), cache_handle(cache), _gating_handle(gating), 1, ue.shape[0], L.ptr(ue),
            L.ptr(uw), float(cache.config.tau), L.ptr(offs), L.ptr(ids), int(k), L.ptr(out_ids), L.ptr(out_sc), None)
     return out_ids, out_sc.astype(_out_dtype(query.user_embs, np.float32), copy=False)
 
@@ -467,6 +560,7 @@ def batch_mol_top_k(cache, gating: GatingNetwork, user_embs, user_feats, k: int,
     whole corpus (candidates=None, = RetrievalEngine.full_top_k, engine.py:140-147).
     Returns (ids (B,k) int64, scores (B,k) float32)."""
     ue = L.f32(user_embs)
+    _check_users(cache, gating, ue, np.asarray(user_feats))
     B = ue.shape[0]
     uw = L.f32(gating.user_net(np.asarray(user_feats)))
     out_ids = np.empty((B, k), dtype=np.int64)
@@ -480,7 +574,7 @@ def batch_mol_top_k(cache, gating: GatingNetwork, user_embs, user_feats, k: int,
         offs = np.zeros(B + 1, dtype=np.int64)
         offs[1:] = np.cumsum([c.size for c in lists])
         ids = np.ascontiguousarray(np.concatenate(lists))
-    L.call("molr_mol_top_k", L.ctx(), cache.device_handle(), _gating_handle(gating), B, ue.shape[1], L.ptr(ue),
+    L.call("molr_mol_top_k", L.ctx(), cache_handle(cache), _gating_handle(gating), B, ue.shape[1], L.ptr(ue),
            L.ptr(uw), float(cache.config.tau), L.ptr(offs), L.ptr(ids), int(k), L.ptr(out_ids), L.ptr(out_sc), None)
     return out_ids, out_sc
 

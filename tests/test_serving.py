@@ -185,9 +185,25 @@ def test_retrieval_engine_drop_in(golden):
             np.array([s for _, s in f]), g["full_scores"][u]).all()
         np.testing.assert_allclose([s for _, s in f], g["full_scores"][u], rtol=1e-3, atol=1e-6)
         np.testing.assert_allclose([s for _, s in q], g["query_scores"][u], rtol=1e-3, atol=1e-6)
-        assert len(set(i for i, _ in q) & set(g["query_ids"][u].tolist())) >= 9
+        # same candidates as the reference engine (bit-exact stage 1), so the same top-k modulo
+        # ties within the score tolerance
+        qi = [i for i, _ in q]
+        ref_i = g["query_ids"][u].tolist()
+        if qi != ref_i:
+            kth = g["query_scores"][u][-1]
+            got_s = dict(q)
+            diff = set(qi) ^ set(ref_i)
+            assert all(abs(got_s.get(i, kth) - kth) <= 1e-3 * abs(kth) + 1e-6 for i in diff), (u, qi, ref_i)
+        fi = [i for i, _ in f]
+        if fi != g["full_ids"][u].tolist():
+            kth = g["full_scores"][u][-1]
+            got_s = dict(f)
+            diff = set(fi) ^ set(g["full_ids"][u].tolist())
+            assert all(abs(got_s.get(i, kth) - kth) <= 1e-3 * abs(kth) + 1e-6 for i in diff), (u, fi)
     assert eng.query(3, 10) == eng.query(3, 10)  # deterministic per (seed, user)
-    with pytest.raises(Exception):
+    from paper_2306_04039_b200.errors import OutOfRangeError
+
+    with pytest.raises(OutOfRangeError):
         eng.query(10_000, 5)
 
 
