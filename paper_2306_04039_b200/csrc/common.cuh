@@ -20,6 +20,16 @@
 
 namespace molr {
 
+// Development / cross-check switches (alternative backends, pilot sizes, the MoL epilogue trace).
+// They exist only in the test build, libmolr_b200_dev.so (-DMOLR_DEV_KNOBS), which the cross-check
+// tests load in a subprocess; the production library has one backend per shape and reads no
+// environment.
+#ifdef MOLR_DEV_KNOBS
+inline const char* dev_knob(const char* name) { return getenv(name); }
+#else
+inline const char* dev_knob(const char*) { return nullptr; }
+#endif
+
 // ------------------------------------------------------------------------------------------
 // status
 // ------------------------------------------------------------------------------------------

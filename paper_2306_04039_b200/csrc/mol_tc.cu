@@ -492,6 +492,9 @@ __global__ void __launch_bounds__(64 + NE * 256 + 32 * NE, 1) mol_tc_kernel(Para
     const int bar_id = 1 + eg;
     constexpr int NT = 256;                  // threads per group
     uint32_t ph = 0;
+#ifndef MOLR_DEV_KNOBS
+#define TRACE(tag)
+#else
 #define TRACE(tag)                                                                                     \
   if (P.trace && blockIdx.x == 0 && p == 0 && hf == 0) {                                               \
     unsigned long long c;                                                                              \
@@ -499,6 +502,7 @@ __global__ void __launch_bounds__(64 + NE * 256 + 32 * NE, 1) mol_tc_kernel(Para
     const unsigned long long i = atomicAdd(P.trace, 1ull);                                             \
     if (i < 65535) P.trace[1 + i] = (uint64_t(eg * 16 + (tag)) << 56) | (c & ((1ull << 56) - 1));      \
   }
+#endif
     TileCursor cur;
     for (int64_t tile = blockIdx.x + (int64_t)eg * gridDim.x; tile < T; tile += (int64_t)NE * gridDim.x) {
       const TileInfo t = tile_info(cur, tile, P.B, P.tile_pre, P.begin, P.end, P.X);
@@ -680,7 +684,7 @@ __global__ void b0_image_kernel(int B, const float* __restrict__ ue, uint8_t* __
 
 bool mol_tc_supported(const molr_cache* c, const molr_gating* g, int k_u) {
   return c && g && k_u == 8 && c->k_x == 8 && c->d == 64 && c->G == 64 && g->G == 64 && g->H == 128 &&
-         c->embs_bf16 != nullptr && c->gp_bf16 != nullptr && g->w1t_bf16 != nullptr && !getenv("MOLR_DISABLE_TC");
+         c->embs_bf16 != nullptr && c->gp_bf16 != nullptr && g->w1t_bf16 != nullptr && !dev_knob("MOLR_DISABLE_TC");
 }
 
 __global__ void tile_prefix_kernel(int B, const int64_t* begin, const int64_t* end, int64_t X, int P, int64_t* pre);
@@ -719,14 +723,14 @@ int mol_score_tc(molr_ctx* ctx, const molr_cache* c, const molr_gating* g, int B
   P.out = out;
   P.out_ld = out_ld;
   {
-    const char* e = getenv("MOLR_E1");
+    const char* e = dev_knob("MOLR_E1");
     P.e1_tanh = (e && e[0] == 'a') ? 0 : 1;
-    const char* gm = getenv("MOLR_GATHER");
+    const char* gm = dev_knob("MOLR_GATHER");
     P.gather4 = (c->embs_tmap_ok && !(gm && gm[0] == 'b')) ? 1 : 0;
   }
   Scratch trace;
   P.trace = nullptr;
-  const char* trace_path = getenv("MOLR_TRACE_MOL");
+  const char* trace_path = dev_knob("MOLR_TRACE_MOL");
   if (trace_path) {
     MOLR_TRY(trace.alloc(65536 * 8, s));
     MOLR_CUDA(cudaMemsetAsync(trace.p, 0, 8, s));

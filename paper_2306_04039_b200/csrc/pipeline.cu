@@ -188,10 +188,10 @@ int sample_threshold_tc(molr_ctx* ctx, int mode, const int8_t* scodes, const flo
   const double p = double(n_rank) / double(lam);
   int64_t lam0 = (int64_t)std::ceil(16.0 / p);
   lam0 = (lam0 + 255) / 256 * 256;
-  if (!getenv("MOLR_NO_PILOT") && lam0 * 4 <= lam) {
+  if (!dev_knob("MOLR_NO_PILOT") && lam0 * 4 <= lam) {
     const double mu = double(lam0) * p;
     int64_t n0 = std::min<int64_t>(lam0, (int64_t)std::ceil(mu + 6.0 * std::sqrt(mu) + 16.0));
-    if (const char* e = getenv("MOLR_PILOT_N0")) n0 = std::max<int64_t>(1, std::min<int64_t>(lam0, atoll(e)));  // tests
+    if (const char* e = dev_knob("MOLR_PILOT_N0")) n0 = std::max<int64_t>(1, std::min<int64_t>(lam0, atoll(e)));  // tests
     const double expect = double(lam) * double(n0) / double(lam0);
     const int64_t cap = (int64_t)(2.0 * expect) + 2048;
     Scratch pilot, t0, keys, counts, flag;
@@ -287,10 +287,10 @@ int sample_threshold_f32(molr_ctx* ctx, const molr_cache* c, const int64_t* samp
   const double p = double(n_rank) / double(lam);
   int64_t lam0 = (int64_t)std::ceil(16.0 / p);
   lam0 = (lam0 + 255) / 256 * 256;
-  if (c->d1 == 64 && !getenv("MOLR_NO_PILOT") && lam0 * 4 <= lam) {
+  if (c->d1 == 64 && !dev_knob("MOLR_NO_PILOT") && lam0 * 4 <= lam) {
     const double mu = double(lam0) * p;
     int64_t n0 = std::min<int64_t>(lam0, (int64_t)std::ceil(mu + 6.0 * std::sqrt(mu) + 16.0));
-    if (const char* e = getenv("MOLR_PILOT_N0")) n0 = std::max<int64_t>(1, std::min<int64_t>(lam0, atoll(e)));
+    if (const char* e = dev_knob("MOLR_PILOT_N0")) n0 = std::max<int64_t>(1, std::min<int64_t>(lam0, atoll(e)));
     const double expect = double(lam) * double(n0) / double(lam0);
     const int64_t cap = (int64_t)(2.0 * expect) + 2048;
     Scratch pilot, t0, keys, counts, flag;
@@ -890,7 +890,7 @@ int molr_sample_top_keys(molr_ctx* ctx, const molr_cache* c, int B, int k_u, con
       // largest whenever >= nk rows passed; otherwise the full score matrix below
       const double p = double(nk) / double(m);
       int64_t lam0 = ((int64_t)std::ceil(16.0 / p) + 255) / 256 * 256;
-      if (!getenv("MOLR_NO_PILOT") && lam0 * 4 <= m) {
+      if (!dev_knob("MOLR_NO_PILOT") && lam0 * 4 <= m) {
         const double mu = double(lam0) * p;
         const int64_t n0 = std::min<int64_t>(lam0, (int64_t)std::ceil(mu + 6.0 * std::sqrt(mu) + 16.0));
         const int64_t cap = (int64_t)(2.0 * double(m) * double(n0) / double(lam0)) + 2048;

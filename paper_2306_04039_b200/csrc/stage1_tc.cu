@@ -1352,8 +1352,8 @@ __global__ void gather_f32_rows_kernel(int64_t n, int64_t np, const float* __res
 }  // namespace s1bf
 
 bool s1_tc_supported(const molr_cache* c, int mode) {
-  return c && mode != MOLR_S1_FLOAT && c->d1 == 64 && c->s1_codes && c->s1_chunk_mm && !getenv("MOLR_DISABLE_TC") &&
-         !getenv("MOLR_S1_NO_TC");
+  return c && mode != MOLR_S1_FLOAT && c->d1 == 64 && c->s1_codes && c->s1_chunk_mm && !dev_knob("MOLR_DISABLE_TC") &&
+         !dev_knob("MOLR_S1_NO_TC");
 }
 
 // Scan rows [0, n) of an interleaved code matrix against B queries (chunks of 1024 per launch).
@@ -1401,7 +1401,7 @@ int s1_tc_scan(molr_ctx* ctx, int mode, const int8_t* codes, const float* scales
       }
       P.out = out ? reinterpret_cast<char*>(out) + int64_t(b0) * ld * 4 : nullptr;
       P.ld = ld;
-      const bool small = Bc <= SB && !getenv("MOLR_S1_NO_SMALL");
+      const bool small = Bc <= SB && !dev_knob("MOLR_S1_NO_SMALL");
       auto launch = [&](auto kern) -> int {
         const int bytes = small ? S_SMEM_BYTES : SMEM_BYTES;
         MOLR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
@@ -1444,7 +1444,7 @@ int s1_tc_scan(molr_ctx* ctx, int mode, const int8_t* codes, const float* scales
 }
 
 bool s1_bf_supported(const molr_cache* c, int mode) {
-  return c && mode == MOLR_S1_FLOAT && c->d1 == 64 && c->s1_f32 && c->X > 0 && !getenv("MOLR_DISABLE_TC") && !getenv("MOLR_S1_NO_BF");
+  return c && mode == MOLR_S1_FLOAT && c->d1 == 64 && c->s1_f32 && c->X > 0 && !dev_knob("MOLR_DISABLE_TC") && !dev_knob("MOLR_S1_NO_BF");
 }
 
 static int s1_bf_build(molr_cache* c, cudaStream_t s) {
@@ -1520,7 +1520,7 @@ int s1_f16_filter(molr_ctx* ctx, const F16View& V, int B, const float* q, const 
       P.cta_bcounts = bcount.as<int32_t>();
       {
         KTimer t(ctx, timer, s, double(Bc) * n);
-        if (Bc <= 32 && !getenv("MOLR_S1_NO_SMALL")) {  // items-in-M variant for small batches
+        if (Bc <= 32 && !dev_knob("MOLR_S1_NO_SMALL")) {  // items-in-M variant for small batches
           auto kern = Bc <= 16 ? bf_small_kernel<16> : bf_small_kernel<32>;
           MOLR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SS_SMEM));
           kern<<<grid, NTHREADS, SS_SMEM, s>>>(P);

@@ -13,6 +13,7 @@ GOLDEN = os.path.join(ROOT, "tests", "golden")
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
     config.addinivalue_line("markers", "slow: larger sizes")
+    config.addinivalue_line("markers", "devknobs: also cross-checks alternative backends under the dev build")
 
 
 @pytest.fixture(scope="session")

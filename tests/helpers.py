@@ -1,8 +1,28 @@
 """Shared test helpers: golden fixtures -> product objects and oracle objects."""
 
+import os
+
 import numpy as np
 
 import oracle as O
+
+# the development build (libmolr_b200_dev.so, -DMOLR_DEV_KNOBS): the only library that honours the
+# cross-check switches (alternative SIMT backends, pilot sizes); tests/test_gpu_devbuild.py runs the
+# `devknobs` tests under it in a subprocess
+DEV_BUILD = os.path.basename(os.environ.get("MOLR_LIB_PATH", "")) == "libmolr_b200_dev.so"
+
+
+def with_knob(monkeypatch, env, fn):
+    """fn() with the development switches `env` set — only under the dev build; None otherwise."""
+    if not DEV_BUILD:
+        return None
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    try:
+        return fn()
+    finally:
+        for k in env:
+            monkeypatch.delenv(k, raising=False)
 
 
 def bf16_to_f32(u16):

@@ -2,6 +2,7 @@
 the int8 view, same corpus (python tools/float_probe.py [X])."""
 import os, sys, time
 sys.path.insert(0, os.environ.get("GRAFT_REPO_ROOT", "/root/repo")); os.chdir(sys.path[0])
+os.environ["MOLR_LIB_PATH"] = os.path.join(sys.path[0], "paper_2306_04039_b200", "libmolr_b200_dev.so")  # switches
 import numpy as np, torch
 import bench as Bm
 from paper_2306_04039_b200 import _lib as L

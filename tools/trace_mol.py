@@ -7,6 +7,8 @@ import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 os.environ["MOLR_TRACE_MOL"] = "/tmp/mol_trace.bin"
+# the trace exists only in the development build (-DMOLR_DEV_KNOBS)
+os.environ["MOLR_LIB_PATH"] = os.path.join(sys.path[0], "paper_2306_04039_b200", "libmolr_b200_dev.so")
 from tests.test_gpu_parity import _prod_gating, _synthetic_prod_cache  # noqa: E402
 from paper_2306_04039_b200.mol import batch_score_all  # noqa: E402
 
