@@ -308,7 +308,8 @@ def oracle_parity(cfg, model, cache, ue, feats, ids, scores, q_exact, q_scores=8
     uw = O.mlp(O.MlpW(*model["user_net"]), feats).astype(np.float32)
     cross = CO.Net(*model["cross_net"])
     q = min(q_exact, ids.shape[0])
-    chunk = max(1, min(1 << 20, (1 << 28) // max(q, 1)))
+    # 256K rows (0.5 GB of f32 staging on the device, which the 100M cache leaves little room for)
+    chunk = max(1, min(1 << 18, (1 << 28) // max(q, 1)))
     ex_i, ex_s = CO.exact_top_k_streamed(cache.read, X, ue[:q], uw[:q], cross, TAU, k, chunk=chunk)
     recall = float(np.mean([len(set(ids[b].tolist()) & set(ex_i[b].tolist())) / k for b in range(q)]))
     identical = int(sum(ids[b].tolist() == ex_i[b].tolist() for b in range(q)))

@@ -121,12 +121,12 @@ def exact_top_k_streamed(read_rows, n_items: int, user_embs, uw, cross: Net, tau
                          chunk: int = 1 << 21, threads: int = 0):
     """The reference's exhaustive MoL top-k (RetrievalEngine.full_top_k, engine.py:140-147: every
     item scored by mol.py:329-345, ranked by np.lexsort((ids, -s)), mol.py:407) over a corpus too
-    large to hold on the host in f32: `read_rows(lo, hi)` returns (item_embs (n,k_x,d),
-    gate_pre (n,G)) for rows [lo, hi) (f32 or bf16 bits).  Returns (ids (B,k), scores (B,k))."""
+    large to hold on the host in f32: `read_rows(row0, n)` returns (item_embs (n,k_x,d),
+    gate_pre (n,G)) for rows [row0, row0 + n) (f32 or bf16 bits).  Returns (ids (B,k), scores (B,k))."""
     ue = np.ascontiguousarray(user_embs, dtype=np.float32)
     tk = TopK(ue.shape[0], k)
     for lo in range(0, n_items, chunk):
         hi = min(n_items, lo + chunk)
-        e, g = read_rows(lo, hi)
+        e, g = read_rows(lo, hi - lo)
         tk.add(scores(e, g, ue, uw, cross, tau, threads=threads), lo, threads=threads)
     return tk.ids, tk.scores

@@ -1,6 +1,6 @@
 set -x
-nproc; free -g | head -2
-timeout 2400 python -m pytest tests -q -m gpu -x -k "baseline_configs or dropin or serving or oracle" 2>&1 | tail -40 > gpurun_out/r2b_newtests.log
-timeout 600 python bench.py --config ml1m --no-cpu > gpurun_out/r2b_bench_ml1m.json 2> gpurun_out/r2b_bench_ml1m.err
-timeout 900 python bench.py --no-cpu > gpurun_out/r2b_bench_100m.json 2> gpurun_out/r2b_bench_100m.err
-timeout 2400 python -m pytest tests -q -m gpu 2>&1 | tail -30 > gpurun_out/r2b_gputest_all.log
+lscpu | head -20
+python tools/blas_order_probe.py > gpurun_out/r2c_blas_order.log 2>&1
+timeout 900 python -m pytest tests -q -m gpu -x -k "baseline_configs" 2>&1 | tail -5 > gpurun_out/r2c_newtests.log
+timeout 900 ncu --set full --import-source on --kernel-name-base demangled -k 'regex:s1_tc_kernel<0>' -c 1 -o gpurun_out/r2c_s1_full python bench.py --config 10m --steps 1 --warmup 1 --no-cpu --no-oracle > gpurun_out/r2c_ncu.log 2>&1
+timeout 900 python bench.py --no-cpu > gpurun_out/r2c_bench_100m.json 2> gpurun_out/r2c_bench_100m.err
