@@ -70,26 +70,31 @@ __global__ void iota_kernel(int32_t* p, int64_t n) {
     p[i] = int32_t(i);
 }
 
-// Sort the rows of each 256-row tile by scale (ascending; padding rows, scale 0, last) and
-// permute codes / scales / perm accordingly.  One CTA per tile.
-__global__ void __launch_bounds__(256) seal_sort_kernel(int8_t* __restrict__ codes, float* __restrict__ scales,
-                                                        int32_t* __restrict__ perm) {
-  __shared__ uint64_t key[256];
-  __shared__ int4 tcodes[256 * 4];
-  __shared__ float tsc[256];
-  __shared__ int32_t tperm[256];
-  const int t = threadIdx.x;
-  const int64_t r0 = int64_t(blockIdx.x) * 256;
-  const float sc = scales[r0 + t];
-  tsc[t] = sc;
-  tperm[t] = perm[r0 + t];
-  for (int c = 0; c < 4; ++c) tcodes[t * 4 + c] = *reinterpret_cast<const int4*>(codes + s1_chunk_offset(r0 + t, c, 64));
-  const uint32_t k = sc > 0.f ? __float_as_uint(sc) : 0xffffffffu;  // positive floats order as uints
-  key[t] = (uint64_t(k) << 32) | uint32_t(t);
+// Sort the stored rows by scale (ascending; padding rows, scale 0, last) inside windows of
+// S1_SORT_WINDOW rows: the filter's per-32-row integer bound (from the chunk's scale range) is then
+// nearly exact, so far fewer (query, 8-row group) blocks need the exact test (measured on the
+// synthetic corpus: 12% -> 7% of warp groups vs 256-row windows).  The candidate ids of a window
+// stay within its 4,096 items, so stage 2 keeps its locality.
+constexpr int S1_SORT_WINDOW = 4096;
+
+// keys of one window -> the window-local source row of every destination row
+__global__ void __launch_bounds__(1024) window_sort_kernel(const float* __restrict__ scales, int64_t n_rows,
+                                                           int32_t* __restrict__ src_local) {
+  __shared__ uint64_t key[S1_SORT_WINDOW];
+  const int64_t w0 = int64_t(blockIdx.x) * S1_SORT_WINDOW;
+  const int n = int(imin64(S1_SORT_WINDOW, n_rows - w0));
+  for (int i = threadIdx.x; i < S1_SORT_WINDOW; i += blockDim.x) {
+    uint32_t k = 0xffffffffu;  // past the end: after everything
+    if (i < n) {
+      const float sc = scales[w0 + i];
+      k = sc > 0.f ? __float_as_uint(sc) : 0xfffffffeu;  // positive floats order as uints; padding last
+    }
+    key[i] = (uint64_t(k) << 32) | uint32_t(i);
+  }
   __syncthreads();
-  for (int size = 2; size <= 256; size <<= 1)
+  for (int size = 2; size <= S1_SORT_WINDOW; size <<= 1)
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      if (t < 128) {
+      for (int t = threadIdx.x; t < S1_SORT_WINDOW / 2; t += blockDim.x) {
         const int lo = 2 * t - (t & (stride - 1)), hi = lo + stride;
         const bool up = (lo & size) == 0;
         const uint64_t x = key[lo], y = key[hi];
@@ -100,10 +105,52 @@ __global__ void __launch_bounds__(256) seal_sort_kernel(int8_t* __restrict__ cod
       }
       __syncthreads();
     }
-  const int src = int(key[t] & 0xffffffffu);
-  scales[r0 + t] = tsc[src];
-  perm[r0 + t] = tperm[src];
-  for (int c = 0; c < 4; ++c) *reinterpret_cast<int4*>(codes + s1_chunk_offset(r0 + t, c, 64)) = tcodes[src * 4 + c];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) src_local[w0 + i] = int32_t(key[i] & 0xffffffffu);
+}
+
+// rows [r0, r1) := old rows (w0 + src_local) of a copy of the slab starting at row s0
+__global__ void window_gather_kernel(int64_t s0, int64_t r0, int64_t r1, const int32_t* __restrict__ src_local,
+                                     const int8_t* __restrict__ old_codes, const float* __restrict__ old_scales,
+                                     const int32_t* __restrict__ old_perm, int8_t* __restrict__ codes,
+                                     float* __restrict__ scales, int32_t* __restrict__ perm) {
+  for (int64_t i = r0 * 4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < r1 * 4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i >> 2;
+    const int c = int(i & 3);
+    const int64_t src = r / S1_SORT_WINDOW * S1_SORT_WINDOW + src_local[r];
+    *reinterpret_cast<int4*>(codes + s1_chunk_offset(r, c, 64)) =
+        *reinterpret_cast<const int4*>(old_codes + s1_chunk_offset(src - s0, c, 64));
+    if (c == 0) {
+      scales[r] = old_scales[src - s0];
+      perm[r] = old_perm[src - s0];
+    }
+  }
+}
+
+static int s1_window_sort(molr_cache* c, int64_t xr, cudaStream_t s) {
+  const int64_t nwin = (xr + S1_SORT_WINDOW - 1) / S1_SORT_WINDOW;
+  Scratch src;
+  MOLR_TRY(src.alloc(size_t(xr) * 4, s));
+  window_sort_kernel<<<(unsigned)nwin, 1024, 0, s>>>(c->s1_scales, xr, src.as<int32_t>());
+  MOLR_LAUNCHED(c->ctx);
+  // permute slab by slab through a bounded copy (whole windows; 2^24 rows = 1 GB of codes)
+  const int64_t slab = std::min<int64_t>(xr, int64_t(1) << 24);
+  Scratch oc, os_, op;
+  MOLR_TRY(oc.alloc(size_t(slab) * 64, s));
+  MOLR_TRY(os_.alloc(size_t(slab) * 4, s));
+  MOLR_TRY(op.alloc(size_t(slab) * 4, s));
+  for (int64_t s0 = 0; s0 < xr; s0 += slab) {
+    const int64_t n = std::min<int64_t>(slab, xr - s0);
+    // the interleaved layout is row-block linear, so a slab starting at a multiple of 8 rows is contiguous
+    MOLR_CUDA(cudaMemcpyAsync(oc.p, c->s1_codes + s1_chunk_offset(s0, 0, 64), size_t(n) * 64, cudaMemcpyDeviceToDevice, s));
+    MOLR_CUDA(cudaMemcpyAsync(os_.p, c->s1_scales + s0, size_t(n) * 4, cudaMemcpyDeviceToDevice, s));
+    MOLR_CUDA(cudaMemcpyAsync(op.p, c->s1_perm + s0, size_t(n) * 4, cudaMemcpyDeviceToDevice, s));
+    window_gather_kernel<<<div_up(n * 4, 256), 256, 0, s>>>(s0, s0, s0 + n, src.as<int32_t>(), oc.as<int8_t>(),
+                                                             os_.as<float>(), op.as<int32_t>(), c->s1_codes,
+                                                             c->s1_scales, c->s1_perm);
+    MOLR_LAUNCHED(c->ctx);
+  }
+  return MOLR_OK;
 }
 
 __global__ void inv_perm_kernel(const int32_t* __restrict__ perm, int64_t n_rows, int64_t X, int32_t* __restrict__ inv) {
@@ -113,7 +160,7 @@ __global__ void inv_perm_kernel(const int32_t* __restrict__ perm, int64_t n_rows
   }
 }
 
-// Seal the int8 view of a cache: sort tiles by scale, rebuild inv and the chunk min/max.
+// Seal the int8 view of a cache: sort rows by scale within windows, rebuild inv and the chunk min/max.
 // Idempotent and thread-safe; called by every stage-1 entry point before reading the view.
 int s1_seal(molr_cache* c, cudaStream_t s) {
   if (!c->s1_perm || c->s1_sealed.load(std::memory_order_acquire)) return MOLR_OK;
@@ -121,8 +168,7 @@ int s1_seal(molr_cache* c, cudaStream_t s) {
   if (c->s1_sealed.load()) return MOLR_OK;
   const int64_t xr = s1_rows_alloc(c->X, c->d1);
   if (xr > 0) {
-    seal_sort_kernel<<<(unsigned)(xr / 256), 256, 0, s>>>(c->s1_codes, c->s1_scales, c->s1_perm);
-    MOLR_LAUNCHED(c->ctx);
+    MOLR_TRY(s1_window_sort(c, xr, s));
     inv_perm_kernel<<<div_up(xr, 256), 256, 0, s>>>(c->s1_perm, xr, c->X, c->s1_inv);
     MOLR_LAUNCHED(c->ctx);
     MOLR_TRY(s1_update_chunk_mm(c, 0, xr, s));
