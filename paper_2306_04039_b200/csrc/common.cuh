@@ -409,6 +409,60 @@ __host__ __device__ __forceinline__ int64_t s1_rows_alloc(int64_t X, int d1) {
   return d1 == 64 ? (X + 255) / 256 * 256 : X;
 }
 
+// The reference's float stage-1 score is NumPy's `view @ q` (hindexer.py:112), i.e. OpenBLAS sgemv.
+// Its summation order on the reference host (OpenBLAS 0.3.30 SkylakeX kernels; the GPU box reports
+// the same, tools/blas_order_probe.py) for rows inside sgemv's 4-row blocks is reproduced exactly:
+//   d % 8 == 0 and d >= 16: four lanes and two accumulators taking alternate 4-element blocks
+//     (fused multiply-add), lanes combined (acc0 + acc1), then (l0 + l1) + (l2 + l3);
+//   d == 8: rounded products, ((p0 + p1) + (p2 + p3)) + ((p4 + p5) + (p6 + p7));
+//   d == 4: (p0 + p1) + (p2 + p3);
+//   other d: the sequential fmaf chain (within fp32 summation-order tolerance of the reference).
+// (OpenBLAS scores the last X % 4 rows of a matrix with another kernel; those rows agree only to
+// within summation-order tolerance.)
+__device__ __forceinline__ float s1_dot_f32(const float* __restrict__ v, const float* __restrict__ q, int d) {
+  if (d >= 16 && (d & 7) == 0) {
+    float a0[4] = {0.f, 0.f, 0.f, 0.f}, a1[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int k = 0; k < d; k += 8) {
+#pragma unroll
+      for (int l = 0; l < 4; ++l) {
+        a0[l] = fmaf(v[k + l], q[k + l], a0[l]);
+        a1[l] = fmaf(v[k + 4 + l], q[k + 4 + l], a1[l]);
+      }
+    }
+    const float t0 = a0[0] + a1[0], t1 = a0[1] + a1[1], t2 = a0[2] + a1[2], t3 = a0[3] + a1[3];
+    return (t0 + t1) + (t2 + t3);
+  }
+  if (d == 8) {
+    float p[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) p[k] = __fmul_rn(v[k], q[k]);
+    return ((p[0] + p[1]) + (p[2] + p[3])) + ((p[4] + p[5]) + (p[6] + p[7]));
+  }
+  if (d == 4) return (__fmul_rn(v[0], q[0]) + __fmul_rn(v[1], q[1])) + (__fmul_rn(v[2], q[2]) + __fmul_rn(v[3], q[3]));
+  float acc = 0.f;
+  for (int k = 0; k < d; ++k) acc = fmaf(v[k], q[k], acc);
+  return acc;
+}
+
+// d = 64 with the row already in registers (same order as s1_dot_f32)
+__device__ __forceinline__ float s1_dot64(const float (&v)[64], const float* __restrict__ q) {
+  float a0[4] = {0.f, 0.f, 0.f, 0.f}, a1[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int k = 0; k < 64; k += 8) {
+    const float4 x = *reinterpret_cast<const float4*>(q + k), y = *reinterpret_cast<const float4*>(q + k + 4);
+    a0[0] = fmaf(v[k], x.x, a0[0]);
+    a0[1] = fmaf(v[k + 1], x.y, a0[1]);
+    a0[2] = fmaf(v[k + 2], x.z, a0[2]);
+    a0[3] = fmaf(v[k + 3], x.w, a0[3]);
+    a1[0] = fmaf(v[k + 4], y.x, a1[0]);
+    a1[1] = fmaf(v[k + 5], y.y, a1[1]);
+    a1[2] = fmaf(v[k + 6], y.z, a1[2]);
+    a1[3] = fmaf(v[k + 7], y.w, a1[3]);
+  }
+  const float t0 = a0[0] + a1[0], t1 = a0[1] + a1[1], t2 = a0[2] + a1[2], t3 = a0[3] + a1[3];
+  return (t0 + t1) + (t2 + t3);
+}
+
 __host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
 __host__ __device__ __forceinline__ int64_t imax64(int64_t a, int64_t b) { return a > b ? a : b; }
 

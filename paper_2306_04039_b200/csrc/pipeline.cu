@@ -95,22 +95,7 @@ filter_scan_kernel(int64_t n, int dim, const float* __restrict__ vf, const int8_
       if (MODE == MOLR_S1_FLOAT) {
         const float* v = vf + r * dim;
         const float* q = reinterpret_cast<const float*>(qs) + b * dim;
-        float acc = 0.f;
-        if (dim == 64) {  // (the row is re-read from L1 per query; same sequential fmaf chain)
-          const float4* v4 = reinterpret_cast<const float4*>(v);
-          const float4* q4 = reinterpret_cast<const float4*>(q);
-#pragma unroll
-          for (int k = 0; k < 16; ++k) {
-            const float4 x = __ldg(v4 + k), y = q4[k];
-            acc = fmaf(x.x, y.x, acc);
-            acc = fmaf(x.y, y.y, acc);
-            acc = fmaf(x.z, y.z, acc);
-            acc = fmaf(x.w, y.w, acc);
-          }
-        } else {
-          for (int k = 0; k < dim; ++k) acc = fmaf(v[k], q[k], acc);
-        }
-        key = f32_key(acc);
+        key = f32_key(s1_dot_f32(v, q, dim));  // (the row is re-read from L1 per query)
       } else {
         int32_t acc = 0;
         const int64_t pos = inv ? inv[r] : r;
@@ -238,7 +223,7 @@ int sample_threshold_tc(molr_ctx* ctx, int mode, const int8_t* scodes, const flo
 }
 
 
-// Float view: score the sampled rows (v row in registers, the sequential fmaf chain of
+// Float view: score the sampled rows (v row in registers, the s1_dot64 order of
 // scan_scores_kernel) and append the ascending keys of the scores >= t0[b] (pilot threshold).
 __global__ void __launch_bounds__(256) sample_keys_f32_kernel(int64_t n, const float* __restrict__ vf,
                                                               const int64_t* __restrict__ rows_idx, int B,
@@ -261,17 +246,7 @@ __global__ void __launch_bounds__(256) sample_keys_f32_kernel(int64_t n, const f
       v[4 * k] = x.x, v[4 * k + 1] = x.y, v[4 * k + 2] = x.z, v[4 * k + 3] = x.w;
     }
     for (int b = 0; b < B; ++b) {
-      const float4* q4 = reinterpret_cast<const float4*>(q) + b * 16;
-      float acc = 0.f;
-#pragma unroll
-      for (int k = 0; k < 16; ++k) {
-        const float4 y = q4[k];
-        acc = fmaf(v[4 * k], y.x, acc);
-        acc = fmaf(v[4 * k + 1], y.y, acc);
-        acc = fmaf(v[4 * k + 2], y.z, acc);
-        acc = fmaf(v[4 * k + 3], y.w, acc);
-      }
-      const uint32_t key = f32_key(acc);
+      const uint32_t key = f32_key(s1_dot64(v, q + b * 64));
       if (key >= tk[b]) {
         const int64_t pos = (int64_t)atomicAdd(reinterpret_cast<unsigned long long*>(counts + b), 1ull);
         if (pos < cap) keys[int64_t(b) * cap + pos] = key;

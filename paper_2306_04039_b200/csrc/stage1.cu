@@ -79,7 +79,7 @@ __global__ void scan_scores_kernel(int mode, int64_t n, int dim, const float* __
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = rows_idx ? rows_idx[i] : i;
     if (mode == MOLR_S1_FLOAT && dim == 64) {
-      // the row stays in registers across the queries (same sequential fmaf chain)
+      // the row stays in registers across the queries (s1_dot64: NumPy/OpenBLAS order)
       float v[64];
       const float4* v4 = reinterpret_cast<const float4*>(vf + r * 64);
 #pragma unroll
@@ -87,26 +87,13 @@ __global__ void scan_scores_kernel(int mode, int64_t n, int dim, const float* __
         const float4 x = __ldg(v4 + k);
         v[4 * k] = x.x, v[4 * k + 1] = x.y, v[4 * k + 2] = x.z, v[4 * k + 3] = x.w;
       }
-      for (int b = 0; b < B; ++b) {
-        const float4* q4 = reinterpret_cast<const float4*>(sq) + b * 16;
-        float acc = 0.f;
-#pragma unroll
-        for (int k = 0; k < 16; ++k) {
-          const float4 y = q4[k];
-          acc = fmaf(v[4 * k], y.x, acc);
-          acc = fmaf(v[4 * k + 1], y.y, acc);
-          acc = fmaf(v[4 * k + 2], y.z, acc);
-          acc = fmaf(v[4 * k + 3], y.w, acc);
-        }
-        reinterpret_cast<float*>(out)[b * ld + i] = acc;
-      }
+      for (int b = 0; b < B; ++b)
+        reinterpret_cast<float*>(out)[b * ld + i] = s1_dot64(v, reinterpret_cast<const float*>(sq) + b * 64);
     } else if (mode == MOLR_S1_FLOAT) {
       const float* v = vf + r * dim;
       for (int b = 0; b < B; ++b) {
         const float* q = reinterpret_cast<const float*>(sq) + b * dim;
-        float acc = 0.f;
-        for (int k = 0; k < dim; ++k) acc = fmaf(v[k], q[k], acc);
-        reinterpret_cast<float*>(out)[b * ld + i] = acc;
+        reinterpret_cast<float*>(out)[b * ld + i] = s1_dot_f32(v, q, dim);
       }
     } else {
       const int64_t pos = inv ? inv[r] : r;  // stored position of item r (sealed, scale-sorted tiles)

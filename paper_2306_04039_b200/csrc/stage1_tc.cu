@@ -318,26 +318,33 @@ __global__ void __launch_bounds__(NTHREADS, 1) s1_tc_kernel(Params P) {
             }
           }
         } else {
-          // per thread: one query (TMEM lane), 64 item columns as 2 chunks of 32 rows
+          // per thread: one query (TMEM lane), 64 item columns as 2 chunks of 32 rows.  Per chunk
+          // the common case costs a 3-input max tree (0.5 instr per accumulator) and one warp vote:
+          //  * L = an integer bound necessary for passing anywhere in the 32-row chunk (from the
+          //    chunk's 1/min, 1/max scale with a 4e-6 relative margin; rows are stored sorted by
+          //    scale within 4,096-row windows, so the chunk's scale range and L are tight);
+          //  * chunk max >= L for no lane of the warp -> nothing in these 32 x 32 pairs can pass;
+          //  * otherwise per 8-row group another vote, and in a flagged group each accumulator
+          //    >= L (rare, divergent) gets the exact fp32 test fl(acc * scale) >= t
+          //    (NumPy's acc.astype(f32) * scales, hindexer.py:111; strict > as >= nextafter(t);
+          //    raw mode: acc >= t exactly, L itself) and is appended to the query's segment
+          //    with a shared-memory counter.
           const uint32_t traw = reinterpret_cast<const uint32_t*>(sm + OFF_T)[q];
           const float tf = __uint_as_float(traw);
-          // strict (s > t) as s >= the next float above t (thresholds are finite scores);
-          // raw: acc >= t (+1 when strict)
           const float tfe = P.strict ? __uint_as_float(tf >= 0.f ? (tf == 0.f ? 1u : traw + 1u) : traw - 1u) : tf;
           const int32_t ti = int32_t(traw) + (P.strict ? 1 : 0);
-          const float4* sc4 = reinterpret_cast<const float4*>(sc);
           const float tlo = tf * (1.0f - 4e-6f), thi = tf * (1.0f + 4e-6f);
-          uint32_t mask[2];
+          const bool qok = q < P.B;
+          int32_t* dst = qok ? cand_cta + int64_t(q) * P.cap : nullptr;
           uint32_t ra[32], rb[32];
           TMEM_LD32(tm, ra);
 #pragma unroll
           for (int cc = 0; cc < 2; ++cc) {
             uint32_t* a = cc ? rb : ra;
-            // integer bound L: acc >= L is necessary to pass anywhere in this 32-row chunk
-            // (from the chunk's (1/min, 1/max) scale with a relative margin; computed while the
-            // TMEM load is in flight).  Padding rows are masked below, so their bound is moot.
             int32_t L;
-            if (RAW) {
+            if (!qok) {
+              L = 0x7fffffff;  // padding query rows never flag a group
+            } else if (RAW) {
               L = ti;  // exact
             } else {
               const float2 inv = mm[cc];
@@ -346,63 +353,31 @@ __global__ void __launch_bounds__(NTHREADS, 1) s1_tc_kernel(Params P) {
             TMEM_WAIT32(a);
             if (cc == 0) TMEM_LD32(tm + 32, rb);  // next chunk loads under this chunk's test
             const int j0 = cc * 32;
-            // per 8-column group: max as a shallow tree of 3-input maxes; the warp-wide OR of the
-            // per-lane group hits makes the group branches warp-uniform
-            uint32_t h = 0;
+            const int32_t* v = reinterpret_cast<const int32_t*>(a);
+            int32_t gm[4];
 #pragma unroll
-            for (int g8 = 0; g8 < 4; ++g8) {
-              const int32_t* v = reinterpret_cast<const int32_t*>(a) + g8 * 8;
-              const int32_t gm = max(__vimax3_s32(v[0], v[1], v[2]), __vimax3_s32(v[3], v[4], max(v[5], max(v[6], v[7]))));
-              h |= uint32_t(gm >= L) << g8;
-            }
-            h = __reduce_or_sync(0xffffffffu, h);
-            uint32_t m = 0;
+            for (int g8 = 0; g8 < 4; ++g8)
+              gm[g8] = max(__vimax3_s32(v[g8 * 8], v[g8 * 8 + 1], v[g8 * 8 + 2]),
+                           __vimax3_s32(v[g8 * 8 + 3], v[g8 * 8 + 4], max(v[g8 * 8 + 5], max(v[g8 * 8 + 6], v[g8 * 8 + 7]))));
+            const int32_t cm = max(__vimax3_s32(gm[0], gm[1], gm[2]), gm[3]);
+            if (__any_sync(0xffffffffu, cm >= L)) {
 #pragma unroll
-            for (int g8 = 0; g8 < 4; ++g8) {
-              if (h & (1u << g8)) {  // some lane may have a passer in this group: test all 8 exactly
-                const int32_t* v = reinterpret_cast<const int32_t*>(a) + g8 * 8;
-                uint32_t bits = 0;
-                if (RAW) {
+              for (int g8 = 0; g8 < 4; ++g8) {
+                if (!__any_sync(0xffffffffu, gm[g8] >= L)) continue;
 #pragma unroll
-                  for (int jj = 0; jj < 8; ++jj) bits |= uint32_t(v[jj] >= L) << jj;
-                } else {  // exact fp32 test: fl(acc * scale) >= t  (hindexer.py:111)
-                  const float4 s0 = sc4[(j0 + g8 * 8) >> 2], s1 = sc4[((j0 + g8 * 8) >> 2) + 1];
-                  const float sv[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
-#pragma unroll
-                  for (int jj = 0; jj < 8; ++jj) bits |= uint32_t(__fmul_rn((float)v[jj], sv[jj]) >= tfe) << jj;
+                for (int jj = 0; jj < 8; ++jj) {
+                  const int32_t acc = v[g8 * 8 + jj];
+                  const int j = j0 + g8 * 8 + jj;
+                  if (acc >= L && j < nvalid) {
+                    float sv = 0.f;
+                    if (!RAW) sv = __fmul_rn((float)acc, sc[j]);
+                    if (RAW || sv >= tfe) {
+                      const uint32_t pos = atomicAdd(scnt + q, 1u);  // shared-memory counter
+                      if ((int64_t)pos < P.seg)
+                        dst[pos] = KEYS ? int32_t(RAW ? i32_key(acc) : f32_key(sv)) : pm[j];
+                    }
+                  }
                 }
-                m |= bits << (g8 * 8);
-              }
-            }
-            const int lim = nvalid - j0;  // valid columns in this chunk
-            if (lim < 32) m &= lim <= 0 ? 0u : ((1u << lim) - 1u);
-            mask[cc] = m;
-            if (KEYS && m && q < P.B) {  // append the passers' ascending score keys now (a[] is live)
-              uint32_t pos = atomicAdd(scnt + q, (uint32_t)__popc(m));
-              while (m) {
-                const int j = __ffs(m) - 1;
-                m &= m - 1;
-                uint32_t accv = 0;
-#pragma unroll
-                for (int jj = 0; jj < 32; ++jj) accv = (jj == j) ? a[jj] : accv;  // static register select
-                const int32_t acc = int32_t(accv);
-                const uint32_t key = RAW ? i32_key(acc) : f32_key(__fmul_rn((float)acc, sc[j0 + j]));
-                if ((int64_t)pos < P.seg) cand_cta[int64_t(q) * P.cap + pos] = int32_t(key);
-                ++pos;
-              }
-            }
-          }
-          const int total = __popc(mask[0]) + __popc(mask[1]);
-          if (!KEYS && total && q < P.B) {
-            uint32_t pos = atomicAdd(scnt + q, (uint32_t)total);  // shared-memory counter
-#pragma unroll
-            for (int cc = 0; cc < 2; ++cc) {
-              uint32_t m = mask[cc];
-              while (m) {
-                const int j = __ffs(m) - 1;
-                m &= m - 1;
-                if ((int64_t)pos < P.seg) cand_cta[int64_t(q) * P.cap + pos] = pm[cc * 32 + j];
-                ++pos;
               }
             }
           }
@@ -715,8 +690,9 @@ inline unsigned compact_split(const molr_ctx* ctx, int Bc, int G) {
 // ---------------------------------------------------------------------------------------------
 // Float view (MOLR_S1_FLOAT, hindexer.py:112 `view @ q` in fp32) on the tensor cores.
 //
-// The reference's float score is an fp32 dot; the product's fp32 definition is the sequential
-// fmaf chain of filter_scan_kernel / scan_scores_kernel (the sample threshold comes from it).
+// The reference's float score is an fp32 dot (NumPy/OpenBLAS); the product's fp32 definition is
+// s1_dot_f32 (common.cuh: OpenBLAS's summation order), used by filter_scan_kernel /
+// scan_scores_kernel and the exact re-check (the sample threshold comes from it).
 // Operands are fp16 after an exact power-of-two scaling (view: one global sv putting max|v| in
 // [2^14, 2^15); query: its own sq), so v = sv v' + dv with |dv| <= 2^-11 |v| + 2^-25 sv (the
 // second term for fp16 subnormals) and likewise for q.  With fp32 accumulation of the exact
@@ -1304,14 +1280,14 @@ __global__ void seg_max_kernel(int64_t n, const int32_t* __restrict__ cnt, int* 
   if ((threadIdx.x & 31) == 0 && m > 0) atomicMax(mx, m);
 }
 
-// exact fp32 re-score of the undecided band (the sequential fmaf chain of filter_scan_kernel);
+// exact fp32 re-score of the undecided band (the s1_dot64 order of filter_scan_kernel);
 // passers are appended after the query's certain passers (counts[b] = running total)
 __global__ void __launch_bounds__(256) recheck_band_kernel(int G, int64_t seg, int64_t cap_in, const int32_t* __restrict__ band,
                                                            const int32_t* __restrict__ bcnt, const float* __restrict__ vf,
                                                            const float* __restrict__ qf, const uint32_t* __restrict__ tkeys,
                                                            int strict, int64_t cap_out, int32_t* __restrict__ cand,
                                                            int64_t* __restrict__ counts) {
-  __shared__ float sq[64];
+  __shared__ __align__(16) float sq[64];
   const int b = blockIdx.x;
   if (threadIdx.x < 64) sq[threadIdx.x] = qf[int64_t(b) * 64 + threadIdx.x];
   __syncthreads();
@@ -1321,17 +1297,14 @@ __global__ void __launch_bounds__(256) recheck_band_kernel(int G, int64_t seg, i
     const int32_t* src = band + int64_t(b) * cap_in + int64_t(g) * seg;
     for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
       const int32_t r = src[i];
-      const float4* v = reinterpret_cast<const float4*>(vf + int64_t(r) * 64);
-      float acc = 0.f;
+      const float4* v4 = reinterpret_cast<const float4*>(vf + int64_t(r) * 64);
+      float v[64];
 #pragma unroll
       for (int k = 0; k < 16; ++k) {
-        const float4 x = __ldg(v + k);
-        acc = fmaf(x.x, sq[4 * k], acc);
-        acc = fmaf(x.y, sq[4 * k + 1], acc);
-        acc = fmaf(x.z, sq[4 * k + 2], acc);
-        acc = fmaf(x.w, sq[4 * k + 3], acc);
+        const float4 x = __ldg(v4 + k);
+        v[4 * k] = x.x, v[4 * k + 1] = x.y, v[4 * k + 2] = x.z, v[4 * k + 3] = x.w;
       }
-      const uint32_t key = f32_key(acc);
+      const uint32_t key = f32_key(s1_dot64(v, sq));
       if (strict ? key > tk : key >= tk) {
         const int64_t pos = (int64_t)atomicAdd(reinterpret_cast<unsigned long long*>(counts + b), 1ull);
         if (pos < cap_out) cand[int64_t(b) * cap_out + pos] = r;
@@ -1586,23 +1559,20 @@ int s1_f16_image(molr_ctx* ctx, const molr_cache* cc, const int64_t* rows, int64
 // keys[b, j] = f32_key(exact fp32 score of row rows_f32[ids[b, j]]) for the j < min(counts[b], cap)
 __global__ void passer_keys_kernel(int B, int64_t cap, const int32_t* __restrict__ ids, const int64_t* __restrict__ counts,
                                    const float* __restrict__ vf, const float* __restrict__ qf, uint32_t* __restrict__ keys) {
-  __shared__ float sq[64];
+  __shared__ __align__(16) float sq[64];
   const int b = blockIdx.x;
   if (threadIdx.x < 64) sq[threadIdx.x] = qf[int64_t(b) * 64 + threadIdx.x];
   __syncthreads();
   const int64_t n = imin64(counts[b], cap);
   for (int64_t i = blockIdx.y * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.y * blockDim.x) {
-    const float4* v = reinterpret_cast<const float4*>(vf + int64_t(ids[int64_t(b) * cap + i]) * 64);
-    float acc = 0.f;
+    const float4* v4 = reinterpret_cast<const float4*>(vf + int64_t(ids[int64_t(b) * cap + i]) * 64);
+    float v[64];
 #pragma unroll
     for (int k = 0; k < 16; ++k) {
-      const float4 x = __ldg(v + k);
-      acc = fmaf(x.x, sq[4 * k], acc);
-      acc = fmaf(x.y, sq[4 * k + 1], acc);
-      acc = fmaf(x.z, sq[4 * k + 2], acc);
-      acc = fmaf(x.w, sq[4 * k + 3], acc);
+      const float4 x = __ldg(v4 + k);
+      v[4 * k] = x.x, v[4 * k + 1] = x.y, v[4 * k + 2] = x.z, v[4 * k + 3] = x.w;
     }
-    keys[int64_t(b) * cap + i] = f32_key(acc);
+    keys[int64_t(b) * cap + i] = f32_key(s1_dot64(v, sq));
   }
 }
 
