@@ -291,6 +291,157 @@ def cpu_baseline(cfg, reps=2, procs=None, X1=1_000_000):
 
 
 # ------------------------------------------------------------------------------------------
+# CPU baseline: the UNMODIFIED reference package (baseline/_ref, tools/install_reference.sh) on
+# the host cores, on the same corpus and queries, measured (not extrapolated)
+# ------------------------------------------------------------------------------------------
+def _reference_package():
+    p = os.path.join(ROOT, "baseline", "_ref")
+    if os.path.isdir(os.path.join(p, "molr")) and p not in sys.path:
+        sys.path.insert(0, p)
+    try:
+        import molr.hindexer  # noqa: F401
+        import molr.mol  # noqa: F401
+        import molr.numerics  # noqa: F401
+        import molr.quant  # noqa: F401
+        return sys.modules["molr"]
+    except ImportError:
+        return None
+
+
+_REF = {}
+
+
+def _ref_query(i):
+    """One query through the reference's own functions in a forked worker (numpy on one thread):
+    stage 1 = molr.hindexer.h_indexer over the whole int8 view (hindexer.py:135-163, incl. the
+    rng.permutation and the int32 mat-vec), stage 2 = molr.mol.mol_top_k over the candidates
+    (mol.py:389-408); the exact path = mol_top_k over the whole corpus (engine.py:140-147)."""
+    from threadpoolctl import threadpool_limits
+
+    import molr.hindexer as RH
+    import molr.mol as RM
+    import molr.numerics as RN
+
+    st = _REF
+    u = st["users"][i]
+    state = RM.QueryState(user_embs=st["ue"][u], gate_features=st["feats"][u])
+    with threadpool_limits(1):
+        t0 = time.perf_counter()
+        if st["exact"]:
+            ids, sc = RM.mol_top_k(st["cache"], st["gating"], np.arange(st["X"]), state, st["k"])
+            t1 = t2 = time.perf_counter()
+            same_cand = True
+        else:
+            cand = RH.h_indexer(st["view"], st["ue"][u].mean(axis=0), st["hcfg"], RN.make_rng([9000, int(u)])).indices
+            t1 = time.perf_counter()
+            sub = st["sub"][i]  # the candidates' cache rows (pre-gathered from the device cache)
+            same_cand = cand.size == sub[2].size and bool(np.array_equal(cand, sub[2]))
+            pos, sc = RM.mol_top_k(sub[0], st["gating"], np.arange(cand.size), state, min(st["k"], cand.size))
+            ids = sub[2][pos]
+            t2 = time.perf_counter()
+    return t1 - t0, t2 - t1, same_cand, ids, sc
+
+
+def reference_baseline(cfg, model, cache, ue, feats, *, budget_s=30.0, ours=None):
+    """Time the unmodified reference package on the host cores (one forked process per query, up
+    to the cores / memory allow), on the bench's corpus (read back from the device cache,
+    exactly) and queries.  `ours(u)` returns the product's drop-in result for query u on the GPU —
+    (candidates of paper_2306_04039_b200.hindexer.h_indexer with the reference's rng, ids and
+    scores of its mol_top_k) — used to pre-gather stage 2's rows and compared with the reference's
+    candidates (bit-identical expected) and top-k."""
+    import multiprocessing as mp
+
+    molr = _reference_package()
+    if molr is None:
+        return None
+    import molr.hindexer as RH
+    import molr.mol as RM
+    import molr.quant as RQ
+
+    exact = cfg.get("exact", False)
+    X, k = cfg["X"], cfg["k"]
+    mcfg = RM.MoLConfig(k_u=K_U, k_x=K_X, d=D, tau=TAU, gating_hidden=H, dropout_p=0.0)
+    gating = RM.GatingNetwork(RM.Mlp(*model["user_net"]), RM.Mlp(*model["item_net"]), RM.Mlp(*model["cross_net"]))
+    cores = len(os.sched_getaffinity(0))
+    try:
+        avail = os.sysconf("SC_AVPHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
+    except (ValueError, OSError):
+        avail = 64 << 30
+    st = {"ue": ue, "feats": feats, "gating": gating, "X": X, "k": k, "exact": exact}
+    t_prep = time.perf_counter()
+    if exact:
+        embs, gp = cache.read(0, X)
+        st["cache"] = RM.ItemCache(config=mcfg, item_embs=embs, item_gate_pre=gp, stage1_embs=embs.mean(axis=1))
+        per_proc = (256 << 20) + X * 4 * 64 * 6
+    else:
+        codes = np.empty((X, D), dtype=np.int8)
+        scales = np.empty(X, dtype=np.float32)
+        step = 1 << 22
+        for lo in range(0, X, step):
+            n = min(step, X - lo)
+            cache.read_stage1(lo, n, codes[lo:lo + n], scales[lo:lo + n])
+        st["view"] = RQ.QuantizedRows(codes=codes, scales=scales)
+        st["hcfg"] = RH.HIndexerConfig(k_prime=cfg["k_prime"], sample_ratio=cfg["ratio"], quantized=True)
+        # int8_matvec materialises the int32 codes (quant.py:90) + permutation + scores per process
+        per_proc = X * (D * 4 + 8 + 4 + 4) + (1 << 30)
+    procs = max(1, min(cores, int((avail - (4 << 30)) // per_proc)))
+    # one calibration query in the parent sizes the sample to ~budget_s of wall time
+    st["users"] = [0]
+    if not exact:
+        st["sub"] = {}
+    _REF.clear()
+    _REF.update(st)
+    if not exact:
+        _REF["sub"][0] = _sub_cache(RM, mcfg, cache, ours, st, 0)
+    t_one = sum(_ref_query(0)[:2])
+    nq = procs * max(1, int(budget_s / max(t_one, 1e-3)))
+    nq = min(nq, ue.shape[0]) if exact else min(procs, ue.shape[0])
+    users = list(range(nq))
+    _REF["users"] = users
+    if not exact:
+        for i in range(1, nq):
+            _REF["sub"][i] = _sub_cache(RM, mcfg, cache, ours, st, i)
+    t_prep = time.perf_counter() - t_prep
+    t0 = time.perf_counter()
+    with mp.get_context("fork").Pool(min(procs, nq)) as pool:
+        res = pool.map(_ref_query, range(nq), chunksize=max(1, nq // (4 * procs)))
+    wall = time.perf_counter() - t0
+    t1 = [r[0] for r in res]
+    tq = [r[0] + r[1] for r in res]
+    out = {"value": nq / wall, "unit": "queries/s", "cores": min(procs, nq), "kind": "reference",
+           "s_per_query_per_core": float(np.median(tq)), "p50_query_s": float(np.median(tq)),
+           "stage1_s": float(np.median(t1)), "queries": nq, "wall_s": round(wall, 2), "prep_s": round(t_prep, 1),
+           "candidates_identical_to_dropin": None if exact else all(r[2] for r in res)}
+    what = (f"exact mol_top_k over all {X:,} items" if exact else
+            f"h_indexer (int8 view, {X:,} rows incl. rng.permutation + int32 mat-vec) + mol_top_k over its "
+            f"~{cfg['k_prime']:,} candidates")
+    out["sample"] = (f"unmodified reference package (baseline/_ref molr) on {out['cores']} processes x 1 thread: "
+                     f"{nq} queries, {what}; {out['p50_query_s']:.2f} s per query, wall {wall:.1f} s")
+    if not exact:
+        same, ov = 0, []
+        for i in range(nq):
+            oi, ri = _REF["sub"][i][1], res[i][3]
+            same += int(oi.tolist() == ri.tolist())
+            ov.append(len(set(oi.tolist()) & set(ri.tolist())) / len(ri))
+        out["dropin_topk_identical_to_reference"] = same
+        out["dropin_topk_overlap_min"] = float(min(ov))
+    return out
+
+
+def _sub_cache(RM, mcfg, cache, ours, st, i):
+    """The candidate rows of query i (the drop-in h_indexer on the GPU gives the reference's exact
+    candidate set for the same rng) as a reference ItemCache: stage 2's input, gathered outside
+    the timed region."""
+    from paper_2306_04039_b200.hindexer import index_select
+
+    cand, top_ids, _ = ours(i)
+    sub = index_select(cache, cand)
+    rc = RM.ItemCache(config=mcfg, item_embs=np.array(sub.item_embs), item_gate_pre=np.array(sub.item_gate_pre),
+                      stage1_embs=np.array(sub.stage1_embs))
+    return rc, top_ids, cand
+
+
+# ------------------------------------------------------------------------------------------
 # parity against the CPU oracle at the bench's own config (outside the timed region)
 # ------------------------------------------------------------------------------------------
 def oracle_parity(cfg, model, cache, ue, feats, ids, scores, q_exact, q_scores=8):
@@ -375,15 +526,18 @@ def main():
     if args.items:
         cfg["X"] = args.items
         cfg["label"] += f" (items={args.items})"
-    if args.impl == "reference":
-        return run_reference(args, cfg)
+    ref_arm = args.impl == "reference"
+    if ref_arm and int(os.environ.get("RANK", "0")) != 0:
+        return  # the reference arm runs on rank 0 alone (host cores), the other ranks exit 0
+    if ref_arm and _reference_package() is None:
+        return run_reference(args, cfg)  # no baseline/_ref install: the oracle port (kind "port")
 
     import torch
     import torch.distributed as dist
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    world = 1 if ref_arm else int(os.environ.get("WORLD_SIZE", "1"))
+    rank = 0 if ref_arm else int(os.environ.get("RANK", "0"))
+    local = 0 if ref_arm else int(os.environ.get("LOCAL_RANK", "0"))
     # MOLR_BENCH_SHARE_GPU=1 (testing the sharded path on a 1-GPU box): every rank on cuda:0 and
     # gloo for the (tiny) candidate exchange, since NCCL refuses two ranks on one device
     share = os.environ.get("MOLR_BENCH_SHARE_GPU") == "1"
@@ -452,6 +606,43 @@ def main():
         cnt_t = torch.empty((B,), dtype=torch.int64, device=dev)
     stream = torch.cuda.current_stream()
     sp = stream.cuda_stream
+
+    def ours_dropin(view_holder):
+        """The product's drop-in per-query path for query u of the batch (GPU): h_indexer with the
+        reference's rng (make_rng([9000, u])) on the host int8 view, then mol_top_k."""
+        from paper_2306_04039_b200.hindexer import HIndexerConfig as OH
+        from paper_2306_04039_b200.hindexer import h_indexer as oh
+        from paper_2306_04039_b200.mol import QueryState, mol_top_k
+        from paper_2306_04039_b200.numerics import make_rng
+
+        hc = OH(k_prime=cfg["k_prime"], sample_ratio=cfg["ratio"], quantized=True)
+
+        def run(u):
+            cand = oh(view_holder["view"], ref_ue[u].mean(axis=0), hc, make_rng([9000, int(u)])).indices
+            ids, sc = mol_top_k(cache, gating, cand, QueryState(user_embs=ref_ue[u], gate_features=feats_h[u]), k)
+            return cand, ids, sc
+        return run
+
+    if ref_arm:
+        L.call("molr_query_prep", ctx, B, D_U, feats_d.data_ptr(), PROJ_H, up1.data_ptr(), upb1.data_ptr(),
+               up2.data_ptr(), K_U, D, 1, H, uw1.data_ptr(), ub1.data_ptr(), uw2.data_ptr(), G, float(DEFAULT_EPS),
+               ue_d.data_ptr(), uw_d.data_ptr(), sp)
+        torch.cuda.synchronize()
+        ref_ue = ue_d.cpu().numpy()
+        cb = reference_baseline(cfg, model, cache, ref_ue, feats_h, ours=ours_dropin(_REF))
+        line = {"metric": metric_name(args.config, cfg), "impl": "reference",
+                "value": cb["value"], "unit": "queries/s", "n_gpus": args.gpus, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": 1e3 * B / cb["value"],
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "dtype": "f32 NumPy (int8 stage-1 view, int32 accumulate)",
+                "data": "synthetic: the bench's corpus and queries, read back exactly from the device cache",
+                "config": {"workload": cfg["label"], "items": cfg["X"], "batch": cfg["B"], "k": cfg["k"],
+                           "k_prime": cfg["k_prime"], "sample_ratio": cfg["ratio"]},
+                "cpu_baseline": {k2: cb[k2] for k2 in ("value", "unit", "cores", "kind", "sample")},
+                "reference_run": cb,
+                "e2e": {"value": cb["value"], "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
 
     def step(i, feats_ptr, host_out=None):
         """One batch through the C-ABI, from the users' raw features (the query a user makes,
@@ -735,7 +926,12 @@ def main():
         "metric": metric, "value": value, "unit": "queries/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": "bf16+f32 (fp32 accumulate)" if f32_view else "bf16+int8 (fp32 accumulate)",
+        # the arithmetic the path computes in (K1/K2): stage 1 int8 x int8 -> int32 (exact) or the
+        # fp16 pre-test + exact fp32 re-check; MoL: bf16 item components x (bf16 hi + lo) query split with
+        # fp32 accumulate, cross-net layer 1 bf16 (hi/lo bias), layer 2 fp16, SiLU via tanh.approx,
+        # combine / softmax / gated sum in fp32
+        "dtype": ("stage1 " + ("fp16 pre-test + fp32 exact re-check" if f32_view else "int8 (int32 acc, exact)")
+                  + "; MoL bf16 x bf16-hi/lo (fp32 acc), cross-net L1 bf16 / L2 fp16, tanh.approx SiLU, fp32 softmax"),
         "data": "synthetic (reference init convention model.py:121-163; bf16-representable item cache built on device)",
         "config": {"workload": cfg["label"], "items": X, "items_per_gpu": Xl, "batch": B, "k": k,
                    "k_prime": cfg["k_prime"], "k_prime_per_gpu": kp_local, "sample_ratio": cfg["ratio"],
@@ -759,8 +955,15 @@ def main():
     line["clocks"] = clk.summary()
     if not args.no_cpu and world == 1:  # the host baseline is timed on rank 0 at N=1 only
         try:
-            cb = cpu_baseline(cfg)
+            ref_ue = ue_d.cpu().numpy()
+            cb = None
+            if not f32_view:  # the unmodified reference package when installed (baseline/_ref)
+                cb = reference_baseline(cfg, model, cache, ref_ue, feats_h, ours=ours_dropin(_REF))
+            if cb is None:  # else the oracle port, extrapolated
+                cb = cpu_baseline(cfg)
             line["cpu_baseline"] = {k2: cb[k2] for k2 in ("value", "unit", "cores", "kind", "sample")}
+            if cb.get("kind") == "reference":
+                line["cpu_baseline"]["reference_run"] = {k2: v for k2, v in cb.items() if k2 not in line["cpu_baseline"]}
         except Exception as e:  # keep the GPU line even if the host run fails
             line["cpu_baseline"] = {"value": None, "error": repr(e)}
     print(json.dumps(line), flush=True)

@@ -1,11 +1,34 @@
 // C-ABI plumbing: contexts, the immutable device ItemCache (mol.py:216-291) and gating weights.
 #include <mutex>
+#include <vector>
 
 #include "common.cuh"
 #include "stage1.cuh"
 
 namespace molr {
 thread_local molr_arena* tl_arena = nullptr;
+
+namespace {
+struct ThreadStreams {
+  std::vector<std::pair<const molr_ctx*, cudaStream_t>> v;
+  ~ThreadStreams() {
+    for (auto& e : v) cudaStreamDestroy(e.second);  // (errors at process teardown are moot)
+  }
+};
+thread_local ThreadStreams tl_streams;
+}  // namespace
+
+cudaStream_t thread_stream(molr_ctx* ctx) {
+  for (auto& e : tl_streams.v)
+    if (e.first == ctx) return e.second;
+  cudaStream_t st = nullptr;
+  if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) {
+    cudaGetLastError();
+    return ctx->stream;
+  }
+  tl_streams.v.emplace_back(ctx, st);
+  return st;
+}
 
 static thread_local std::string g_last_error;
 void set_error(const std::string& msg) { g_last_error = msg; }
@@ -456,7 +479,7 @@ int molr_cache_create(molr_ctx* ctx, int64_t X, int k_x, int d, int G, const flo
                       const float* scales, molr_cache** out) {
   if (!ctx || !out || !embs || !gp) MOLR_FAIL(MOLR_ERR_INVALID, "null argument");
   MOLR_CUDA(cudaSetDevice(ctx->device));
-  cudaStream_t s = ctx->stream;
+  cudaStream_t s = pick_stream(ctx, nullptr);
   bool e_exact = false, g_exact = false;
   MOLR_TRY(probe_bf16(ctx, embs, X * k_x * d, s, &e_exact));
   MOLR_TRY(probe_bf16(ctx, gp, X * G, s, &g_exact));

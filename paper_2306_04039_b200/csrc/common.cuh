@@ -138,12 +138,18 @@ struct KTimer {
     }
     cudaEventRecord(a, s);
   }
+  // end of the timed launches; `work` may still be set afterwards (e.g. once counts are known)
+  void stop() {
+    if (a && !stopped) cudaEventRecord(b, s);
+    stopped = true;
+  }
   ~KTimer() {
     if (!a) return;
-    cudaEventRecord(b, s);
+    stop();
     std::lock_guard<std::mutex> g(ctx->prof_mu);
     ctx->prof_pending.push_back({name, a, b, work});
   }
+  bool stopped = false;
 };
 }  // namespace molr
 
@@ -199,11 +205,16 @@ struct molr_gating {
 
 namespace molr {
 
+// The calling thread's own non-blocking stream on ctx's device (created on first use, destroyed
+// at thread exit): calls that pass no stream from different threads run concurrently instead of
+// serialising on one shared stream (engine.py:6: "any number of threads, no locks").
+cudaStream_t thread_stream(molr_ctx* ctx);
+
 // Every entry point resolves its stream first; clearing any stale non-sticky launch error here
 // keeps it from being attributed to this call's launches.
 inline cudaStream_t pick_stream(molr_ctx* ctx, void* s) {
   cudaGetLastError();
-  return s ? reinterpret_cast<cudaStream_t>(s) : ctx->stream;
+  return s ? reinterpret_cast<cudaStream_t>(s) : thread_stream(ctx);
 }
 
 // True if the kernel can dereference p directly (device or managed memory).

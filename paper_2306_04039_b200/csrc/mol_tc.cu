@@ -697,9 +697,9 @@ int mol_score_tc(molr_ctx* ctx, const molr_cache* c, const molr_gating* g, int B
   MOLR_TRY(pre.alloc(size_t(B + 1) * 8, s));
   tile_prefix_kernel<<<1, 1024, 0, s>>>(B, segs.begin, segs.end, segs.X, tc::TILE, pre.as<int64_t>());
   MOLR_LAUNCHED(ctx);
-  int64_t T = 0;
-  MOLR_CUDA(cudaMemcpyAsync(&T, pre.as<int64_t>() + B, 8, cudaMemcpyDeviceToHost, s));
-  MOLR_CUDA(cudaStreamSynchronize(s));
+  // the persistent kernel reads the tile count from pre[B] itself (no host round trip); the grid
+  // is one CTA per SM unless the (dense) tile count is known to be smaller
+  const int64_t T = segs.begin ? int64_t(ctx->num_sms) : int64_t(B) * ((segs.X + tc::TILE - 1) / tc::TILE);
   if (T == 0) return MOLR_OK;
   Scratch b0;
   MOLR_TRY(b0.alloc(size_t(B) * 2048, s));

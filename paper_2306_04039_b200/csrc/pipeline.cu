@@ -167,13 +167,18 @@ __global__ void gather_codes_kernel(const int8_t* __restrict__ src, const float*
 //   3. the n_rank-th largest passer key IS the n_rank-th largest sampled score whenever at least
 //      n_rank rows passed (every row >= t passes); otherwise (or on capacity overflow) fall back to
 //      scoring the full sample.  Exact in every case.
+//
+// With `fail` (device int) the pilot's outcome is not read back: the pilot threshold is used and a
+// failed pilot (fewer than n_rank passers, or key-buffer / segment overflow) only sets *fail, which
+// the caller checks after its end-of-call synchronisation and reruns with force_full.
 int sample_threshold_tc(molr_ctx* ctx, int mode, const int8_t* scodes, const float* sscales, int64_t lam, int B,
-                        const int8_t* qc, int64_t n_rank, Scratch& ss, uint32_t* tkey, cudaStream_t s) {
+                        const int8_t* qc, int64_t n_rank, Scratch& ss, uint32_t* tkey, cudaStream_t s,
+                        bool force_full = false, int* fail = nullptr, const S1Deferred* defer = nullptr) {
   const bool raw = mode == MOLR_S1_INT8_RAW;
   const double p = double(n_rank) / double(lam);
   int64_t lam0 = (int64_t)std::ceil(16.0 / p);
   lam0 = (lam0 + 255) / 256 * 256;
-  if (!dev_knob("MOLR_NO_PILOT") && lam0 * 4 <= lam) {
+  if (!force_full && !dev_knob("MOLR_NO_PILOT") && lam0 * 4 <= lam) {
     const double mu = double(lam0) * p;
     int64_t n0 = std::min<int64_t>(lam0, (int64_t)std::ceil(mu + 6.0 * std::sqrt(mu) + 16.0));
     if (const char* e = dev_knob("MOLR_PILOT_N0")) n0 = std::max<int64_t>(1, std::min<int64_t>(lam0, atoll(e)));  // tests
@@ -197,15 +202,16 @@ int sample_threshold_tc(molr_ctx* ctx, int mode, const int8_t* scodes, const flo
       MOLR_CUDA(cudaMemsetAsync(counts.p, 0, size_t(B) * 8, s));
       MOLR_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int) * 2, s));
       MOLR_TRY(s1_tc_scan(ctx, mode, scodes, sscales, mm.as<float2>(), nullptr, lam, B, qc, t0.as<uint32_t>(), 0, cap,
-                          keys.as<int32_t>(), counts.as<int64_t>(), nullptr, 0, s, /*emit_keys=*/true));
+                          keys.as<int32_t>(), counts.as<int64_t>(), nullptr, 0, s, /*emit_keys=*/true, defer));
     }
+    int* fl = fail ? fail : flag.as<int>();
     {
       KTimer t(ctx, "select_nth", s, double(B) * expect);
-      MOLR_TRY(nth_largest_keys(ctx, B, cap, keys.as<uint32_t>(), counts.as<int64_t>(), n_rank, tkey,
-                                flag.as<int>(), s));
-      max_count_kernel<<<div_up(B, 256), 256, 0, s>>>(B, counts.as<int64_t>(), cap, flag.as<int>());
+      MOLR_TRY(nth_largest_keys(ctx, B, cap, keys.as<uint32_t>(), counts.as<int64_t>(), n_rank, tkey, fl, s));
+      max_count_kernel<<<div_up(B, 256), 256, 0, s>>>(B, counts.as<int64_t>(), cap, fl);
       MOLR_LAUNCHED(ctx);
     }
+    if (fail) return MOLR_OK;  // checked after the caller's end-of-call synchronisation
     int hf = 0;
     MOLR_CUDA(cudaMemcpyAsync(&hf, flag.p, sizeof(int), cudaMemcpyDeviceToHost, s));
     MOLR_CUDA(cudaStreamSynchronize(s));
@@ -524,7 +530,7 @@ int molr_mol_top_k(molr_ctx* ctx, const molr_cache* c, const molr_gating* g, int
 int molr_index_select(molr_ctx* ctx, const molr_cache* c, int64_t n, const int64_t* ids, molr_cache** out) {
   if (!ctx || !c || !out) MOLR_FAIL(MOLR_ERR_INVALID, "null argument");
   MOLR_CUDA(cudaSetDevice(ctx->device));
-  cudaStream_t s = ctx->stream;
+  cudaStream_t s = pick_stream(ctx, nullptr);
   if (c->s1_codes) MOLR_TRY(s1_seal(const_cast<molr_cache*>(c), s));
   molr_cache* r = nullptr;
   MOLR_TRY(molr_cache_alloc(ctx, n, c->k_x, c->d, c->G, c->d1, c->storage, &r));
@@ -620,55 +626,68 @@ static int two_stage_impl(molr_ctx* ctx, const molr_cache* c, const molr_gating*
       MOLR_TRY(qs.alloc(size_t(B) * 4, s));
       MOLR_TRY(prepare_queries(ctx, mode, B, c->d1, q.as<float>(), qc.as<int8_t>(), qs.as<float>(), s));
     }
-    Scratch ss, tkey;
-    MOLR_TRY(tkey.alloc(size_t(B) * 4, s));
-    if (tkeys_in) {
-      MOLR_CUDA(cudaMemcpyAsync(tkey.p, tkeys_in, size_t(B) * 4, cudaMemcpyDefault, s));
-    } else {
-    // 2. sample
-    int bits = 2;
-    while ((int64_t(1) << bits) < X) bits += 2;
-    Scratch samp;
-    MOLR_TRY(samp.alloc(size_t(lam) * 8, s));
-    feistel_sample_kernel<<<std::min(div_up(lam, 256), ctx->num_sms * 8), 256, 0, s>>>(X, lam, seed, bits / 2,
-                                                                                       samp.as<int64_t>());
-    MOLR_LAUNCHED(ctx);
-    // 3. sample scores [B][lam] then n-th largest per query
-    const double nr = std::nearbyint(double(k_prime * lam) / double(X));  // Python round(): half-even
-    const int64_t n_rank = std::max<int64_t>(1, (int64_t)nr);
+    // 2-6 run as one stream of launches with no host round trip: the pilot's outcome, the
+    // filter's per-CTA segment and per-query capacity overflows are recorded on the device and
+    // checked once after the call's single synchronisation; the (rare) overflow reruns 2-6 with
+    // the exact sizes.
     const bool use_tc = s1_tc_supported(c, mode);
-    if (use_tc) {
-      // gather the sample rows into a contiguous operand, then the tensor-core scan writes scores
-      const int64_t lp = (lam + 255) / 256 * 256;
-      Scratch scodes, sscales;
-      MOLR_TRY(scodes.alloc(size_t(lp) * 64, s));
-      MOLR_TRY(sscales.alloc(size_t(lp) * 4, s));
-      MOLR_CUDA(cudaMemsetAsync(scodes.p, 0, size_t(lp) * 64, s));
-      MOLR_CUDA(cudaMemsetAsync(sscales.p, 0, size_t(lp) * 4, s));
-      gather_sample_kernel<<<std::min(div_up(lam * 4, 256), ctx->num_sms * 8), 256, 0, s>>>(
-          c->s1_codes, c->s1_scales, c->s1_inv, samp.as<int64_t>(), lam, scodes.as<int8_t>(), sscales.as<float>());
-      MOLR_LAUNCHED(ctx);
-      MOLR_TRY(sample_threshold_tc(ctx, mode, scodes.as<int8_t>(), sscales.as<float>(), lam, B, qc.as<int8_t>(),
-                                   n_rank, ss, tkey.as<uint32_t>(), s));
-    } else if (mode == MOLR_S1_FLOAT) {
-      MOLR_TRY(sample_threshold_f32(ctx, c, samp.as<int64_t>(), lam, B, q.as<float>(), n_rank, ss, tkey.as<uint32_t>(), s));
-    } else {
-      MOLR_TRY(ss.alloc(size_t(B) * lam * 4, s));
-      KTimer t(ctx, "stage1_sample_scan", s, double(B) * lam);
-      MOLR_TRY(scan_scores(ctx, mode, lam, c->d1, c->s1_f32, c->s1_codes, s1_interleaved(c->d1), c->s1_inv, c->s1_scales,
-                           samp.as<int64_t>(), B, q.as<float>(), qc.as<int8_t>(), ss.p, lam, s));
-    }
-    if (!use_tc && mode != MOLR_S1_FLOAT) {
-      KTimer t(ctx, "select_nth", s, double(B) * lam);
-      MOLR_TRY(nth_largest_rows(ctx, B, lam, ss.p, mode == MOLR_S1_INT8_RAW, lam, nullptr, 0, n_rank,
-                                tkey.as<uint32_t>(), s));
-    }
-    }  // thresholds
-    const bool use_tc = s1_tc_supported(c, mode);
-    // 4. filter scan with capacity; retry once with the exact maximum if it overflowed
     int64_t cap = imin64(X, k_prime + k_prime / 4 + 1024);
+    bool full_sample = false;
+    int64_t seg_min_pilot = 0, seg_min_main = 0;
     MOLR_TRY(counts.alloc(size_t(B) * 8, s));
-    for (int attempt = 0; attempt < 2; ++attempt) {
+    Scratch dflags;  // [0] pilot failed  [1] pilot key-scan segment need  [2] filter segment need
+    MOLR_TRY(dflags.alloc(16, s));
+    int hfl[4] = {0, 0, 0, 0};
+    for (int attempt = 0; attempt < 4; ++attempt) {
+      MOLR_CUDA(cudaMemsetAsync(dflags.p, 0, 16, s));
+      int64_t seg_used_pilot = 0, seg_used_main = 0;
+      const S1Deferred dpilot{dflags.as<int>() + 1, seg_min_pilot, &seg_used_pilot};
+      const S1Deferred dmain{dflags.as<int>() + 2, seg_min_main, &seg_used_main};
+      Scratch ss, tkey;
+      MOLR_TRY(tkey.alloc(size_t(B) * 4, s));
+      if (tkeys_in) {
+        MOLR_CUDA(cudaMemcpyAsync(tkey.p, tkeys_in, size_t(B) * 4, cudaMemcpyDefault, s));
+      } else {
+        // 2. sample
+        int bits = 2;
+        while ((int64_t(1) << bits) < X) bits += 2;
+        Scratch samp;
+        MOLR_TRY(samp.alloc(size_t(lam) * 8, s));
+        feistel_sample_kernel<<<std::min(div_up(lam, 256), ctx->num_sms * 8), 256, 0, s>>>(X, lam, seed, bits / 2,
+                                                                                           samp.as<int64_t>());
+        MOLR_LAUNCHED(ctx);
+        // 3. n-th largest sampled score per query
+        const double nr = std::nearbyint(double(k_prime * lam) / double(X));  // Python round(): half-even
+        const int64_t n_rank = std::max<int64_t>(1, (int64_t)nr);
+        if (use_tc) {
+          // gather the sample rows into a contiguous operand, then the tensor-core scans
+          const int64_t lp = (lam + 255) / 256 * 256;
+          Scratch scodes, sscales;
+          MOLR_TRY(scodes.alloc(size_t(lp) * 64, s));
+          MOLR_TRY(sscales.alloc(size_t(lp) * 4, s));
+          MOLR_CUDA(cudaMemsetAsync(scodes.p, 0, size_t(lp) * 64, s));
+          MOLR_CUDA(cudaMemsetAsync(sscales.p, 0, size_t(lp) * 4, s));
+          gather_sample_kernel<<<std::min(div_up(lam * 4, 256), ctx->num_sms * 8), 256, 0, s>>>(
+              c->s1_codes, c->s1_scales, c->s1_inv, samp.as<int64_t>(), lam, scodes.as<int8_t>(), sscales.as<float>());
+          MOLR_LAUNCHED(ctx);
+          MOLR_TRY(sample_threshold_tc(ctx, mode, scodes.as<int8_t>(), sscales.as<float>(), lam, B, qc.as<int8_t>(),
+                                       n_rank, ss, tkey.as<uint32_t>(), s, full_sample, dflags.as<int>(), &dpilot));
+        } else if (mode == MOLR_S1_FLOAT) {
+          MOLR_TRY(sample_threshold_f32(ctx, c, samp.as<int64_t>(), lam, B, q.as<float>(), n_rank, ss,
+                                        tkey.as<uint32_t>(), s));
+        } else {
+          MOLR_TRY(ss.alloc(size_t(B) * lam * 4, s));
+          {
+            KTimer t(ctx, "stage1_sample_scan", s, double(B) * lam);
+            MOLR_TRY(scan_scores(ctx, mode, lam, c->d1, c->s1_f32, c->s1_codes, s1_interleaved(c->d1), c->s1_inv,
+                                 c->s1_scales, samp.as<int64_t>(), B, q.as<float>(), qc.as<int8_t>(), ss.p, lam, s));
+          }
+          KTimer t(ctx, "select_nth", s, double(B) * lam);
+          MOLR_TRY(nth_largest_rows(ctx, B, lam, ss.p, mode == MOLR_S1_INT8_RAW, lam, nullptr, 0, n_rank,
+                                    tkey.as<uint32_t>(), s));
+        }
+      }
+      // 4. filter scan with capacity (overflow: rerun with the exact maximum)
       MOLR_TRY(cand.alloc(size_t(B) * cap * 4, s));
       MOLR_CUDA(cudaMemsetAsync(counts.p, 0, size_t(B) * 8, s));
       const int per_q = mode == MOLR_S1_FLOAT ? c->d1 * 4 : c->d1;
@@ -694,47 +713,66 @@ static int two_stage_impl(molr_ctx* ctx, const molr_cache* c, const molr_gating*
         KTimer t(ctx, "stage1_filter_tc", s, double(B) * X);
         MOLR_TRY(s1_tc_scan(ctx, mode, c->s1_codes, c->s1_scales, c->s1_chunk_mm, c->s1_perm, X, B, qc.as<int8_t>(),
                             tkey.as<uint32_t>(), comparator == MOLR_STRICT, cap, cand.as<int32_t>(), counts.as<int64_t>(),
-                            nullptr, 0, s));
+                            nullptr, 0, s, false, &dmain));
       } else {
         KTimer t(ctx, "stage1_filter_scan", s, double(B) * X);
         if (mode == MOLR_S1_FLOAT) MOLR_TRY(launch(filter_scan_kernel<MOLR_S1_FLOAT>));
         else if (mode == MOLR_S1_INT8) MOLR_TRY(launch(filter_scan_kernel<MOLR_S1_INT8>));
         else MOLR_TRY(launch(filter_scan_kernel<MOLR_S1_INT8_RAW>));
       }
+      MOLR_TRY(sb.alloc(size_t(B) * 8, s));
+      MOLR_TRY(se.alloc(size_t(B) * 8, s));
+      cap_segs_kernel<<<div_up(B, 256), 256, 0, s>>>(B, cap, counts.as<int64_t>(), sb.as<int64_t>(), se.as<int64_t>());
+      MOLR_LAUNCHED(ctx);
+      segs.begin = sb.as<int64_t>();
+      segs.end = se.as<int64_t>();
+      segs.ids = cand.as<int32_t>();
+      // 5. MoL over the passers (queries with < k passers are redone on the whole corpus below,
+      //    engine.py:134-135)
+      Scratch sc;
+      MOLR_TRY(sc.alloc(size_t(B) * cap * 4, s));
+      KTimer tm(ctx, "mol_score", s, 0.0);
+      MOLR_TRY(mol_score_any<int32_t>(ctx, c, g, B, k_u, iue.as<float>(), iuw.as<float>(), tau, segs, sc.as<float>(), 0,
+                                      s));
+      tm.stop();
+      // 6. top-k per query
+      KTimer tk(ctx, "topk_segmented", s, 0.0);
+      MOLR_TRY(segmented_top_k<int32_t>(ctx, B, segs, sc.as<float>(), 0, k, id_offset, oi.as<int64_t>(),
+                                        os.as<float>(), s));
+      tk.stop();
+      // the call's one synchronisation: passer counts and the deferred overflow flags
       MOLR_CUDA(cudaMemcpyAsync(hcnt.data(), counts.p, size_t(B) * 8, cudaMemcpyDeviceToHost, s));
+      MOLR_CUDA(cudaMemcpyAsync(hfl, dflags.p, 16, cudaMemcpyDeviceToHost, s));
       MOLR_CUDA(cudaStreamSynchronize(s));
-      int64_t mx = *std::max_element(hcnt.begin(), hcnt.end());
-      if (mx <= cap) break;
+      double pairs = 0;
+      for (int b = 0; b < B; ++b) pairs += double(std::min<int64_t>(hcnt[b], cap));
+      tm.work = pairs;
+      tk.work = pairs;
+      bool redo = false;
+      if (hfl[0]) {  // the pilot threshold was not provably the sample's n-th largest
+        full_sample = true;
+        redo = true;
+      }
+      if (hfl[1] > seg_used_pilot) {
+        seg_min_pilot = hfl[1];
+        redo = true;
+      }
+      if (hfl[2] > seg_used_main) {
+        seg_min_main = hfl[2];
+        redo = true;
+      }
+      const int64_t mx = *std::max_element(hcnt.begin(), hcnt.end());
+      if (mx > cap) {
+        cap = mx;
+        redo = true;
+      }
+      if (!redo) break;
+      if (attempt == 3) MOLR_FAIL(MOLR_ERR_CAPACITY, "candidate buffers still overflowing after 3 retries");
       cand.reset();
-      cap = mx;
     }
-    MOLR_TRY(sb.alloc(size_t(B) * 8, s));
-    MOLR_TRY(se.alloc(size_t(B) * 8, s));
-    cap_segs_kernel<<<div_up(B, 256), 256, 0, s>>>(B, cap, counts.as<int64_t>(), sb.as<int64_t>(), se.as<int64_t>());
-    MOLR_LAUNCHED(ctx);
-    segs.begin = sb.as<int64_t>();
-    segs.end = se.as<int64_t>();
-    segs.ids = cand.as<int32_t>();
-    // 5. MoL over passers; queries with < k passers fall back to the whole corpus (engine.py:134-135)
     std::vector<int> fallback;
     for (int b = 0; b < B && !no_fallback; ++b)
       if (hcnt[b] < kk) fallback.push_back(b);
-    int64_t cand_total = int64_t(B) * cap;
-    double pairs = 0;
-    for (int b = 0; b < B; ++b) pairs += double(std::min<int64_t>(hcnt[b], cap));
-    Scratch sc;
-    MOLR_TRY(sc.alloc(size_t(cand_total) * 4, s));
-    {
-      KTimer t(ctx, "mol_score", s, pairs);
-      MOLR_TRY(mol_score_any<int32_t>(ctx, c, g, B, k_u, iue.as<float>(), iuw.as<float>(), tau, segs,
-                                      sc.as<float>(), 0, s));
-    }
-    // 6. top-k per query
-    {
-      KTimer t(ctx, "topk_segmented", s, pairs);
-      MOLR_TRY(segmented_top_k<int32_t>(ctx, B, segs, sc.as<float>(), 0, k, id_offset, oi.as<int64_t>(),
-                                        os.as<float>(), s));
-    }
     if (!fallback.empty()) {
       // dense MoL for the few queries whose candidate set came back smaller than k
       const int F = (int)fallback.size();

@@ -13,11 +13,22 @@ int gather_rows(molr_ctx* ctx, int64_t m, int64_t dim_bytes, const void* src, co
                 cudaStream_t s);
 int prepare_queries(molr_ctx* ctx, int mode, int B, int dim, const float* q, int8_t* qc, float* qs, cudaStream_t s);
 int check_view(const molr_cache* c, int mode);
+// Deferred overflow check for the filter scans of one batched call: instead of reading back the
+// largest per-CTA passer segment after each scan (a host round trip), the scan records it in
+// *seg_need (device, atomicMax) and reports the segment length it used in *seg_used (host); the
+// caller compares the two after its single end-of-call synchronisation and reruns with
+// seg_min = *seg_need if a segment overflowed (rare: passers of one query concentrated in one
+// CTA's block of the corpus).
+struct S1Deferred {
+  int* seg_need = nullptr;   // device
+  int64_t seg_min = 0;       // floor for the segment length
+  int64_t* seg_used = nullptr;  // host: max segment length used by the scans that reported here
+};
 bool s1_tc_supported(const molr_cache* c, int mode);
 int s1_tc_scan(molr_ctx* ctx, int mode, const int8_t* codes, const float* scales, const float2* mm,
                const int32_t* perm, int64_t n, int B,
                const int8_t* qcodes, const uint32_t* tkeys, int strict, int64_t cap, int32_t* cand, int64_t* counts,
-               void* out, int64_t ld, cudaStream_t s, bool emit_keys = false);
+               void* out, int64_t ld, cudaStream_t s, bool emit_keys = false, const S1Deferred* defer = nullptr);
 // chunk (min, max) scale reciprocals of 32-row chunks [c0, c1) of a scale vector (filter bound)
 int encode_rows_tmap(CUtensorMap* tm, const void* base, int64_t rows);
 int chunk_minmax(molr_ctx* ctx, const float* scales, int64_t c0, int64_t c1, float2* mm, cudaStream_t s);

@@ -318,33 +318,26 @@ __global__ void __launch_bounds__(NTHREADS, 1) s1_tc_kernel(Params P) {
             }
           }
         } else {
-          // per thread: one query (TMEM lane), 64 item columns as 2 chunks of 32 rows.  Per chunk
-          // the common case costs a 3-input max tree (0.5 instr per accumulator) and one warp vote:
-          //  * L = an integer bound necessary for passing anywhere in the 32-row chunk (from the
-          //    chunk's 1/min, 1/max scale with a 4e-6 relative margin; rows are stored sorted by
-          //    scale within 4,096-row windows, so the chunk's scale range and L are tight);
-          //  * chunk max >= L for no lane of the warp -> nothing in these 32 x 32 pairs can pass;
-          //  * otherwise per 8-row group another vote, and in a flagged group each accumulator
-          //    >= L (rare, divergent) gets the exact fp32 test fl(acc * scale) >= t
-          //    (NumPy's acc.astype(f32) * scales, hindexer.py:111; strict > as >= nextafter(t);
-          //    raw mode: acc >= t exactly, L itself) and is appended to the query's segment
-          //    with a shared-memory counter.
+          // per thread: one query (TMEM lane), 64 item columns as 2 chunks of 32 rows
           const uint32_t traw = reinterpret_cast<const uint32_t*>(sm + OFF_T)[q];
           const float tf = __uint_as_float(traw);
+          // strict (s > t) as s >= the next float above t (thresholds are finite scores);
+          // raw: acc >= t (+1 when strict)
           const float tfe = P.strict ? __uint_as_float(tf >= 0.f ? (tf == 0.f ? 1u : traw + 1u) : traw - 1u) : tf;
           const int32_t ti = int32_t(traw) + (P.strict ? 1 : 0);
+          const float4* sc4 = reinterpret_cast<const float4*>(sc);
           const float tlo = tf * (1.0f - 4e-6f), thi = tf * (1.0f + 4e-6f);
-          const bool qok = q < P.B;
-          int32_t* dst = qok ? cand_cta + int64_t(q) * P.cap : nullptr;
+          uint32_t mask[2];
           uint32_t ra[32], rb[32];
           TMEM_LD32(tm, ra);
 #pragma unroll
           for (int cc = 0; cc < 2; ++cc) {
             uint32_t* a = cc ? rb : ra;
+            // integer bound L: acc >= L is necessary to pass anywhere in this 32-row chunk
+            // (from the chunk's (1/min, 1/max) scale with a relative margin; computed while the
+            // TMEM load is in flight).  Padding rows are masked below, so their bound is moot.
             int32_t L;
-            if (!qok) {
-              L = 0x7fffffff;  // padding query rows never flag a group
-            } else if (RAW) {
+            if (RAW) {
               L = ti;  // exact
             } else {
               const float2 inv = mm[cc];
@@ -353,31 +346,63 @@ __global__ void __launch_bounds__(NTHREADS, 1) s1_tc_kernel(Params P) {
             TMEM_WAIT32(a);
             if (cc == 0) TMEM_LD32(tm + 32, rb);  // next chunk loads under this chunk's test
             const int j0 = cc * 32;
-            const int32_t* v = reinterpret_cast<const int32_t*>(a);
-            int32_t gm[4];
+            // per 8-column group: max as a shallow tree of 3-input maxes; the warp-wide OR of the
+            // per-lane group hits makes the group branches warp-uniform
+            uint32_t h = 0;
 #pragma unroll
-            for (int g8 = 0; g8 < 4; ++g8)
-              gm[g8] = max(__vimax3_s32(v[g8 * 8], v[g8 * 8 + 1], v[g8 * 8 + 2]),
-                           __vimax3_s32(v[g8 * 8 + 3], v[g8 * 8 + 4], max(v[g8 * 8 + 5], max(v[g8 * 8 + 6], v[g8 * 8 + 7]))));
-            const int32_t cm = max(__vimax3_s32(gm[0], gm[1], gm[2]), gm[3]);
-            if (__any_sync(0xffffffffu, cm >= L)) {
+            for (int g8 = 0; g8 < 4; ++g8) {
+              const int32_t* v = reinterpret_cast<const int32_t*>(a) + g8 * 8;
+              const int32_t gm = max(__vimax3_s32(v[0], v[1], v[2]), __vimax3_s32(v[3], v[4], max(v[5], max(v[6], v[7]))));
+              h |= uint32_t(gm >= L) << g8;
+            }
+            h = __reduce_or_sync(0xffffffffu, h);
+            uint32_t m = 0;
 #pragma unroll
-              for (int g8 = 0; g8 < 4; ++g8) {
-                if (!__any_sync(0xffffffffu, gm[g8] >= L)) continue;
+            for (int g8 = 0; g8 < 4; ++g8) {
+              if (h & (1u << g8)) {  // some lane may have a passer in this group: test all 8 exactly
+                const int32_t* v = reinterpret_cast<const int32_t*>(a) + g8 * 8;
+                uint32_t bits = 0;
+                if (RAW) {
 #pragma unroll
-                for (int jj = 0; jj < 8; ++jj) {
-                  const int32_t acc = v[g8 * 8 + jj];
-                  const int j = j0 + g8 * 8 + jj;
-                  if (acc >= L && j < nvalid) {
-                    float sv = 0.f;
-                    if (!RAW) sv = __fmul_rn((float)acc, sc[j]);
-                    if (RAW || sv >= tfe) {
-                      const uint32_t pos = atomicAdd(scnt + q, 1u);  // shared-memory counter
-                      if ((int64_t)pos < P.seg)
-                        dst[pos] = KEYS ? int32_t(RAW ? i32_key(acc) : f32_key(sv)) : pm[j];
-                    }
-                  }
+                  for (int jj = 0; jj < 8; ++jj) bits |= uint32_t(v[jj] >= L) << jj;
+                } else {  // exact fp32 test: fl(acc * scale) >= t  (hindexer.py:111)
+                  const float4 s0 = sc4[(j0 + g8 * 8) >> 2], s1 = sc4[((j0 + g8 * 8) >> 2) + 1];
+                  const float sv[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+#pragma unroll
+                  for (int jj = 0; jj < 8; ++jj) bits |= uint32_t(__fmul_rn((float)v[jj], sv[jj]) >= tfe) << jj;
                 }
+                m |= bits << (g8 * 8);
+              }
+            }
+            const int lim = nvalid - j0;  // valid columns in this chunk
+            if (lim < 32) m &= lim <= 0 ? 0u : ((1u << lim) - 1u);
+            mask[cc] = m;
+            if (KEYS && m && q < P.B) {  // append the passers' ascending score keys now (a[] is live)
+              uint32_t pos = atomicAdd(scnt + q, (uint32_t)__popc(m));
+              while (m) {
+                const int j = __ffs(m) - 1;
+                m &= m - 1;
+                uint32_t accv = 0;
+#pragma unroll
+                for (int jj = 0; jj < 32; ++jj) accv = (jj == j) ? a[jj] : accv;  // static register select
+                const int32_t acc = int32_t(accv);
+                const uint32_t key = RAW ? i32_key(acc) : f32_key(__fmul_rn((float)acc, sc[j0 + j]));
+                if ((int64_t)pos < P.seg) cand_cta[int64_t(q) * P.cap + pos] = int32_t(key);
+                ++pos;
+              }
+            }
+          }
+          const int total = __popc(mask[0]) + __popc(mask[1]);
+          if (!KEYS && total && q < P.B) {
+            uint32_t pos = atomicAdd(scnt + q, (uint32_t)total);  // shared-memory counter
+#pragma unroll
+            for (int cc = 0; cc < 2; ++cc) {
+              uint32_t m = mask[cc];
+              while (m) {
+                const int j = __ffs(m) - 1;
+                m &= m - 1;
+                if ((int64_t)pos < P.seg) cand_cta[int64_t(q) * P.cap + pos] = pm[cc * 32 + j];
+                ++pos;
               }
             }
           }
@@ -659,10 +684,12 @@ __global__ void __launch_bounds__(256) compact_segments_kernel(int G, int64_t se
   if (threadIdx.x == 0) {
     int64_t acc = 0;
     int mx = 0;
+    // an overflowed segment (c > seg) kept only its first seg passers: the list stays consistent
+    // (every position below counts[b] holds a passer) and max_cta reports the overflow
     for (int g = 0; g < G; ++g) {
       const int c = cnt[int64_t(b) * G + g];
       pre[g] = acc;
-      acc += c;
+      acc += imin64(c, seg);
       mx = max(mx, c);
     }
     pre[G] = acc;
@@ -673,7 +700,7 @@ __global__ void __launch_bounds__(256) compact_segments_kernel(int G, int64_t se
   }
   __syncthreads();
   for (int g = blockIdx.y; g < G; g += gridDim.y) {  // (query, group of segments) per block
-    const int64_t n = imin64(pre[g + 1] - pre[g], seg);
+    const int64_t n = pre[g + 1] - pre[g];
     const int32_t* s = src + int64_t(b) * cap_in + int64_t(g) * seg;
     int32_t* d = dst + int64_t(b) * cap_out + pre[g];
     for (int64_t i = threadIdx.x; i < n; i += blockDim.x)
@@ -1334,7 +1361,7 @@ bool s1_tc_supported(const molr_cache* c, int mode) {
 int s1_tc_scan(molr_ctx* ctx, int mode, const int8_t* codes, const float* scales, const float2* mm,
                const int32_t* perm, int64_t n, int B,
                const int8_t* qcodes, const uint32_t* tkeys, int strict, int64_t cap, int32_t* cand, int64_t* counts,
-               void* out, int64_t ld, cudaStream_t s, bool emit_keys) {
+               void* out, int64_t ld, cudaStream_t s, bool emit_keys, const S1Deferred* defer) {
   using namespace s1tc;
   if (n <= 0 || B <= 0) return MOLR_OK;
   const bool raw = mode == MOLR_S1_INT8_RAW;
@@ -1346,6 +1373,10 @@ int s1_tc_scan(molr_ctx* ctx, int mode, const int8_t* codes, const float* scales
   // per-CTA private segments: expected cap/grid passers each, with headroom; one retry at the
   // exact maximum if a segment overflowed
   int64_t seg = filter ? (cap / grid) + (cap / grid) / 3 + 64 : 0;
+  if (filter && defer) {
+    seg = std::max<int64_t>(seg, defer->seg_min);
+    if (defer->seg_used) *defer->seg_used = std::max<int64_t>(*defer->seg_used, seg);
+  }
   for (int b0 = 0; b0 < B; b0 += MAXQB * QB) {
     const int Bc = std::min(B - b0, MAXQB * QB);
     for (int attempt = 0; attempt < 2; ++attempt) {
@@ -1364,11 +1395,17 @@ int s1_tc_scan(molr_ctx* ctx, int mode, const int8_t* codes, const float* scales
       P.cap = int64_t(grid) * seg;
       P.cand = nullptr;
       P.cta_counts = nullptr;
+      int* mxp = nullptr;
       if (filter) {
         MOLR_TRY(priv.alloc(size_t(Bc) * P.cap * 4, s));
         MOLR_TRY(ccount.alloc(size_t(Bc) * grid * 4, s));
-        MOLR_TRY(mx.alloc(4, s));
-        MOLR_CUDA(cudaMemsetAsync(mx.p, 0, 4, s));
+        if (defer) {
+          mxp = defer->seg_need;
+        } else {
+          MOLR_TRY(mx.alloc(4, s));
+          MOLR_CUDA(cudaMemsetAsync(mx.p, 0, 4, s));
+          mxp = mx.as<int>();
+        }
         P.cand = priv.as<int32_t>();
         P.cta_counts = ccount.as<int32_t>();
       }
@@ -1404,8 +1441,9 @@ int s1_tc_scan(molr_ctx* ctx, int mode, const int8_t* codes, const float* scales
       }
       if (!filter) break;
       compact_segments_kernel<<<dim3(Bc, compact_split(ctx, Bc, grid)), 256, 0, s>>>(
-          grid, seg, P.cap, P.cand, P.cta_counts, cap, cand + int64_t(b0) * cap, counts + b0, mx.as<int>());
+          grid, seg, P.cap, P.cand, P.cta_counts, cap, cand + int64_t(b0) * cap, counts + b0, mxp);
       MOLR_LAUNCHED(ctx);
+      if (defer) break;  // checked by the caller after its end-of-call synchronisation
       int hmx = 0;
       MOLR_CUDA(cudaMemcpyAsync(&hmx, mx.p, 4, cudaMemcpyDeviceToHost, s));
       MOLR_CUDA(cudaStreamSynchronize(s));

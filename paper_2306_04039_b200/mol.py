@@ -383,6 +383,14 @@ class DeviceItemCache:
         L.call("molr_cache_fill", self._dev.value, row0, n, L.ptr(item_embs), L.ptr(item_gate_pre),
                L.ptr(stage1_embs), L.ptr(stage1_codes), L.ptr(stage1_scales), L.ptr(stream))
 
+    def read_stage1(self, row0: int, n: int, codes=None, scales=None):
+        """Rows [row0, row0+n) of the int8 stage-1 view in item order: (codes (n,d') int8, scales (n,))."""
+        codes = np.empty((n, self._d1), dtype=np.int8) if codes is None else codes
+        scales = np.empty(n, dtype=np.float32) if scales is None else scales
+        L.call("molr_cache_read", self._dev.value, int(row0), int(n), None, None, None, L.ptr(codes), L.ptr(scales),
+               None)
+        return codes, scales
+
     def read(self, row0: int, n: int):
         """Rows [row0, row0+n) back to the host as the reference's f32 ItemCache fields:
         (item_embs (n,k_x,d), item_gate_pre (n,G)) — exact (bf16 storage widens losslessly)."""

@@ -890,3 +890,24 @@ def test_topk_sampled_bound_path_ties():
         oi, _ = O.mol_top_k(oc, og, np.arange(X), ue[u], feats[u], 100)
         ref_all = O.score_candidates(oc, og, np.arange(X), ue[u], feats[u])
         assert topk_equal_modulo_ties(bi[u], oi, ref_all)
+
+
+@pytest.mark.parametrize("cross_scale,gate_scale", [(1.0, 1.0), (4.0, 4.0), (16.0, 16.0), (1.0, 64.0), (16.0, 64.0)])
+def test_tc_kernel_precision_margin(cross_scale, gate_scale):
+    """Precision budget of the tcgen05 MoL kernel's reduced-precision cross net (query hi/lo split
+    component GEMM, bf16 L1 with hi/lo bias, fp16 L2, tanh.approx SiLU; K1) against the
+    oracle, from the default init to x16-sharpened cross nets and x64 gate pre-activations (large
+    |uw * gate_pre| arguments of the combine SiLU and a near-one-hot softmax): the worst
+    |s_gpu - s_ref| / (1e-3 |s_ref| + 1e-6) must stay <= 0.5, i.e. at least a 2x margin inside the
+    north_star tolerance."""
+    from paper_2306_04039_b200.mol import batch_score_all
+
+    cache, syn, ue, feats = _synthetic_prod_cache(8_000, seed=9, gate_scale=gate_scale, n_users=16)
+    gating, og = _prod_gating(syn, cross_scale=cross_scale)
+    got = batch_score_all(cache, gating, ue, feats).astype(np.float64)
+    oc = O.Cache(cache.item_embs, cache.item_gate_pre, cache.stage1_embs, None, 20.0, 8)
+    ref = O.batch_score_all(oc, og, ue, feats).astype(np.float64)
+    budget = np.abs(got - ref) / (1e-3 * np.abs(ref) + 1e-6)
+    print(f"cross x{cross_scale} gate x{gate_scale}: max |err| {np.abs(got - ref).max():.3e}, "
+          f"worst fraction of the tolerance used {budget.max():.3f}")
+    assert budget.max() <= 0.5

@@ -228,3 +228,46 @@ def test_numerics_primitives_match_reference_forms():
         ev = np.exp(v - v.max())
         np.testing.assert_allclose(softmax(v), ev / ev.sum(), rtol=tol * 4, atol=tol)
     assert abs(float(silu(np.float32(1.0))) - 0.731059) < 1e-6  # test_numerics.py:94-105
+
+
+@pytest.mark.gpu
+def test_retrieval_engine_100_concurrent_queries_identical(golden):
+    """The lineserver contract (test_lineserver.py:90-107, threads at lineserver.py:69-77): 100
+    concurrent identical queries against one engine return identical bytes; concurrent distinct
+    queries return what they return sequentially.  Every thread calls the C-ABI directly (ctypes
+    releases the GIL) on its own per-thread stream."""
+    import threading
+    from types import SimpleNamespace
+
+    from paper_2306_04039_b200.engine import RetrievalEngine
+    from paper_2306_04039_b200.hindexer import HIndexerConfig
+    from paper_2306_04039_b200.mol import GatingNetwork, Mlp, MoLConfig
+
+    g = golden("engine_case2")
+    mk = lambda p: Mlp(g[p + ".w1"], g[p + ".b1"], g[p + ".w2"])  # noqa: E731
+    params = SimpleNamespace(user_table=g["user_table"], item_table=g["item_table"], user_proj=mk("user_proj"),
+                             item_proj=mk("item_proj"), n_users=g["user_table"].shape[0], compression=None,
+                             gating=GatingNetwork(user_net=mk("user_net"), item_net=mk("item_net"),
+                                                  cross_net=mk("cross_net")))
+    cfg = MoLConfig(k_u=4, k_x=4, d=16, tau=20.0, gating_hidden=32, dropout_p=0.0)
+    eng = RetrievalEngine.from_params(params, cfg, HIndexerConfig(k_prime=300, sample_ratio=0.1, quantized=True),
+                                      seed=11)
+    want = eng.query(7, 10)
+    n_users = min(20, g["user_table"].shape[0])
+    seq = {u: eng.query(u, 10) for u in range(n_users)}
+    out = [None] * 100
+    mixed = [None] * 100
+    start = threading.Barrier(100)
+
+    def worker(i):
+        start.wait()
+        out[i] = eng.query(7, 10)
+        mixed[i] = eng.query(i % n_users, 10)
+
+    th = [threading.Thread(target=worker, args=(i,)) for i in range(100)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert all(r == want for r in out)
+    assert all(mixed[i] == seq[i % n_users] for i in range(100))

@@ -11,7 +11,20 @@ import io
 import subprocess
 import sys
 
+# north_star evidence per kernel: tensor-pipe utilisation (all / imma / hmma sub-pipes), DRAM
+# throughput and bytes, issue utilisation and the pipes that bound the SIMT epilogues
 KEYS = [
+    "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_tensor_subpipe_imma_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_tensor_subpipe_hmma_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_tensor_subpipe_imma.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_tensor_subpipe_hmma.avg.pct_of_peak_sustained_active",
+    "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+    "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+    "smsp__average_warps_issue_stalled_wait_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_math_pipe_throttle_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_sleeping_per_issue_active.ratio",
     "gpu__time_duration.sum", "sm__cycles_elapsed.avg.per_second", "dram__bytes_read.sum", "dram__bytes_write.sum",
     "dram__throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
     "sm__inst_issued.avg.pct_of_peak_sustained_active", "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
@@ -61,9 +74,19 @@ def full(path):
         for k in KEYS:
             if k in d:
                 print(f"  {k:80s} {d[k]:>16s} {units[hdr.index(k)]}")
-        extra = [h for h in hdr if "imma" in h and "realtime" in h and h.endswith("pct_of_peak_sustained_elapsed")]
+        extra = [h for h in hdr if ("imma" in h or "hmma" in h or "pipe_tensor" in h) and "realtime" in h
+                 and h.endswith("pct_of_peak_sustained_elapsed")]
         for k in extra:
             print(f"  {k:80s} {d[k]:>16s} %")
+        # bytes per launch (for profiles/traffic.json)
+        try:
+            rb = float(d["dram__bytes_read.sum"].replace(",", ""))
+            wb = float(d["dram__bytes_write.sum"].replace(",", ""))
+            ur, uw_ = units[hdr.index("dram__bytes_read.sum")], units[hdr.index("dram__bytes_write.sum")]
+            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+            print(f"  {'dram bytes read+write per launch':80s} {rb * scale.get(ur, 1) + wb * scale.get(uw_, 1):16.4g} B")
+        except (KeyError, ValueError):
+            pass
 
 
 if __name__ == "__main__":
