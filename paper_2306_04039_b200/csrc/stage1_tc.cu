@@ -977,18 +977,23 @@ __global__ void __launch_bounds__(NTHREADS, 1) bf_kernel(Params P) {
         const uint32_t tm = tmem_base + buf * 256 + w * 64 + tlane;
         mbar_wait(tfull(buf), uint32_t((jc >> 1) & 1));
         tc_fence_after();
+        bool released = false;
         if (qb * QB + quarter * 32 < P.B) {
           const float t = st_t[q], e = st_e[q];
           const float slack = st_c[q] + fabsf(t) * 1e-6f + 1e-30f;
           uint32_t cert[2], bnd[2];
           uint32_t ra[32], rb[32];
           TMEM_LD32(tm, ra);
+          TMEM_LD32(tm + 32, rb);
+          TMEM_WAIT32(ra);
+          TMEM_WAIT32(rb);
+          tc_fence_before();  // accumulators in registers: release the TMEM buffer early
+          mbar_arrive(tempty(buf));
+          released = true;
 #pragma unroll
           for (int cc = 0; cc < 2; ++cc) {
             uint32_t* a = cc ? rb : ra;
             const float lo = t - (e * cmx[cc] + slack);  // below it the whole chunk fails for certain
-            TMEM_WAIT32(a);
-            if (cc == 0) TMEM_LD32(tm + 32, rb);
             const float* v = reinterpret_cast<const float*>(a);
             uint32_t h = 0;
 #pragma unroll
@@ -1037,8 +1042,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) bf_kernel(Params P) {
             }
           }
         }
-        tc_fence_before();
-        mbar_arrive(tempty(buf));
+        if (!released) {
+          tc_fence_before();
+          mbar_arrive(tempty(buf));
+        }
       }
       mbar_arrive(empty_bar(stage));
       if (++stage == NSTAGE) {
