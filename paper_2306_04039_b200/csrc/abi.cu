@@ -571,8 +571,7 @@ int molr_gating_destroy(molr_gating* g) {
   cudaFree(g->uw1);
   cudaFree(g->ub1);
   cudaFree(g->uw2);
-  cudaFree(g->w1t_bf16);
-  cudaFree(g->w2t_bf16);
+  cudaFree(g->w1t_bf16);  // w2t_bf16 points into the same allocation
   delete g;
   return MOLR_OK;
 }

@@ -18,13 +18,17 @@
 //       bf16, fp32 accumulation.
 //   E0: D0 -> (hi+lo)/tau -> fp32 logits, transposed to one row per pair in the group's smem CL
 //       (kept there for the final gated sum); D0 released
-//   E0.5: row p -> A1 = bf16 logits packed two per column (the A operand of layer 1, from TMEM)
-//   L1: A1 (TMEM) . W1^T (smem) + [1 1 0..] . [b1_hi b1_lo 0..]^T (SS, K=16) -> D1
-//   E1: h = silu(D1) -> A2 = fp16(h), two per column (group cols [0,64): A1 is dead by then)
-//   L2: A2 (TMEM) . W2 (fp16, smem) -> D2 (over D1).  fp16 h and W2 carry 2^-11 relative error:
-//       max |score error| 2.2e-7 under x4-sharpened gating (emulated; tolerance floor 1e-6), and
-//       one fp16 MMA pass replaces the three bf16 hi/lo passes
+//   E0.5: row p -> A1 = the logits split in bf16 hi + lo, packed two per column (the A operand
+//       of layer 1, from TMEM: hi in group cols [0,32), lo in [32,64))
+//   L1: A1_hi . W1_hi + A1_lo . W1_hi + A1_hi . W1_lo (TMEM x smem, three passes: ~2^-16
+//       relative) + [1 1 0..] . [b1_hi b1_lo 0..]^T (SS, K=16) -> D1
+//   E1: h = silu(D1) (ex2 + rcp) -> A2 = h split in fp16 hi + lo (hi over the dead A1, lo over
+//       D1 columns this warp has already read)
+//   L2: A2_hi . W2_hi + A2_lo . W2_hi + A2_hi . W2_lo (fp16, three passes: ~2^-21) -> D2
 //   E2: pi = softmax(silu(uw * gate_pre + D2)); score = sum pi * CL  -> global
+// The cross net runs at ~fp32 accuracy: a single bf16 / fp16 pass and a tanh.approx SiLU gave
+// score errors above the 1e-3 |s| + 1e-6 tolerance once the cross net is sharpened x16
+// (tests/test_gpu_parity.py::test_tc_kernel_precision_margin, emulated in tools/precision_emu.py).
 // The G logits and H hidden units never leave the SM.
 #include <algorithm>
 #include <vector>
@@ -42,7 +46,11 @@ constexpr int KX = 8, D = 64, G = 64, H = 128;
 constexpr int TILE = 128;           // pairs per tile (MMA M)
 constexpr int GROUP = 16;           // items per component MMA (16 items x 8 rows = 128)
 constexpr int NGROUPS = TILE / GROUP;
-constexpr int NSTAGE = 7;           // ring stages (16 KB each): 112 KB of item blocks in flight per SM
+#ifndef MOL_NSTAGE
+#define MOL_NSTAGE 5
+#endif
+// (MOL_FAST / MOL_NSTAGE: timing experiments only — single-pass cross net; not built by the Makefile)
+constexpr int NSTAGE = MOL_NSTAGE;  // ring stages (16 KB each): 80 KB of item blocks in flight per SM
 constexpr int NE = 2;               // epilogue groups
 constexpr int CL_LD = 68;           // fp32 row stride of the logit transpose buffer (conflict-free LDS.128)
 
@@ -51,7 +59,14 @@ constexpr int SZ_STAGE = GROUP * 1024;                  // 16 KB
 constexpr int OFF_RING = 0;
 constexpr int OFF_W1T = OFF_RING + NSTAGE * SZ_STAGE;   // 128 x 64 bf16, SW128      16 KB
 constexpr int OFF_W2T = OFF_W1T + 16384;                // 2 x (64 x 64) fp16, SW128 16 KB
-constexpr int OFF_W1B = OFF_W2T + 16384;                // 128 x 16 bf16, interleave  4 KB
+#ifdef MOL_FAST
+constexpr int SZ_LO = 0;
+#else
+constexpr int SZ_LO = 16384;
+#endif
+constexpr int OFF_W1TL = OFF_W2T + 16384;               // W1 lo parts, as W1T        16 KB
+constexpr int OFF_W2TL = OFF_W1TL + SZ_LO;              // W2 lo parts, as W2T        16 KB
+constexpr int OFF_W1B = OFF_W2TL + SZ_LO;               // 128 x 16 bf16, interleave  4 KB
 constexpr int OFF_BIASA = OFF_W1B + 4096;               // 128 x 16 bf16, interleave  4 KB
 constexpr int NB0 = 3;                                  // B0 (query operand) ring slots
 constexpr int OFF_B0 = OFF_BIASA + 4096;                // NB0 x 16 x 64 bf16 SW128 (u_hi ; u_lo), 2 KB each
@@ -67,7 +82,11 @@ constexpr int OFF_TMEM = OFF_BAR + NBAR * 8;
 constexpr int SMEM_BYTES = OFF_TMEM + 16;
 static_assert(SMEM_BYTES <= 232448, "shared memory budget");
 constexpr int TM_D0 = 0;                                // shared component-logit accumulator
-__host__ __device__ constexpr int tm_grp(int g) { return 128 + 192 * g; }  // A1/A2 at +0, D1/D2 at +64
+__host__ __device__ constexpr int tm_grp(int g) { return 128 + 192 * g; }  // A1/A2 at +0, D1 at +64, D2 at +96
+// group column of A2_lo's hidden chunk ch (8 packed columns): inside D1 columns its warp has read
+// (warp half 0 reads D1 chunks 0..3 in order, half 1 chunks 7..4 in reverse), clear of D2 = D1 [32, 96)
+__host__ __device__ constexpr int a2lo_col(int ch) { return 64 + (ch < 4 ? 8 * ch : 64 + 8 * ch); }
+constexpr int TM_D2 = 96;
 
 // ---- PTX wrappers ---------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -178,6 +197,8 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);  // .x = lo (low 16 bits), .y = hi
   return *reinterpret_cast<uint32_t*>(&v);
 }
+__device__ __forceinline__ float bf16_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf16_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
 __device__ __forceinline__ uint32_t pack_f16(float lo, float hi) {
   __half2 v = __floats2half2_rn(lo, hi);  // .x = lo (low 16 bits), .y = hi
   return *reinterpret_cast<uint32_t*>(&v);
@@ -259,6 +280,8 @@ struct Params {
   const __nv_bfloat16* w1t;   // SW128 image (16 KB)
   const __nv_bfloat16* w2t;   // SW128 image (16 KB), followed by the residual image (16 KB)
   const __nv_bfloat16* w1b;   // interleave image (4 KB)
+  const __nv_bfloat16* w1tl;  // SW128 image of the W1 lo parts (16 KB)
+  const __nv_bfloat16* w2tl;  // SW128 image of the W2 lo parts (16 KB)
   const float* user_embs;     // (B, 8, 64)
   const float* uw;            // (B, 64)
   const int64_t* begin;
@@ -295,9 +318,15 @@ __global__ void __launch_bounds__(64 + NE * 256 + 32 * NE, 1) mol_tc_kernel(Para
     const uint4* src1 = reinterpret_cast<const uint4*>(P.w1t);
     const uint4* src2 = reinterpret_cast<const uint4*>(P.w2t);
     const uint4* src3 = reinterpret_cast<const uint4*>(P.w1b);
+    const uint4* src4 = reinterpret_cast<const uint4*>(P.w1tl);
+    const uint4* src5 = reinterpret_cast<const uint4*>(P.w2tl);
     for (int i = threadIdx.x; i < 1024; i += blockDim.x) {
       reinterpret_cast<uint4*>(sm + OFF_W1T)[i] = __ldg(src1 + i);
       reinterpret_cast<uint4*>(sm + OFF_W2T)[i] = __ldg(src2 + i);
+      if (SZ_LO) {
+        reinterpret_cast<uint4*>(sm + OFF_W1TL)[i] = __ldg(src4 + i);
+        reinterpret_cast<uint4*>(sm + OFF_W2TL)[i] = __ldg(src5 + i);
+      }
     }
     for (int i = threadIdx.x; i < 256; i += blockDim.x) reinterpret_cast<uint4*>(sm + OFF_W1B)[i] = __ldg(src3 + i);
     // bias A operand: K columns 0 and 1 of every row = 1.0 (pairs with the b1 hi / lo rows of W1B)
@@ -456,17 +485,26 @@ __global__ void __launch_bounds__(64 + NE * 256 + 32 * NE, 1) mol_tc_kernel(Para
         mbar_wait(gbar(g, 1), up);  // A1 stored by the group
         tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
+        for (int kk = 0; kk < 4; ++kk) {  // A1_hi . W1_hi + A1_lo . W1_hi + A1_hi . W1_lo
           mma_bf16_ts(tg + 64, tg + kk * 8, desc_sw128(sbase + OFF_W1T + kk * 32), ID128, kk > 0);
+          if (SZ_LO) {
+            mma_bf16_ts(tg + 64, tg + 32 + kk * 8, desc_sw128(sbase + OFF_W1T + kk * 32), ID128, 1);
+            mma_bf16_ts(tg + 64, tg + kk * 8, desc_sw128(sbase + OFF_W1TL + kk * 32), ID128, 1);
+          }
+        }
         mma_bf16(tg + 64, desc_interleave(sbase + OFF_BIASA, 128, 256), desc_interleave(sbase + OFF_W1B, 128, 256),
                  ID128, 1);
         mma_commit(gbar(g, 2));
         mbar_wait(gbar(g, 3), up);  // A2 (SiLU hidden, fp16) stored by the group
         tc_fence_after();
 #pragma unroll
-        for (int ch = 0; ch < 8; ++ch) {  // hidden K [16ch, 16ch+16): A2 cols [8ch, 8ch+8)
+        for (int ch = 0; ch < 8; ++ch) {  // hidden K [16ch, 16ch+16): A2_hi cols [8ch, 8ch+8), A2_lo a2lo_col(ch)
           const uint32_t bo = (ch >> 2) * 8192 + (ch & 3) * 32;
-          mma_bf16_ts(tg + 64, tg + ch * 8, desc_sw128(sbase + OFF_W2T + bo), idesc_f16(64), ch > 0);
+          mma_bf16_ts(tg + TM_D2, tg + ch * 8, desc_sw128(sbase + OFF_W2T + bo), idesc_f16(64), ch > 0);
+          if (SZ_LO) {
+            mma_bf16_ts(tg + TM_D2, tg + a2lo_col(ch), desc_sw128(sbase + OFF_W2T + bo), idesc_f16(64), 1);
+            mma_bf16_ts(tg + TM_D2, tg + ch * 8, desc_sw128(sbase + OFF_W2TL + bo), idesc_f16(64), 1);
+          }
         }
         mma_commit(gbar(g, 4));
       }
@@ -543,14 +581,17 @@ __global__ void __launch_bounds__(64 + NE * 256 + 32 * NE, 1) mol_tc_kernel(Para
         const float4* row = reinterpret_cast<const float4*>(CL + p * CL_LD + 32 * hf);
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          uint32_t a1[8];
+          uint32_t a1[8], a1l[8];
 #pragma unroll
           for (int m = 0; m < 4; ++m) {
             const float4 x = row[h * 4 + m];
             a1[2 * m] = pack_bf16(x.x, x.y);
             a1[2 * m + 1] = pack_bf16(x.z, x.w);
+            a1l[2 * m] = pack_bf16(x.x - bf16_lo(a1[2 * m]), x.y - bf16_hi(a1[2 * m]));
+            a1l[2 * m + 1] = pack_bf16(x.z - bf16_lo(a1[2 * m + 1]), x.w - bf16_hi(a1[2 * m + 1]));
           }
           TMEM_ST8(tg + 16 * hf + h * 8, a1);
+          TMEM_ST8(tg + 32 + 16 * hf + h * 8, a1l);
         }
         tmem_wait_st();
       }
@@ -573,25 +614,32 @@ __global__ void __launch_bounds__(64 + NE * 256 + 32 * NE, 1) mol_tc_kernel(Para
       TRACE(4);
       tc_fence_after();
       {
+        // warp half 0 walks hidden chunks 0..3, half 1 chunks 7..4, so the A2_lo columns it writes
+        // (a2lo_col) are always D1 columns it has already read
         uint32_t va[16], vb[16];
-        TMEM_LD16(tg + 64 + (4 * hf) * 16, va);
+        const int ch0 = hf ? 7 : 0, dch = hf ? -1 : 1;
+        TMEM_LD16(tg + 64 + ch0 * 16, va);
 #pragma unroll
         for (int c4 = 0; c4 < 4; ++c4) {
-          const int ch = 4 * hf + c4;
+          const int ch = ch0 + dch * c4;
           uint32_t* v = (c4 & 1) ? vb : va;
           tmem_wait_ld();
           if (c4 < 3) {  // next chunk loads under this chunk's SiLU
-            if (c4 & 1) TMEM_LD16(tg + 64 + (ch + 1) * 16, va);
-            else TMEM_LD16(tg + 64 + (ch + 1) * 16, vb);
+            if (c4 & 1) TMEM_LD16(tg + 64 + (ch + dch) * 16, va);
+            else TMEM_LD16(tg + 64 + (ch + dch) * 16, vb);
           }
-          uint32_t w[8];
+          uint32_t w[8], wl[8];
 #pragma unroll
           for (int m = 0; m < 8; ++m) {
             const float x0 = __uint_as_float(v[2 * m]), x1 = __uint_as_float(v[2 * m + 1]);
             const float h0 = P.e1_tanh ? silu_tanh(x0) : silu_acc(x0), h1 = P.e1_tanh ? silu_tanh(x1) : silu_acc(x1);
-            w[m] = pack_f16(h0, h1);
+            const __half2 hh = __floats2half2_rn(h0, h1);
+            const float2 hb = __half22float2(hh);
+            w[m] = *reinterpret_cast<const uint32_t*>(&hh);
+            wl[m] = pack_f16(h0 - hb.x, h1 - hb.y);
           }
-          TMEM_ST8(tg + ch * 8, w);  // A2 = fp16 h, two per column (A1 is dead: L1 has completed)
+          TMEM_ST8(tg + ch * 8, w);  // A2_hi, two per column (A1 is dead: L1 has completed)
+          TMEM_ST8(tg + a2lo_col(ch), wl);
         }
       }
       tmem_wait_st();
@@ -606,8 +654,8 @@ __global__ void __launch_bounds__(64 + NE * 256 + 32 * NE, 1) mol_tc_kernel(Para
       float mx = -INFINITY;
       {
         uint32_t v0[16], v1[16];
-        TMEM_LD16(tg + 64 + 32 * hf, v0);
-        TMEM_LD16(tg + 64 + 32 * hf + 16, v1);
+        TMEM_LD16(tg + TM_D2 + 32 * hf, v0);
+        TMEM_LD16(tg + TM_D2 + 32 * hf + 16, v1);
         tmem_wait_ld();
 #pragma unroll
         for (int m = 0; m < 32; ++m) {
@@ -714,6 +762,8 @@ int mol_score_tc(molr_ctx* ctx, const molr_cache* c, const molr_gating* g, int B
   P.w1t = g->w1t_bf16;
   P.w2t = g->w2t_bf16;
   P.w1b = g->w1t_bf16 + 8192;
+  P.w1tl = g->w1t_bf16 + 18432;
+  P.w2tl = g->w1t_bf16 + 26624;
   P.user_embs = ue;
   P.uw = uw;
   P.begin = segs.begin;
@@ -724,7 +774,7 @@ int mol_score_tc(molr_ctx* ctx, const molr_cache* c, const molr_gating* g, int B
   P.out_ld = out_ld;
   {
     const char* e = dev_knob("MOLR_E1");
-    P.e1_tanh = (e && e[0] == 'a') ? 0 : 1;
+    P.e1_tanh = (e && e[0] == 't') ? 1 : 0;  // dev: the 1-MUFU tanh.approx SiLU (below tolerance when sharpened)
     const char* gm = dev_knob("MOLR_GATHER");
     P.gather4 = (c->embs_tmap_ok && !(gm && gm[0] == 'b')) ? 1 : 0;
   }
@@ -773,12 +823,18 @@ extern "C" int molr_gating_tc_prepare(molr_gating* g) {
   MOLR_CUDA(cudaMemcpy(w1.data(), g->w1, w1.size() * 4, cudaMemcpyDefault));
   MOLR_CUDA(cudaMemcpy(b1.data(), g->b1, b1.size() * 4, cudaMemcpyDefault));
   MOLR_CUDA(cudaMemcpy(w2.data(), g->w2, w2.size() * 4, cudaMemcpyDefault));
-  std::vector<__nv_bfloat16> img(8192 + 2048 + 8192, __float2bfloat16(0.0f));
+  // [W1T hi 8192][W1B 2048][W2T hi 8192 (fp16)][W1T lo 8192][W2T lo 8192 (fp16)]
+  std::vector<__nv_bfloat16> img(8192 + 2048 + 8192 + 8192 + 8192, __float2bfloat16(0.0f));
   auto sw = [](int r, int k) {  // element offset in an SW128 K-major [rows x 64] region
     return (r >> 3) * 512 + (r & 7) * 64 + ((((k >> 3) ^ (r & 7))) << 3) + (k & 7);
   };
   for (int j = 0; j < 128; ++j)
-    for (int gg = 0; gg < 64; ++gg) img[sw(j, gg)] = __float2bfloat16(w1[size_t(gg) * 128 + j]);
+    for (int gg = 0; gg < 64; ++gg) {
+      const float x = w1[size_t(gg) * 128 + j];
+      const __nv_bfloat16 hi = __float2bfloat16(x);
+      img[sw(j, gg)] = hi;
+      img[18432 + sw(j, gg)] = __float2bfloat16(x - __bfloat162float(hi));
+    }
   for (int j = 0; j < 128; ++j) {
     __nv_bfloat16 hi = __float2bfloat16(b1[j]);
     __nv_bfloat16 lo = __float2bfloat16(b1[j] - __bfloat162float(hi));
@@ -789,11 +845,12 @@ extern "C" int molr_gating_tc_prepare(molr_gating* g) {
   // W2^T as fp16 (the L2 MMA runs fp16 x fp16 -> f32: h and W2 at 2^-11 relative)
   for (int gg = 0; gg < 64; ++gg)
     for (int j = 0; j < 128; ++j) {
-      const __half hv = __float2half_rn(w2[size_t(j) * 64 + gg]);
+      const float x = w2[size_t(j) * 64 + gg];
+      const __half hv = __float2half_rn(x);
       reinterpret_cast<__half*>(img.data())[8192 + 2048 + (j >> 6) * 4096 + sw(gg, j & 63)] = hv;
+      reinterpret_cast<__half*>(img.data())[26624 + (j >> 6) * 4096 + sw(gg, j & 63)] = __float2half_rn(x - __half2float(hv));
     }
-  // layout in device memory: [W1T 8192 bf16][W1B 2048 bf16][W2T 8192 fp16] -> w1t_bf16 points at
-  // the start, w2t_bf16 at +10240
+  // w1t_bf16 points at the start of the image, w2t_bf16 at +10240
   MOLR_CUDA(cudaMalloc(&g->w1t_bf16, img.size() * 2));
   MOLR_CUDA(cudaMemcpy(g->w1t_bf16, img.data(), img.size() * 2, cudaMemcpyHostToDevice));
   g->w2t_bf16 = g->w1t_bf16 + 10240;

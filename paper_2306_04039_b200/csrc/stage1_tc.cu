@@ -341,25 +341,20 @@ __global__ void __launch_bounds__(NTHREADS, 1) s1_tc_kernel(Params P) {
               L = ti;  // exact
             } else {
               const float2 inv = mm[cc];
-              L = max(__float2int_rd(fminf(tlo * inv.y, thi * inv.x)), -1073741824) - 1;
+              // floor(x - 1) saturates (no wrap) for the hopeless chunks of very large |t|
+              L = __float2int_rd(fmaf(tf >= 0.f ? tlo : thi, tf >= 0.f ? inv.y : inv.x, -1.0f));
             }
             TMEM_WAIT32(a);
             if (cc == 0) TMEM_LD32(tm + 32, rb);  // next chunk loads under this chunk's test
             const int j0 = cc * 32;
-            // per 8-column group: max as a shallow tree of 3-input maxes; the warp-wide OR of the
-            // per-lane group hits makes the group branches warp-uniform
-            uint32_t h = 0;
-#pragma unroll
-            for (int g8 = 0; g8 < 4; ++g8) {
-              const int32_t* v = reinterpret_cast<const int32_t*>(a) + g8 * 8;
-              const int32_t gm = max(__vimax3_s32(v[0], v[1], v[2]), __vimax3_s32(v[3], v[4], max(v[5], max(v[6], v[7]))));
-              h |= uint32_t(gm >= L) << g8;
-            }
-            h = __reduce_or_sync(0xffffffffu, h);
+            // per 8-column group: max as a tree of four 3-input maxes; a warp vote per group makes
+            // the group branches warp-uniform
             uint32_t m = 0;
 #pragma unroll
             for (int g8 = 0; g8 < 4; ++g8) {
-              if (h & (1u << g8)) {  // some lane may have a passer in this group: test all 8 exactly
+              const int32_t* v = reinterpret_cast<const int32_t*>(a) + g8 * 8;
+              const int32_t gm = __vimax3_s32(__vimax3_s32(v[0], v[1], v[2]), __vimax3_s32(v[3], v[4], v[5]), max(v[6], v[7]));
+              if (__any_sync(0xffffffffu, gm >= L)) {  // some lane may have a passer in this group: test all 8 exactly
                 const int32_t* v = reinterpret_cast<const int32_t*>(a) + g8 * 8;
                 uint32_t bits = 0;
                 if (RAW) {
@@ -761,6 +756,11 @@ constexpr int NTHREADS = 64 + NEPI * 128;
 static_assert(SMEM_BYTES <= 232448, "shared memory");
 constexpr uint32_t IDESC = (1u << 4) | (uint32_t(NT >> 3) << 17) | (uint32_t(QB >> 4) << 24);  // f16 x f16 -> f32
 
+__device__ __forceinline__ float fmax3(float a, float b, float c) {  // FMNMX3
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
 __host__ __device__ __forceinline__ int64_t bf_offset(int64_t r, int k) {  // element offset of v[r][k]
   return ((r >> 3) << 9) + int64_t(k >> 3) * 64 + ((r & 7) << 3) + (k & 7);
 }
@@ -995,22 +995,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) bf_kernel(Params P) {
             uint32_t* a = cc ? rb : ra;
             const float lo = t - (e * cmx[cc] + slack);  // below it the whole chunk fails for certain
             const float* v = reinterpret_cast<const float*>(a);
-            uint32_t h = 0;
-#pragma unroll
-            for (int g8 = 0; g8 < 4; ++g8) {
-              const float* u = v + g8 * 8;
-              const float gm = fmaxf(fmaxf(fmaxf(u[0], u[1]), fmaxf(u[2], u[3])), fmaxf(fmaxf(u[4], u[5]), fmaxf(u[6], u[7])));
-              h |= uint32_t(gm >= lo) << g8;
-            }
-            h = __reduce_or_sync(0xffffffffu, h);
             // in a hit group: certain above the chunk's upper bound, band between the two bounds
             // (the chunk's max row norm for both: two compares per element)
             const float hi = t + (e * cmx[cc] + slack);
             uint32_t mc = 0, ml = 0;
 #pragma unroll
             for (int g8 = 0; g8 < 4; ++g8) {
-              if (h & (1u << g8)) {
-                const float* u = v + g8 * 8;
+              const float* u = v + g8 * 8;
+              const float gm = fmax3(fmax3(u[0], u[1], u[2]), fmax3(u[3], u[4], u[5]), fmaxf(u[6], u[7]));
+              if (__any_sync(0xffffffffu, gm >= lo)) {
 #pragma unroll
                 for (int jj = 0; jj < 8; ++jj) {
                   mc |= uint32_t(u[jj] >= hi) << (g8 * 8 + jj);

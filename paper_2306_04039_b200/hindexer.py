@@ -233,14 +233,20 @@ def index_select(cache: ItemCache, indices) -> ItemCache:
     out = C.c_void_p()
     L.call("molr_index_select", L.ctx(), cache_handle(cache), n, L.ptr(indices), C.byref(out))
     h = L.Handle(out.value, "molr_cache_destroy")
+    storage = C.c_int()
+    L.call("molr_cache_info", h.value, None, C.byref(storage), None)
     embs = np.empty((n, cfg.k_x, cfg.d), dtype=np.float32)
     gp = np.empty((n, cfg.num_logits), dtype=np.float32)
     s1 = np.empty((n, cache.stage1_dim), dtype=np.float32)
     codes = scales = None
-    if cache.stage1_q is not None:
-        codes = np.empty((n, cache.stage1_q.codes.shape[1]), dtype=np.int8)
+    if storage.value & L.STORE_S1_INT8:
+        codes = np.empty((n, cache.stage1_dim), dtype=np.int8)
         scales = np.empty(n, dtype=np.float32)
     L.call("molr_cache_read", h.value, 0, n, L.ptr(embs), L.ptr(gp), L.ptr(s1), L.ptr(codes), L.ptr(scales), None)
+    if not storage.value & L.STORE_S1_F32:
+        # a device-only corpus (DeviceItemCache) may keep just the int8 stage-1 view: its rows'
+        # float view is then the dequantised codes (quant.py:57-62)
+        s1 = codes.astype(np.float32) * scales[:, None] if codes is not None else np.zeros_like(s1)
     for a in (embs, gp, s1, codes, scales):  # the device copy mirrors them: immutable (mol.py:218)
         if a is not None:
             a.flags.writeable = False
