@@ -47,13 +47,21 @@ CONFIGS = {
     # B users x all X items; the full ML-20M run is 138K users
     "ml20m": dict(X=27_000, B=1024, k=100, k_prime=None, ratio=None, exact=True, users=138_000,
                   label="ML-20M-shaped synthetic: 27K items, exact MoL top-100"),
+    # a reference-built cache (mol.py:294-326 in f32: components and gate pre-activations not
+    # bf16-representable), served by the tcgen05 scorer through its bf16 hi + lo image (K1)
+    "ml20m_f32cache": dict(X=27_000, B=1024, k=100, k_prime=None, ratio=None, exact=True, users=138_000,
+                           cache="f32", label="ML-20M-shaped synthetic, f32 (reference-built) cache: 27K items, "
+                                               "exact MoL top-100"),
+    "books_f32cache": dict(X=2_300_000, B=1024, k=100, k_prime=100_000, ratio=0.01, cache="f32",
+                           label="Amazon-Books-shaped 2.3M items, f32 (reference-built) cache"),
     # BASELINE configs[0]: one step = every user of the ML-1M shape against the whole corpus
     "ml1m": dict(X=3_706, B=6_040, k=200, k_prime=None, ratio=None, exact=True, users=6_040,
                  label="ML-1M-shaped synthetic: 6,040 users x 3,706 items, exact MoL top-200"),
 }
 # queries checked against the CPU oracle (oracle/molr_oracle.c) after the timed region: exhaustive
 # oracle top-k for ORACLE_Q[config] queries (all users for ML-1M), oracle scores of the returned items
-ORACLE_Q = {"100m": 2, "100m_f32": 2, "10m": 8, "10m_f32": 8, "books": 16, "ml20m": 64, "ml1m": 6_040}
+ORACLE_Q = {"100m": 2, "100m_f32": 2, "10m": 8, "10m_f32": 8, "books": 16, "ml20m": 64, "ml1m": 6_040,
+            "ml20m_f32cache": 64, "books_f32cache": 16}
 K_U = K_X = 8
 D = 64
 G = 64
@@ -65,6 +73,7 @@ CHUNK = 500_000  # global corpus generation chunk (shard boundaries are chunk-al
 
 # per-unit algorithmic work: one MoL pair, one stage-1 (query, row) dot
 PAIR_BYTES = K_X * D * 2 + G * 2 + 4       # bf16 item components + bf16 gate_pre + int32 id = 1156 B
+PAIR_BYTES_F32C = K_X * D * 4 + G * 4 + 4  # f32 cache: bf16 hi + lo components + f32 gate_pre + id = 2308 B
 PAIR_FLOPS = 2 * (G * D + G * H + H * G)   # component GEMM + cross-net 64->128->64 = 40960
 S1_OPS = 2 * D                             # int8 MACs x 2 per (query, row)
 
@@ -96,7 +105,7 @@ def synthetic_model(seed=4242):
             "user_net": _mlp(rng, D_U, H, G), "item_net": _mlp(rng, D_X, H, G), "cross_net": _mlp(rng, G, H, G)}
 
 
-def build_shard(model, X, lo, hi, seed, dev, lib, ctx, storage=None):
+def build_shard(model, X, lo, hi, seed, dev, lib, ctx, storage=None, f32_cache=False):
     """Build rows [lo, hi) of the global corpus on the device into a DeviceItemCache through the
     product's fused cache build (molr_cache_build_rows: item_proj MLP -> L2 norm -> item_net ->
     bf16 storage rounding -> stage-1 mean -> int8), from a synthetic item table drawn on the
@@ -108,7 +117,11 @@ def build_shard(model, X, lo, hi, seed, dev, lib, ctx, storage=None):
     from paper_2306_04039_b200.numerics import DEFAULT_EPS
 
     cfg = MoLConfig(k_u=K_U, k_x=K_X, d=D, tau=TAU, gating_hidden=H, dropout_p=0.0)
-    cache = DeviceItemCache(cfg, hi - lo, D, L.STORE_S1_INT8 if storage is None else storage)
+    if storage is None:
+        storage = L.STORE_S1_INT8
+    if f32_cache:  # the reference's f32 cache values (no bf16 rounding), stored losslessly in f32
+        storage |= L.STORE_EMBS_F32 | L.STORE_GP_F32
+    cache = DeviceItemCache(cfg, hi - lo, D, storage)
     W = {k: [torch.from_numpy(a).to(dev) for a in v] for k, v in model.items()}
     pw, nw = W["item_proj"], W["item_net"]
     s = torch.cuda.current_stream().cuda_stream
@@ -122,7 +135,8 @@ def build_shard(model, X, lo, hi, seed, dev, lib, ctx, storage=None):
             t = t[c0 - g0:c1 - g0].contiguous()
             L.call("molr_cache_build_rows", cache.device_handle(), c0 - lo, c1 - c0, D_X, t.data_ptr(), PROJ_H,
                    pw[0].data_ptr(), pw[1].data_ptr(), pw[2].data_ptr(), H, nw[0].data_ptr(), nw[1].data_ptr(),
-                   nw[2].data_ptr(), L.BUILD_L2_NORMALIZE | L.BUILD_ROUND_BF16, float(DEFAULT_EPS), s)
+                   nw[2].data_ptr(), L.BUILD_L2_NORMALIZE | (0 if f32_cache else L.BUILD_ROUND_BF16),
+                   float(DEFAULT_EPS), s)
     torch.cuda.synchronize()
     return cfg, cache
 
@@ -580,9 +594,10 @@ def main():
     model = synthetic_model()
     t_build = time.perf_counter()
     f32_view = cfg.get("view") == "f32"
+    f32_cache = cfg.get("cache") == "f32"
     s1_mode = L.S1_FLOAT if f32_view else L.S1_INT8
     mcfg, cache = build_shard(model, X, lo, hi, seed=11, dev=dev, lib=lib, ctx=ctx,
-                              storage=L.STORE_S1_F32 if f32_view else None)
+                              storage=L.STORE_S1_F32 if f32_view else None, f32_cache=cfg.get("cache") == "f32")
     t_build = time.perf_counter() - t_build
     gating = GatingNetwork(Mlp(*model["user_net"]), Mlp(*model["item_net"]), Mlp(*model["cross_net"]))
     gh = _gating_handle(gating)
@@ -615,7 +630,8 @@ def main():
         from paper_2306_04039_b200.mol import QueryState, mol_top_k
         from paper_2306_04039_b200.numerics import make_rng
 
-        hc = OH(k_prime=cfg["k_prime"], sample_ratio=cfg["ratio"], quantized=True)
+        # (the exact configs never call it: they have no h-indexer)
+        hc = None if exact else OH(k_prime=cfg["k_prime"], sample_ratio=cfg["ratio"], quantized=True)
 
         def run(u):
             cand = oh(view_holder["view"], ref_ue[u].mean(axis=0), hc, make_rng([9000, int(u)])).indices
@@ -890,10 +906,11 @@ def main():
                  "per_unit": f"{PAIR_FLOPS} tensor FLOPs per (user, item) pair", "peak_src": pk["src"],
                  "note": "SFU/latency-bound (320 MUFU ops per pair); see DESIGN.md"}
         elif name in ("mol_score", "mol_score_tc"):
-            achieved = units * PAIR_BYTES / per_launch_s / 1e9
+            pb = PAIR_BYTES_F32C if f32_cache else PAIR_BYTES
+            achieved = units * pb / per_launch_s / 1e9
             r = {"kernel": name, "bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                  "frac": achieved / pk["hbm_gbs"], "traffic": None, "units_per_launch": units,
-                 "per_unit": f"{PAIR_BYTES} B per (query, candidate) pair", "peak_src": pk["src"]}
+                 "per_unit": f"{pb} B per (query, candidate) pair", "peak_src": pk["src"]}
         elif name == "stage1_filter_f16":
             achieved = units * S1_OPS / per_launch_s / 1e12
             r = {"kernel": name, "bound": "tensor", "achieved": achieved, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
@@ -927,12 +944,15 @@ def main():
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         # the arithmetic the path computes in (K1/K2): stage 1 int8 x int8 -> int32 (exact) or the
-        # fp16 pre-test + exact fp32 re-check; MoL: bf16 item components x (bf16 hi + lo) query split with
-        # fp32 accumulate, cross-net layer 1 bf16 (hi/lo bias), layer 2 fp16, SiLU via tanh.approx,
-        # combine / softmax / gated sum in fp32
+        # fp16 pre-test + exact fp32 re-check; MoL: bf16 item components (bf16 hi + lo for an f32 cache) x
+        # (bf16 hi + lo) query split with fp32 accumulate, cross-net layer 1 three bf16 hi/lo passes (hi/lo
+        # bias), layer 2 three fp16 hi/lo passes, SiLU as ex2 + rcp, combine / softmax / gated sum in fp32
         "dtype": ("stage1 " + ("fp16 pre-test + fp32 exact re-check" if f32_view else "int8 (int32 acc, exact)")
-                  + "; MoL bf16 x bf16-hi/lo (fp32 acc), cross-net L1 bf16 / L2 fp16, tanh.approx SiLU, fp32 softmax"),
-        "data": "synthetic (reference init convention model.py:121-163; bf16-representable item cache built on device)",
+                  + ("; MoL f32 cache as bf16 hi+lo x bf16-hi/lo" if f32_cache else "; MoL bf16 x bf16-hi/lo")
+                  + " (fp32 acc), cross-net L1 3-pass bf16 hi/lo / L2 3-pass fp16 hi/lo, ex2+rcp SiLU, fp32 softmax"),
+        "data": ("synthetic (reference init convention model.py:121-163; " +
+                 ("f32 item cache as the reference builds it (mol.py:294-326), built on device)" if f32_cache else
+                  "bf16-representable item cache built on device)")),
         "config": {"workload": cfg["label"], "items": X, "items_per_gpu": Xl, "batch": B, "k": k,
                    "k_prime": cfg["k_prime"], "k_prime_per_gpu": kp_local, "sample_ratio": cfg["ratio"],
                    "lambda_per_gpu": lam_local,

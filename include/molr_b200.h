@@ -117,6 +117,10 @@ int molr_cache_read(const molr_cache* cache, int64_t row0, int64_t n, float* ite
                     float* stage1_scales, void* stream);
 /* storage: the molr_storage bits the cache was built with */
 int molr_cache_info(const molr_cache* cache, int64_t* n_items, int* storage, int64_t* device_bytes);
+/* 1 if MoL scoring of this (cache, gating, k_u) runs on the fused tcgen05 kernel (production shape
+ * k_u = k_x = 8, d = 64, G = 64, H = 128; bf16-exact caches, or f32-stored caches through their
+ * bf16 hi + lo image), 0 if on the generic SIMT fp32 kernel; < 0 on a null argument. */
+int molr_mol_uses_tensor_cores(const molr_cache* cache, const molr_gating* gating, int k_u);
 
 /* Elementwise primitives (numerics.py:69-81): op 0 sigmoid (scipy expit), 1 silu, 2 silu_grad;
  * dtype 0 = f32, 2 = f64 (the input's NumPy dtype). */

@@ -50,6 +50,7 @@ SIGNATURES = {
     "molr_cache_destroy": [P],
     "molr_cache_build_rows": [P, L, L, I, P, I, P, P, P, I, P, P, P, I, F, P],
     "molr_cache_info": [P, P, P, P],
+    "molr_mol_uses_tensor_cores": [P, P, I],
     "molr_gating_create": [P, I, I, P, P, P, I, I, P, P, P, P],
     "molr_gating_destroy": [P],
     "molr_component_logits": [P, I, I, I, I, P, P, D, I, P, P],

@@ -88,6 +88,30 @@ __global__ void embs_to_bf16_kernel(const float* __restrict__ x, int64_t rows, i
   if (local_bad) atomicOr(bad, 1);
 }
 
+// f32 item components -> bf16 hi + lo images in the cache's pre-swizzled layout (hi at row r,
+// lo at row X + r): x = hi + lo to ~2^-17 relative
+__global__ void embs_to_hilo_kernel(const float* __restrict__ x, int64_t rows, int64_t row0, int64_t X, int k_x, int d,
+                                    __nv_bfloat16* __restrict__ hl) {
+  const int64_t ne = int64_t(k_x) * d;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows * ne; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / ne;
+    const int e = int(i % ne), b = e / d, k = e % d;
+    const float v = x[i];
+    const __nv_bfloat16 h = __float2bfloat16_rn(v);
+    const int64_t o = (row0 + r) * ne + emb_offset(b, k, d, true);
+    hl[o] = h;
+    hl[X * ne + o] = __float2bfloat16_rn(v - __bfloat162float(h));
+  }
+}
+
+int build_embs_hilo(molr_cache* c, int64_t row0, int64_t n, cudaStream_t s) {
+  if (!c->embs_hl || n <= 0) return MOLR_OK;
+  const int64_t ne = int64_t(c->k_x) * c->d;
+  embs_to_hilo_kernel<<<c->ctx->num_sms * 8, 256, 0, s>>>(c->embs_f32 + row0 * ne, n, row0, c->X, c->k_x, c->d, c->embs_hl);
+  MOLR_LAUNCHED(c->ctx);
+  return MOLR_OK;
+}
+
 __global__ void iota_kernel(int32_t* p, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     p[i] = int32_t(i);
@@ -349,6 +373,12 @@ int molr_cache_alloc(molr_ctx* ctx, int64_t X, int k_x, int d, int G, int d1, in
   size_t ne = size_t(X) * k_x * d;
   int st = (storage & MOLR_STORE_EMBS_F32) ? grab((void**)&c->embs_f32, ne * 4) : grab((void**)&c->embs_bf16, ne * 2);
   if (!st && c->embs_bf16 && k_x * d == 512 && X > 0) c->embs_tmap_ok = encode_rows_tmap(&c->embs_tmap, c->embs_bf16, X);
+  if (!st && c->embs_f32 && k_x == 8 && d == 64 && X > 0) {  // hi + lo image for the tensor-core scorer
+    st = grab((void**)&c->embs_hl, ne * 4);
+    if (!st)
+      c->embs_hl_tmap_ok = encode_rows_tmap(&c->embs_hi_tmap, c->embs_hl, X) &&
+                           encode_rows_tmap(&c->embs_lo_tmap, c->embs_hl + ne, X);
+  }
   if (!st && (storage & MOLR_STORE_GP_F32)) st = grab((void**)&c->gp_f32, size_t(X) * G * 4);
   if (!st && !(storage & MOLR_STORE_GP_F32)) st = grab((void**)&c->gp_bf16, size_t(X) * G * 2);
   if (!st && (storage & MOLR_STORE_S1_F32)) st = grab((void**)&c->s1_f32, size_t(X) * d1 * 4);
@@ -399,6 +429,7 @@ int molr_cache_fill(molr_cache* c, int64_t row0, int64_t n, const float* embs, c
       size_t off = size_t(row0 + r) * per_row;
       if (c->embs_f32) {
         MOLR_CUDA(cudaMemcpyAsync(c->embs_f32 + off, embs + r * per_row, size_t(m * per_row) * 4, cudaMemcpyDefault, s));
+        MOLR_TRY(build_embs_hilo(c, row0 + r, m, s));
       } else {
         In e;
         MOLR_TRY(e.stage(embs + r * per_row, size_t(m * per_row) * 4, s));
@@ -501,6 +532,7 @@ int molr_cache_destroy(molr_cache* c) {
   cudaSetDevice(c->ctx->device);
   cudaFree(c->embs_bf16);
   cudaFree(c->embs_f32);
+  cudaFree(c->embs_hl);
   cudaFree(c->gp_bf16);
   cudaFree(c->gp_f32);
   cudaFree(c->s1_f32);

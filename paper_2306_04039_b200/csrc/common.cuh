@@ -173,6 +173,14 @@ struct molr_cache {
   // TMA descriptor over item_embs as (X rows x 1 KB) for tile::gather4 loads (bf16, k_x*d = 512)
   alignas(64) CUtensorMap embs_tmap{};
   int embs_tmap_ok = 0;
+  // f32-stored item_embs (not bf16-representable, e.g. a reference-built cache, mol.py:322-324)
+  // with k_x * d = 512: a bf16 hi + lo image (x = hi + lo to ~2^-17) in the same pre-swizzled
+  // layout, hi rows [0, X) then lo rows [X, 2X), so the tensor-core scorer runs two component
+  // passes; TMA descriptors over each half
+  __nv_bfloat16* embs_hl = nullptr;
+  alignas(64) CUtensorMap embs_hi_tmap{};
+  alignas(64) CUtensorMap embs_lo_tmap{};
+  int embs_hl_tmap_ok = 0;
   int32_t* s1_perm = nullptr;
   int32_t* s1_inv = nullptr;
   std::atomic<int> s1_sealed{0};

@@ -275,8 +275,11 @@ __device__ __forceinline__ int64_t cand_id(const Id* __restrict__ ids, const Til
 struct Params {
   int B;
   float inv_tau;
-  const __nv_bfloat16* embs;  // (X, 8, 64) pre-swizzled item blocks
-  const __nv_bfloat16* gp;    // (X, 64)
+  const __nv_bfloat16* embs;  // (X, 8, 64) pre-swizzled item blocks (the hi image of an f32 cache)
+  const __nv_bfloat16* embs_lo;  // hl: the lo image (x = hi + lo), same layout
+  int hl;                     // f32 cache: two component passes (hi, lo) per item group
+  const __nv_bfloat16* gp;    // (X, 64) bf16, or null when gpf is set
+  const float* gpf;           // (X, 64) f32 gate pre-activations (f32-stored cache)
   const __nv_bfloat16* w1t;   // SW128 image (16 KB)
   const __nv_bfloat16* w2t;   // SW128 image (16 KB), followed by the residual image (16 KB)
   const __nv_bfloat16* w1b;   // interleave image (4 KB)
@@ -298,7 +301,8 @@ struct Params {
 
 template <class Id>
 __global__ void __launch_bounds__(64 + NE * 256 + 32 * NE, 1) mol_tc_kernel(Params P, const Id* __restrict__ ids,
-                                                                  const __grid_constant__ CUtensorMap tmap) {
+                                                                  const __grid_constant__ CUtensorMap tmap,
+                                                                  const __grid_constant__ CUtensorMap tmap_lo) {
   extern __shared__ __align__(1024) uint8_t sm[];
   const uint32_t sbase = smem_u32(sm);
   if ((sbase & 1023u) != 0u) __trap();  // SW128 operands need 1024-aligned atoms
@@ -392,20 +396,24 @@ __global__ void __launch_bounds__(64 + NE * 256 + 32 * NE, 1) mol_tc_kernel(Para
 #pragma unroll
       for (int g = 0; g < NGROUPS; ++g) {
         const int64_t x = __shfl_sync(0xffffffffu, xid[g >> 1], 16 * (g & 1) + (lane & 15));
-        mbar_wait(empty_bar(stage), phase ^ 1);
-        if (lane == 0) mbar_arrive_expect_tx(full_bar(stage), SZ_STAGE);
-        __syncwarp();
-        if (P.gather4) {  // 4 items (4 KB) per TMA request: lane l < 4 fetches items 4l .. 4l+3
-          const int r0 = __shfl_sync(0xffffffffu, int(x), (4 * lane) & 15), r1 = __shfl_sync(0xffffffffu, int(x), (4 * lane + 1) & 15);
-          const int r2 = __shfl_sync(0xffffffffu, int(x), (4 * lane + 2) & 15), r3 = __shfl_sync(0xffffffffu, int(x), (4 * lane + 3) & 15);
-          if (lane < 4) gather4_g2s(sbase + OFF_RING + stage * SZ_STAGE + lane * 4096, &tmap, r0, r1, r2, r3, full_bar(stage));
-        } else if (lane < GROUP) {
-          bulk_g2s(sbase + OFF_RING + stage * SZ_STAGE + lane * 1024, P.embs + x * (KX * D), 1024, full_bar(stage));
-        }
-        __syncwarp();
-        if (++stage == NSTAGE) {
-          stage = 0;
-          phase ^= 1;
+        for (int part = 0; part <= P.hl; ++part) {  // f32 cache: the group's hi blocks, then its lo blocks
+          mbar_wait(empty_bar(stage), phase ^ 1);
+          if (lane == 0) mbar_arrive_expect_tx(full_bar(stage), SZ_STAGE);
+          __syncwarp();
+          if (P.gather4) {  // 4 items (4 KB) per TMA request: lane l < 4 fetches items 4l .. 4l+3
+            const int r0 = __shfl_sync(0xffffffffu, int(x), (4 * lane) & 15), r1 = __shfl_sync(0xffffffffu, int(x), (4 * lane + 1) & 15);
+            const int r2 = __shfl_sync(0xffffffffu, int(x), (4 * lane + 2) & 15), r3 = __shfl_sync(0xffffffffu, int(x), (4 * lane + 3) & 15);
+            if (lane < 4)
+              gather4_g2s(sbase + OFF_RING + stage * SZ_STAGE + lane * 4096, part ? &tmap_lo : &tmap, r0, r1, r2, r3, full_bar(stage));
+          } else if (lane < GROUP) {
+            bulk_g2s(sbase + OFF_RING + stage * SZ_STAGE + lane * 1024, (part ? P.embs_lo : P.embs) + x * (KX * D), 1024,
+                     full_bar(stage));
+          }
+          __syncwarp();
+          if (++stage == NSTAGE) {
+            stage = 0;
+            phase ^= 1;
+          }
         }
       }
     }
@@ -419,6 +427,7 @@ __global__ void __launch_bounds__(64 + NE * 256 + 32 * NE, 1) mol_tc_kernel(Para
       int64_t ctile = blockIdx.x;
       int64_t kc = 0;
       int cgrp = -1;  // -1: waiting for D0 free + B0
+      int cpart = 0;  // f32 cache: 0 = the group's hi blocks, 1 = its lo blocks (accumulated)
       // per epilogue group chain: state 0 need L1 (a1_ready), 1 need L2 (a2_ready); use count
       int gstate[NE];
       uint32_t guse[NE];
@@ -447,13 +456,19 @@ __global__ void __launch_bounds__(64 + NE * 256 + 32 * NE, 1) mol_tc_kernel(Para
               const uint32_t a0 = sbase + OFF_RING + stage * SZ_STAGE;
 #pragma unroll
               for (int kk = 0; kk < 4; ++kk)
-                mma_bf16(tmem_base + TM_D0 + cgrp * 16, desc_sw128(a0 + kk * 32), desc_sw128(b0 + kk * 32), ID16, kk > 0);
+                mma_bf16(tmem_base + TM_D0 + cgrp * 16, desc_sw128(a0 + kk * 32), desc_sw128(b0 + kk * 32), ID16,
+                         (kk > 0 || cpart > 0) ? 1u : 0u);
               mma_commit(empty_bar(stage));
               if (++stage == NSTAGE) {
                 stage = 0;
                 rphase ^= 1;
               }
-              ++cgrp;
+              if (cpart < P.hl) {
+                ++cpart;
+              } else {
+                cpart = 0;
+                ++cgrp;
+              }
             }
             if (cgrp == NGROUPS) {
               mma_commit(gbar(int(kc & 1), 0));  // D0 of local tile kc complete -> group kc % 2
@@ -547,9 +562,9 @@ __global__ void __launch_bounds__(64 + NE * 256 + 32 * NE, 1) mol_tc_kernel(Para
       if (hf == 0 && p < G) UW[p] = __ldg(P.uw + (int64_t)t.b * G + p);
       // prefetch this row's gate pre-activations of this half (bf16 x 32 = 64 B)
       uint4 gpr[4];
-      {
-        const int64_t x = cand_id(ids, t, p < t.np ? p : 0);
-        const uint4* src = reinterpret_cast<const uint4*>(P.gp + x * G) + hf * 4;
+      const int64_t xrow = cand_id(ids, t, p < t.np ? p : 0);
+      if (!P.gpf) {
+        const uint4* src = reinterpret_cast<const uint4*>(P.gp + xrow * G) + hf * 4;
 #pragma unroll
         for (int m = 0; m < 4; ++m) gpr[m] = __ldg(src + m);
       }
@@ -605,7 +620,8 @@ __global__ void __launch_bounds__(64 + NE * 256 + 32 * NE, 1) mol_tc_kernel(Para
           TileCursor c2 = cur;
           const TileInfo u = tile_info(c2, nt, P.B, P.tile_pre, P.begin, P.end, P.X);
           const int64_t xn = cand_id(ids, u, p < u.np ? p : 0);
-          asm volatile("prefetch.global.L1 [%0];" ::"l"(P.gp + xn * G + hf * 32));
+          if (P.gpf) asm volatile("prefetch.global.L1 [%0];" ::"l"(P.gpf + xn * G + hf * 32));
+          else asm volatile("prefetch.global.L1 [%0];" ::"l"(P.gp + xn * G + hf * 32));
           if (hf == 0 && p < G) asm volatile("prefetch.global.L1 [%0];" ::"l"(P.uw + (int64_t)u.b * G + p));
         }
       }
@@ -657,11 +673,18 @@ __global__ void __launch_bounds__(64 + NE * 256 + 32 * NE, 1) mol_tc_kernel(Para
         TMEM_LD16(tg + TM_D2 + 32 * hf, v0);
         TMEM_LD16(tg + TM_D2 + 32 * hf + 16, v1);
         tmem_wait_ld();
+        const float4* gsrc = P.gpf ? reinterpret_cast<const float4*>(P.gpf + xrow * G + 32 * hf) : nullptr;
 #pragma unroll
         for (int m = 0; m < 32; ++m) {
           const int g = 32 * hf + m;
-          const uint32_t wv = (&gpr[m >> 3].x)[(m & 7) >> 1];
-          const float gpv = __uint_as_float((m & 1) ? (wv & 0xFFFF0000u) : (wv << 16));
+          float gpv;
+          if (gsrc) {  // f32 cache: the row (prefetched into L1 during the previous tile)
+            const float4 g4 = __ldg(gsrc + (m >> 2));
+            gpv = (m & 3) == 0 ? g4.x : (m & 3) == 1 ? g4.y : (m & 3) == 2 ? g4.z : g4.w;
+          } else {
+            const uint32_t wv = (&gpr[m >> 3].x)[(m & 7) >> 1];
+            gpv = __uint_as_float((m & 1) ? (wv & 0xFFFF0000u) : (wv << 16));
+          }
           const float d2 = __uint_as_float(m < 16 ? v0[m] : v1[m - 16]);
           const float x = silu_acc(fmaf(UW[g], gpv, d2));
           pre[m] = x;
@@ -732,7 +755,8 @@ __global__ void b0_image_kernel(int B, const float* __restrict__ ue, uint8_t* __
 
 bool mol_tc_supported(const molr_cache* c, const molr_gating* g, int k_u) {
   return c && g && k_u == 8 && c->k_x == 8 && c->d == 64 && c->G == 64 && g->G == 64 && g->H == 128 &&
-         c->embs_bf16 != nullptr && c->gp_bf16 != nullptr && g->w1t_bf16 != nullptr && !dev_knob("MOLR_DISABLE_TC");
+         (c->embs_bf16 != nullptr || (c->embs_hl != nullptr && c->embs_hl_tmap_ok)) &&
+         (c->gp_bf16 != nullptr || c->gp_f32 != nullptr) && g->w1t_bf16 != nullptr && !dev_knob("MOLR_DISABLE_TC");
 }
 
 __global__ void tile_prefix_kernel(int B, const int64_t* begin, const int64_t* end, int64_t X, int P, int64_t* pre);
@@ -757,8 +781,12 @@ int mol_score_tc(molr_ctx* ctx, const molr_cache* c, const molr_gating* g, int B
   P.B = B;
   P.b0img = b0.as<uint8_t>();
   P.inv_tau = 1.0f / tau;
-  P.embs = c->embs_bf16;
+  const bool hl = c->embs_bf16 == nullptr;  // f32-stored components: hi + lo image, two passes
+  P.hl = hl ? 1 : 0;
+  P.embs = hl ? c->embs_hl : c->embs_bf16;
+  P.embs_lo = hl ? c->embs_hl + size_t(c->X) * 512 : nullptr;
   P.gp = c->gp_bf16;
+  P.gpf = c->gp_bf16 ? nullptr : c->gp_f32;
   P.w1t = g->w1t_bf16;
   P.w2t = g->w2t_bf16;
   P.w1b = g->w1t_bf16 + 8192;
@@ -776,7 +804,7 @@ int mol_score_tc(molr_ctx* ctx, const molr_cache* c, const molr_gating* g, int B
     const char* e = dev_knob("MOLR_E1");
     P.e1_tanh = (e && e[0] == 't') ? 1 : 0;  // dev: the 1-MUFU tanh.approx SiLU (below tolerance when sharpened)
     const char* gm = dev_knob("MOLR_GATHER");
-    P.gather4 = (c->embs_tmap_ok && !(gm && gm[0] == 'b')) ? 1 : 0;
+    P.gather4 = ((hl ? c->embs_hl_tmap_ok : c->embs_tmap_ok) && !(gm && gm[0] == 'b')) ? 1 : 0;
   }
   Scratch trace;
   P.trace = nullptr;
@@ -790,7 +818,8 @@ int mol_score_tc(molr_ctx* ctx, const molr_cache* c, const molr_gating* g, int B
   const int smem = tc::SMEM_BYTES;
   MOLR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const int grid = (int)std::min<int64_t>(T, ctx->num_sms);
-  kern<<<grid, 64 + tc::NE * 256 + 32 * tc::NE, smem, s>>>(P, segs.ids, c->embs_tmap);
+  kern<<<grid, 64 + tc::NE * 256 + 32 * tc::NE, smem, s>>>(P, segs.ids, hl ? c->embs_hi_tmap : c->embs_tmap,
+                                                            hl ? c->embs_lo_tmap : c->embs_tmap);
   MOLR_LAUNCHED(ctx);
   if (trace_path) {  // dev tool: dump CTA 0's epilogue timeline
     std::vector<unsigned long long> h(65536);
@@ -812,6 +841,11 @@ template int mol_score_tc<int32_t>(molr_ctx*, const molr_cache*, const molr_gati
 }  // namespace molr
 
 using namespace molr;
+
+extern "C" int molr_mol_uses_tensor_cores(const molr_cache* c, const molr_gating* g, int k_u) {
+  if (!c || !g) return MOLR_ERR_INVALID;
+  return mol_tc_supported(c, g, k_u) ? 1 : 0;
+}
 
 // Weight operand images for the tensor-core path (built once per gating handle):
 //   W1T  [128 hidden rows j][64 K = logit g]      bf16, SW128 K-major   (16 KB)

@@ -542,6 +542,7 @@ int molr_index_select(molr_ctx* ctx, const molr_cache* c, int64_t n, const int64
     };
     g(c->embs_bf16, r->embs_bf16, int64_t(c->k_x) * c->d * 2);
     g(c->embs_f32, r->embs_f32, int64_t(c->k_x) * c->d * 4);
+    if (st == MOLR_OK && r->embs_hl) st = build_embs_hilo(r, 0, n, s);
     g(c->gp_bf16, r->gp_bf16, int64_t(c->G) * 2);
     g(c->gp_f32, r->gp_f32, int64_t(c->G) * 4);
     g(c->s1_f32, r->s1_f32, int64_t(c->d1) * 4);

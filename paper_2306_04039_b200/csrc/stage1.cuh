@@ -34,6 +34,8 @@ int encode_rows_tmap(CUtensorMap* tm, const void* base, int64_t rows);
 int chunk_minmax(molr_ctx* ctx, const float* scales, int64_t c0, int64_t c1, float2* mm, cudaStream_t s);
 int s1_update_chunk_mm(molr_cache* c, int64_t row0, int64_t n, cudaStream_t s);
 int s1_seal(molr_cache* c, cudaStream_t s);
+// rows [row0, row0 + n) of an f32-stored cache's bf16 hi + lo image, from its embs_f32 (abi.cu)
+int build_embs_hilo(molr_cache* c, int64_t row0, int64_t n, cudaStream_t s);
 // float view (MOLR_S1_FLOAT) on the tensor cores: bf16 MMA pre-test + exact fp32 re-check of the
 // band the bf16 rounding cannot decide (same candidate set as the fp32 scan)
 bool s1_bf_supported(const molr_cache* c, int mode);

@@ -587,8 +587,16 @@ def batch_mol_top_k(cache, gating: GatingNetwork, user_embs, user_feats, k: int,
     return out_ids, out_sc
 
 
+def uses_tensor_cores(cache, gating: GatingNetwork, k_u: Optional[int] = None) -> bool:
+    """Whether MoL scoring of this cache and gating runs on the fused tcgen05 kernel (the production
+    shape; bf16-exact caches directly, f32-stored caches such as a reference-built one through
+    their bf16 hi + lo image) rather than the generic SIMT fp32 kernel."""
+    k = cache.config.k_u if k_u is None else int(k_u)
+    return L.load().molr_mol_uses_tensor_cores(C.c_void_p(cache_handle(cache)), C.c_void_p(_gating_handle(gating)), k) == 1
+
+
 __all__ = [
     "MoLConfig", "Mlp", "GatingNetwork", "QueryState", "ItemCache", "DeviceItemCache", "component_logits",
     "decomposed_gating", "mol_score", "build_item_cache", "score_candidates", "batch_score_all", "mol_top_k",
-    "batch_mol_top_k",
+    "batch_mol_top_k", "uses_tensor_cores",
 ]
