@@ -218,21 +218,12 @@ __device__ __forceinline__ float rcp(float x) {
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-// SiLU with one MUFU (tanh.approx, ~5e-4 relative): kept for experiments; the production path
-// uses silu_acc because the hidden units are carried at ~2^-17 (hi/lo split) into layer 2
-// Hidden-layer SiLU, one MUFU, branch-free: x*sigmoid(x) = h + h*tanh(h), h = x/2.  Absolute
-// error <= |h| * 2^-11 (tanh.approx); the hidden units only feed the linear layer W2, where
-// absolute error is what matters.
-__device__ __forceinline__ float silu_tanh(float x) {
-  const float h = 0.5f * x;
-  return fmaf(h, fast_tanh(h), h);
-}
-__device__ __forceinline__ float silu_fast(float x) {
-  float h = 0.5f * x;
-  return fmaf(h, fast_tanh(h), h);
-}
-// SiLU as x * rcp(1 + 2^(-x log2 e)) with ex2 + rcp (~1e-7 relative)
-__device__ __forceinline__ float silu_acc(float x) { return x * rcp(1.0f + ex2(-1.4426950408889634f * x)); }
+// The cross net and the combine run in "log2 units": layer 1's weights and bias, and uw, carry a
+// factor -log2(e) (folded into the weight images / the per-query uw load), so with x' = -log2(e) x
+//   sigmoid(x) = 1 / (1 + 2^x'),  -log2(e) silu(x) = x' / (1 + 2^x')
+// and the hidden units h' = -log2(e) h make layer 2 return -log2(e) D2 with W2 unchanged.  One
+// ex2 + one rcp per SiLU (~1e-7 relative), no scaling multiplies.
+__device__ __forceinline__ float silu_l2(float xs) { return xs * rcp(1.0f + ex2(xs)); }
 
 // SW128 K-major byte offset of 16-byte chunk `c` of row `r` within a [rows x 128 B] region.
 __device__ __forceinline__ uint32_t sw128(int r, int c) { return (r >> 3) * 1024 + (r & 7) * 128 + ((c ^ (r & 7)) << 4); }
@@ -294,12 +285,11 @@ struct Params {
   const uint8_t* b0img;       // (B, 2048) per-query B0 operand images (b0_image_kernel)
   float* out;
   int64_t out_ld;
-  int e1_tanh;  // hidden SiLU via tanh.approx (1 MUFU) instead of ex2 + rcp (2 MUFU)
   unsigned long long* trace;  // dev tool (MOLR_TRACE_MOL): CTA 0 epilogue timeline, else null
   int gather4;  // item fetch by TMA tile::gather4 (4 items per request) instead of 1 KB bulk copies
 };
 
-template <class Id>
+template <class Id, bool GPF>
 __global__ void __launch_bounds__(64 + NE * 256 + 32 * NE, 1) mol_tc_kernel(Params P, const Id* __restrict__ ids,
                                                                   const __grid_constant__ CUtensorMap tmap,
                                                                   const __grid_constant__ CUtensorMap tmap_lo) {
@@ -559,15 +549,12 @@ __global__ void __launch_bounds__(64 + NE * 256 + 32 * NE, 1) mol_tc_kernel(Para
     TileCursor cur;
     for (int64_t tile = blockIdx.x + (int64_t)eg * gridDim.x; tile < T; tile += (int64_t)NE * gridDim.x) {
       const TileInfo t = tile_info(cur, tile, P.B, P.tile_pre, P.begin, P.end, P.X);
-      if (hf == 0 && p < G) UW[p] = __ldg(P.uw + (int64_t)t.b * G + p);
-      // prefetch this row's gate pre-activations of this half (bf16 x 32 = 64 B)
+      if (hf == 0 && p < G) UW[p] = -1.4426950408889634f * __ldg(P.uw + (int64_t)t.b * G + p);  // log2 units
       uint4 gpr[4];
       const int64_t xrow = cand_id(ids, t, p < t.np ? p : 0);
-      if (!P.gpf) {
-        const uint4* src = reinterpret_cast<const uint4*>(P.gp + xrow * G) + hf * 4;
-#pragma unroll
-        for (int m = 0; m < 4; ++m) gpr[m] = __ldg(src + m);
-      }
+      // this row's gate pre-activations into L1 now, read in E2 (holding them in registers through
+      // the tile spilled)
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(GPF ? (const void*)(P.gpf + xrow * G + hf * 32) : (const void*)(P.gp + xrow * G + hf * 32)));
       // ---- E0: component logits (shared D0) -> CL (transpose to one row per pair); free D0 ----
       TRACE(0);
       mbar_wait(gbar(eg, 0), ph);
@@ -620,7 +607,7 @@ __global__ void __launch_bounds__(64 + NE * 256 + 32 * NE, 1) mol_tc_kernel(Para
           TileCursor c2 = cur;
           const TileInfo u = tile_info(c2, nt, P.B, P.tile_pre, P.begin, P.end, P.X);
           const int64_t xn = cand_id(ids, u, p < u.np ? p : 0);
-          if (P.gpf) asm volatile("prefetch.global.L1 [%0];" ::"l"(P.gpf + xn * G + hf * 32));
+          if (GPF) asm volatile("prefetch.global.L1 [%0];" ::"l"(P.gpf + xn * G + hf * 32));
           else asm volatile("prefetch.global.L1 [%0];" ::"l"(P.gp + xn * G + hf * 32));
           if (hf == 0 && p < G) asm volatile("prefetch.global.L1 [%0];" ::"l"(P.uw + (int64_t)u.b * G + p));
         }
@@ -648,7 +635,7 @@ __global__ void __launch_bounds__(64 + NE * 256 + 32 * NE, 1) mol_tc_kernel(Para
 #pragma unroll
           for (int m = 0; m < 8; ++m) {
             const float x0 = __uint_as_float(v[2 * m]), x1 = __uint_as_float(v[2 * m + 1]);
-            const float h0 = P.e1_tanh ? silu_tanh(x0) : silu_acc(x0), h1 = P.e1_tanh ? silu_tanh(x1) : silu_acc(x1);
+            const float h0 = silu_l2(x0), h1 = silu_l2(x1);  // -log2(e) silu(D1)
             const __half2 hh = __floats2half2_rn(h0, h1);
             const float2 hb = __half22float2(hh);
             w[m] = *reinterpret_cast<const uint32_t*>(&hh);
@@ -666,19 +653,27 @@ __global__ void __launch_bounds__(64 + NE * 256 + 32 * NE, 1) mol_tc_kernel(Para
       mbar_wait(gbar(eg, 4), ph);
       TRACE(6);
       tc_fence_after();
+      // pre = silu(x), x = uw gate_pre + D2 (mol.py:186-193); t = x' sigmoid(x) = -log2(e) pre, so the
+      // softmax is 2^(min t - t) / sum
       float pre[32];
-      float mx = -INFINITY;
+      float mx = INFINITY;
       {
         uint32_t v0[16], v1[16];
         TMEM_LD16(tg + TM_D2 + 32 * hf, v0);
         TMEM_LD16(tg + TM_D2 + 32 * hf + 16, v1);
         tmem_wait_ld();
-        const float4* gsrc = P.gpf ? reinterpret_cast<const float4*>(P.gpf + xrow * G + 32 * hf) : nullptr;
+        // GPF (f32 cache): the row, prefetched into L1 during the previous tile
+        const float4* gsrc = GPF ? reinterpret_cast<const float4*>(P.gpf + xrow * G + 32 * hf) : nullptr;
+        if (!GPF) {
+          const uint4* src = reinterpret_cast<const uint4*>(P.gp + xrow * G) + hf * 4;
+#pragma unroll
+          for (int m = 0; m < 4; ++m) gpr[m] = __ldg(src + m);
+        }
 #pragma unroll
         for (int m = 0; m < 32; ++m) {
           const int g = 32 * hf + m;
           float gpv;
-          if (gsrc) {  // f32 cache: the row (prefetched into L1 during the previous tile)
+          if (GPF) {
             const float4 g4 = __ldg(gsrc + (m >> 2));
             gpv = (m & 3) == 0 ? g4.x : (m & 3) == 1 ? g4.y : (m & 3) == 2 ? g4.z : g4.w;
           } else {
@@ -686,15 +681,14 @@ __global__ void __launch_bounds__(64 + NE * 256 + 32 * NE, 1) mol_tc_kernel(Para
             gpv = __uint_as_float((m & 1) ? (wv & 0xFFFF0000u) : (wv << 16));
           }
           const float d2 = __uint_as_float(m < 16 ? v0[m] : v1[m - 16]);
-          const float x = silu_acc(fmaf(UW[g], gpv, d2));
+          const float x = silu_l2(fmaf(UW[g], gpv, d2));
           pre[m] = x;
-          mx = fmaxf(mx, x);
+          mx = fminf(mx, x);
         }
       }
       XR[hf] = mx;
       named_sync(bar_id, NT);
-      mx = fmaxf(XR[0], XR[1]);
-      const float ml = mx * 1.4426950408889634f;
+      mx = fminf(XR[0], XR[1]);
       float sum = 0.f, acc = 0.f;
       const float4* row = reinterpret_cast<const float4*>(CL + p * CL_LD + 32 * hf);
 #pragma unroll
@@ -703,7 +697,7 @@ __global__ void __launch_bounds__(64 + NE * 256 + 32 * NE, 1) mol_tc_kernel(Para
         const float cv[4] = {c.x, c.y, c.z, c.w};
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          const float e = ex2(fmaf(pre[m4 * 4 + i], 1.4426950408889634f, -ml));
+          const float e = ex2(mx - pre[m4 * 4 + i]);
           sum += e;
           acc = fmaf(e, cv[i], acc);
         }
@@ -801,8 +795,6 @@ int mol_score_tc(molr_ctx* ctx, const molr_cache* c, const molr_gating* g, int B
   P.out = out;
   P.out_ld = out_ld;
   {
-    const char* e = dev_knob("MOLR_E1");
-    P.e1_tanh = (e && e[0] == 't') ? 1 : 0;  // dev: the 1-MUFU tanh.approx SiLU (below tolerance when sharpened)
     const char* gm = dev_knob("MOLR_GATHER");
     P.gather4 = ((hl ? c->embs_hl_tmap_ok : c->embs_tmap_ok) && !(gm && gm[0] == 'b')) ? 1 : 0;
   }
@@ -814,7 +806,7 @@ int mol_score_tc(molr_ctx* ctx, const molr_cache* c, const molr_gating* g, int B
     MOLR_CUDA(cudaMemsetAsync(trace.p, 0, 8, s));
     P.trace = trace.as<unsigned long long>();
   }
-  auto kern = tc::mol_tc_kernel<Id>;
+  auto kern = P.gpf ? tc::mol_tc_kernel<Id, true> : tc::mol_tc_kernel<Id, false>;
   const int smem = tc::SMEM_BYTES;
   MOLR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const int grid = (int)std::min<int64_t>(T, ctx->num_sms);
@@ -862,16 +854,19 @@ extern "C" int molr_gating_tc_prepare(molr_gating* g) {
   auto sw = [](int r, int k) {  // element offset in an SW128 K-major [rows x 64] region
     return (r >> 3) * 512 + (r & 7) * 64 + ((((k >> 3) ^ (r & 7))) << 3) + (k & 7);
   };
+  // layer 1 in log2 units (see silu_l2): W1 and b1 times -log2(e), rounded once to f32, then split
+  const double nl2e = -1.4426950408889634;
   for (int j = 0; j < 128; ++j)
     for (int gg = 0; gg < 64; ++gg) {
-      const float x = w1[size_t(gg) * 128 + j];
+      const float x = float(nl2e * double(w1[size_t(gg) * 128 + j]));
       const __nv_bfloat16 hi = __float2bfloat16(x);
       img[sw(j, gg)] = hi;
       img[18432 + sw(j, gg)] = __float2bfloat16(x - __bfloat162float(hi));
     }
   for (int j = 0; j < 128; ++j) {
-    __nv_bfloat16 hi = __float2bfloat16(b1[j]);
-    __nv_bfloat16 lo = __float2bfloat16(b1[j] - __bfloat162float(hi));
+    const float bj = float(nl2e * double(b1[j]));
+    __nv_bfloat16 hi = __float2bfloat16(bj);
+    __nv_bfloat16 lo = __float2bfloat16(bj - __bfloat162float(hi));
     const int base = 8192 + (j >> 3) * 128 + (j & 7) * 8;  // ilv(j, 0) in elements (chunk 0: K 0..7)
     img[base + 0] = hi;
     img[base + 1] = lo;
