@@ -924,7 +924,7 @@ def main():
                  "frac": achieved / peak_i8, "traffic": None, "units_per_launch": units,
                  "per_unit": f"{S1_OPS} int8 ops per (query, row)",
                  "peak_src": f"2x {pk['src']} bf16 (int8 dense rate)",
-                 "note": "bound by the SIMT threshold test of every accumulator (~4.5 instr each), not the MMA"}
+                 "note": "bound by the SIMT threshold test of every accumulator (ALU pipe, ~3.2 instr each), not the MMA"}
         else:
             return None
         if args.config == "100m" and world == 1:  # the committed capture is of the 100M N=1 step
