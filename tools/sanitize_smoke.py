@@ -51,4 +51,15 @@ h = HIndexerConfig(k_prime=KP, sample_ratio=0.2, quantized=True)
 res = _run_shards(lambda r, ex: two_stage_top_k_sharded(shards[r], gating, ue, uw, 20, h, X_global=X, row_lo=cuts[r],
                                                         exchange=ex, seed=1), 2)
 assert np.array_equal(res[0][0], ids) and np.array_equal(res[0][2], cand)
-print("sanitize smoke OK", int(cand.sum()), int(c2.sum()), int(c3.sum()))
+# round 2: an f32-stored (reference-built) cache on the tensor-core scorer (hi + lo component
+# image, f32 gate pre-activations), through the batched exact top-k and the two-stage path
+from tests.test_gpu_parity import _f32_prod_cache  # noqa: E402
+from paper_2306_04039_b200.mol import uses_tensor_cores  # noqa: E402
+
+fcache, fsyn, fue, ffeats = _f32_prod_cache(int(os.environ.get("SAN_X", 8_000)), seed=5, n_users=8)
+fgating, _ = _prod_gating(fsyn)
+assert uses_tensor_cores(fcache, fgating)
+fi, fs = batch_mol_top_k(fcache, fgating, fue, ffeats, 20)
+two_stage_top_k(fcache, fgating, fue, fgating.user_net(ffeats), 20, HIndexerConfig(k_prime=KP, sample_ratio=0.2,
+                                                                                  quantized=True), seed=4)
+print("sanitize smoke OK", int(cand.sum()), int(c2.sum()), int(c3.sum()), int(fi.sum()))
