@@ -270,8 +270,9 @@ int molr_query_prep(molr_ctx* ctx, int B, int d_u, const float* feats, int proj_
   auto mlp = [&](int hidden, const In& w1, const In& bb, const In& w2, int out_dim, float* out) -> int {
     const size_t smem = size_t(d_u + hidden) * 4;
     MOLR_CUDA(cudaFuncSetAttribute(mlp_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    mlp_forward_kernel<<<std::min(B, ctx->num_sms * 8), 128, smem, s>>>(B, d_u, hidden, out_dim, w1.as<float>(),
-                                                                      bb.as<float>(), w2.as<float>(), x.as<float>(), out);
+    const dim3 grid(std::min(B, ctx->num_sms * 8), std::min(div_up(out_dim, 128), std::max(1, ctx->num_sms / std::max(B, 1))));
+    mlp_forward_kernel<<<grid, 128, smem, s>>>(B, d_u, hidden, out_dim, w1.as<float>(), bb.as<float>(), w2.as<float>(),
+                                               x.as<float>(), out);
     MOLR_LAUNCHED(ctx);
     return MOLR_OK;
   };

@@ -45,7 +45,9 @@ __global__ void mlp_forward_kernel(int rows, int in_dim, int hidden, int out_dim
       hs[j] = silu_f32(acc + b1[j]);
     }
     __syncthreads();
-    for (int o = threadIdx.x; o < out_dim; o += blockDim.x) {
+    // gridDim.y blocks share a row's outputs (small batches: more blocks in flight; every block
+    // recomputes the same hidden layer, so results do not depend on the split)
+    for (int o = blockIdx.y * blockDim.x + threadIdx.x; o < out_dim; o += gridDim.y * blockDim.x) {
       float acc = 0.f;
       for (int j = 0; j < hidden; ++j) acc = fmaf(hs[j], w2[int64_t(j) * out_dim + o], acc);
       out[int64_t(r) * out_dim + o] = acc;

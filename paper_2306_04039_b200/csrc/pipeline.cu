@@ -132,16 +132,24 @@ __global__ void cap_segs_kernel(int B, int64_t cap, const int64_t* __restrict__ 
   }
 }
 
-// gather sampled stage-1 rows (codes interleaved + scales) into a contiguous padded operand
+// gather sampled stage-1 rows (codes interleaved + scales) into a contiguous operand padded to
+// n_pad rows (the padding rows are zeroed here): one thread per row, its four 16-B chunks loaded
+// together (the idx -> inv -> row chain is paid once per row, not once per chunk)
 __global__ void gather_sample_kernel(const int8_t* __restrict__ codes, const float* __restrict__ scales,
                                      const int32_t* __restrict__ inv, const int64_t* __restrict__ idx, int64_t n,
-                                     int8_t* __restrict__ dcodes, float* __restrict__ dscales) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * 4; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i >> 2;
-    const int c = int(i & 3);
-    const int64_t src = inv ? inv[idx[r]] : idx[r];
-    *reinterpret_cast<int4*>(dcodes + s1_chunk_offset(r, c, 64)) = *reinterpret_cast<const int4*>(codes + s1_chunk_offset(src, c, 64));
-    if (c == 0) dscales[r] = scales[src];
+                                     int64_t n_pad, int8_t* __restrict__ dcodes, float* __restrict__ dscales) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_pad; r += (int64_t)gridDim.x * blockDim.x) {
+    int4 v[4] = {make_int4(0, 0, 0, 0), make_int4(0, 0, 0, 0), make_int4(0, 0, 0, 0), make_int4(0, 0, 0, 0)};
+    float sc = 0.f;
+    if (r < n) {
+      const int64_t src = inv ? inv[idx[r]] : idx[r];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) v[c] = __ldg(reinterpret_cast<const int4*>(codes + s1_chunk_offset(src, c, 64)));
+      sc = __ldg(scales + src);
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) *reinterpret_cast<int4*>(dcodes + s1_chunk_offset(r, c, 64)) = v[c];
+    dscales[r] = sc;
   }
 }
 
@@ -654,8 +662,7 @@ static int two_stage_impl(molr_ctx* ctx, const molr_cache* c, const molr_gating*
         while ((int64_t(1) << bits) < X) bits += 2;
         Scratch samp;
         MOLR_TRY(samp.alloc(size_t(lam) * 8, s));
-        feistel_sample_kernel<<<std::min(div_up(lam, 256), ctx->num_sms * 8), 256, 0, s>>>(X, lam, seed, bits / 2,
-                                                                                           samp.as<int64_t>());
+        feistel_sample_kernel<<<div_up(lam, 256), 256, 0, s>>>(X, lam, seed, bits / 2, samp.as<int64_t>());
         MOLR_LAUNCHED(ctx);
         // 3. n-th largest sampled score per query
         const double nr = std::nearbyint(double(k_prime * lam) / double(X));  // Python round(): half-even
@@ -666,10 +673,8 @@ static int two_stage_impl(molr_ctx* ctx, const molr_cache* c, const molr_gating*
           Scratch scodes, sscales;
           MOLR_TRY(scodes.alloc(size_t(lp) * 64, s));
           MOLR_TRY(sscales.alloc(size_t(lp) * 4, s));
-          MOLR_CUDA(cudaMemsetAsync(scodes.p, 0, size_t(lp) * 64, s));
-          MOLR_CUDA(cudaMemsetAsync(sscales.p, 0, size_t(lp) * 4, s));
-          gather_sample_kernel<<<std::min(div_up(lam * 4, 256), ctx->num_sms * 8), 256, 0, s>>>(
-              c->s1_codes, c->s1_scales, c->s1_inv, samp.as<int64_t>(), lam, scodes.as<int8_t>(), sscales.as<float>());
+          gather_sample_kernel<<<div_up(lp, 256), 256, 0, s>>>(c->s1_codes, c->s1_scales, c->s1_inv, samp.as<int64_t>(), lam,
+                                                              lp, scodes.as<int8_t>(), sscales.as<float>());
           MOLR_LAUNCHED(ctx);
           MOLR_TRY(sample_threshold_tc(ctx, mode, scodes.as<int8_t>(), sscales.as<float>(), lam, B, qc.as<int8_t>(),
                                        n_rank, ss, tkey.as<uint32_t>(), s, full_sample, dflags.as<int>(), &dpilot));
@@ -872,8 +877,7 @@ int molr_sample_top_keys(molr_ctx* ctx, const molr_cache* c, int B, int k_u, con
   MOLR_TRY(samp.alloc(size_t(lam) * 8, s));
   MOLR_TRY(loc.alloc(size_t(lam) * 8, s));
   MOLR_TRY(cnt.alloc(8, s));
-  feistel_sample_kernel<<<std::min(div_up(lam, 256), ctx->num_sms * 8), 256, 0, s>>>(X_global, lam, seed, bits / 2,
-                                                                                     samp.as<int64_t>());
+  feistel_sample_kernel<<<div_up(lam, 256), 256, 0, s>>>(X_global, lam, seed, bits / 2, samp.as<int64_t>());
   MOLR_LAUNCHED(ctx);
   MOLR_CUDA(cudaMemsetAsync(cnt.p, 0, 8, s));
   shard_rows_kernel<<<std::min(div_up(lam, 256), ctx->num_sms * 8), 256, 0, s>>>(lam, samp.as<int64_t>(), row_lo,
@@ -893,11 +897,9 @@ int molr_sample_top_keys(molr_ctx* ctx, const molr_cache* c, int B, int k_u, con
       Scratch scodes, sscales;
       MOLR_TRY(scodes.alloc(size_t(lp) * 64, s));
       MOLR_TRY(sscales.alloc(size_t(lp) * 4, s));
-      MOLR_CUDA(cudaMemsetAsync(scodes.p, 0, size_t(lp) * 64, s));
-      MOLR_CUDA(cudaMemsetAsync(sscales.p, 0, size_t(lp) * 4, s));
       MOLR_TRY(s1_seal(const_cast<molr_cache*>(c), s));
-      gather_sample_kernel<<<std::min(div_up(m * 4, 256), ctx->num_sms * 8), 256, 0, s>>>(
-          c->s1_codes, c->s1_scales, c->s1_inv, loc.as<int64_t>(), m, scodes.as<int8_t>(), sscales.as<float>());
+      gather_sample_kernel<<<div_up(lp, 256), 256, 0, s>>>(c->s1_codes, c->s1_scales, c->s1_inv, loc.as<int64_t>(), m, lp,
+                                                          scodes.as<int8_t>(), sscales.as<float>());
       MOLR_LAUNCHED(ctx);
       // pilot (as sample_threshold_tc): a low threshold t0 from the first lam0 local sample rows, the
       // fused filter keeps the keys >= t0, and the nk-th largest of those is the shard's nk-th

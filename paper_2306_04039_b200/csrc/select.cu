@@ -119,15 +119,24 @@ __global__ void __launch_bounds__(kSelThreads)
 segmented_topk_kernel(int B, const int64_t* __restrict__ begin, const int64_t* __restrict__ end,
                       const Id* __restrict__ ids, int64_t X, const float* __restrict__ scores, int64_t dense_ld,
                       int k, int64_t id_offset, uint64_t* __restrict__ spill, int64_t spill_ld,
-                      int64_t* __restrict__ out_ids, float* __restrict__ out_scores) {
+                      int64_t* __restrict__ out_ids, float* __restrict__ out_scores, int P) {
   __shared__ uint32_t hist[256];
   __shared__ uint64_t buf[kSortCap];
   __shared__ int s_count;
-  const int b = blockIdx.x;
-  const int64_t seg0 = begin ? begin[b] : 0;
-  const int64_t n = begin ? end[b] - begin[b] : X;
-  const float* sc = begin ? scores + seg0 : scores + int64_t(b) * dense_ld;
-  const Id* id = ids ? ids + seg0 : nullptr;
+  // P > 1 (small batches): P CTAs per query, CTA p takes slice p of the segment and writes its
+  // top-k as list p of a rank-major (P, B, k) array for merge_topk_kernel
+  const int b = blockIdx.x / P, part = blockIdx.x % P;
+  int64_t seg0 = begin ? begin[b] : 0;
+  int64_t n = begin ? end[b] - begin[b] : X;
+  const int64_t sub0 = n * part / P, sub1 = n * (part + 1) / P;
+  const float* sc = begin ? scores + seg0 + sub0 : scores + int64_t(b) * dense_ld + sub0;
+  const Id* id = ids ? ids + seg0 + sub0 : nullptr;
+  const uint32_t id_base = ids ? 0u : uint32_t(sub0);
+  n = sub1 - sub0;
+  if (P > 1) {
+    out_ids += int64_t(part) * B * k;
+    out_scores += int64_t(part) * B * k;
+  }
   const int kk = (int)imin64(k, n);
   // a segment shorter than k: the tail is "no entry" (id -1, score -inf; merge_topk drops it)
   for (int i = max(kk, 0) + threadIdx.x; i < k; i += blockDim.x) {
@@ -135,7 +144,7 @@ segmented_topk_kernel(int B, const int64_t* __restrict__ begin, const int64_t* _
     out_scores[int64_t(b) * k + i] = -INFINITY;
   }
   if (kk <= 0) return;
-  auto idof = [&](int64_t i) -> uint32_t { return id ? (uint32_t)id[i] : (uint32_t)i; };
+  auto idof = [&](int64_t i) -> uint32_t { return id ? (uint32_t)id[i] : id_base + (uint32_t)i; };
   // ---- fast path: sampled bound + one filtering pass ----------------------------------------
   // bound = the r-th largest of every 16th score, r ~ 4 sigma above the expected number of
   // samples beating the k-th largest, so bound <= k-th largest with overwhelming probability.
@@ -227,6 +236,9 @@ segmented_topk_kernel(int B, const int64_t* __restrict__ begin, const int64_t* _
   }
 }
 
+__global__ void merge_topk_kernel(int P, int B, int k_in, const int64_t* __restrict__ ids, const float* __restrict__ sc,
+                                  int k, int64_t* __restrict__ out_ids, float* __restrict__ out_sc);
+
 template <class Id>
 int segmented_top_k(molr_ctx* ctx, int B, Segs<Id> segs, const float* scores, int64_t dense_ld, int k,
                     int64_t id_offset, int64_t* out_ids, float* out_scores, cudaStream_t s) {
@@ -237,9 +249,28 @@ int segmented_top_k(molr_ctx* ctx, int B, Segs<Id> segs, const float* scores, in
     spill_ld = next_pow2(k);
     MOLR_TRY(spill.alloc(size_t(B) * spill_ld * 8, s));
   }
+  // small batches: one CTA per query leaves the GPU idle while it walks ~K' scores; split each
+  // query over P CTAs (slices), then merge the P top-k lists (exact: the top-k of a union of the
+  // slices' top-k lists under the same (score desc, id asc) order is the top-k of the whole).
+  // At most 8 slices: each stays long enough for the sampled-bound fast path (n >= 32 k)
+  const int P = (spill_ld == 0 && 4 * B <= ctx->num_sms)
+                    ? std::max(1, std::min(std::min(ctx->num_sms / B, 8), int(kSortCap / std::max(k, 1))))
+                    : 1;
+  if (P > 1) {
+    Scratch pi, ps;
+    MOLR_TRY(pi.alloc(size_t(P) * B * k * 8, s));
+    MOLR_TRY(ps.alloc(size_t(P) * B * k * 4, s));
+    segmented_topk_kernel<Id><<<B * P, kSelThreads, 0, s>>>(B, segs.begin, segs.end, segs.ids, segs.X, scores,
+                                                            dense_ld, k, id_offset, nullptr, 0, pi.as<int64_t>(),
+                                                            ps.as<float>(), P);
+    MOLR_LAUNCHED(ctx);
+    merge_topk_kernel<<<B, 256, 0, s>>>(P, B, k, pi.as<int64_t>(), ps.as<float>(), k, out_ids, out_scores);
+    MOLR_LAUNCHED(ctx);
+    return MOLR_OK;
+  }
   segmented_topk_kernel<Id><<<B, kSelThreads, 0, s>>>(B, segs.begin, segs.end, segs.ids, segs.X, scores,
                                                       dense_ld, k, id_offset, spill.as<uint64_t>(), spill_ld,
-                                                      out_ids, out_scores);
+                                                      out_ids, out_scores, 1);
   MOLR_LAUNCHED(ctx);
   return MOLR_OK;
 }
