@@ -246,8 +246,10 @@ def test_stage1_scores_bit_exact(prod):
         raw = stage1_scores(cache.stage1_q, q, raw_int_ordering=True)
         assert raw.dtype == np.int32 and np.array_equal(raw, g["s1_raw"][u])
         assert np.array_equal(stage1_scores(cache.stage1_q, q), g["s1_scaled"][u])
-        np.testing.assert_allclose(stage1_scores(cache.stage1_embs, q), g["s1_float"][u], rtol=1e-5, atol=1e-7)
+        # the float view's dot in OpenBLAS's sgemv order: the reference's fp32 `view @ q` bit for bit
+        assert np.array_equal(stage1_scores(cache.stage1_embs, q), g["s1_float"][u])
         assert exact_top_k(cache.stage1_q, q, 50).tolist() == g["exact_top_k_q"][u].tolist()
+        assert exact_top_k(cache.stage1_embs, q, 50).tolist() == g["exact_top_k_f"][u].tolist()
 
 
 @pytest.mark.parametrize("tag,cfg_kw,view", [
