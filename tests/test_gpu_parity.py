@@ -965,3 +965,12 @@ def test_tc_kernel_f32_cache(gate_f32, scale):
         ti, ts = mol_top_k(cache, gating, ids, q, 50)
         assert topk_equal_modulo_ties(ti, O.mol_top_k(oc, og, ids, ue[u], feats[u], 50)[0], np.where(
             np.isin(np.arange(cache.num_items), ids), ref[u], -np.inf))
+    # index_select of an f32 cache rebuilds the selection's hi + lo image: same scores, same backend
+    from paper_2306_04039_b200.hindexer import index_select
+
+    ids = np.sort(rng.choice(cache.num_items, size=777, replace=False))
+    sub = index_select(cache, ids)
+    assert uses_tensor_cores(sub, gating)
+    q = QueryState(user_embs=ue[0], gate_features=feats[0])
+    np.testing.assert_array_equal(score_candidates(sub, gating, np.arange(ids.size), q),
+                                  score_candidates(cache, gating, ids, q))
