@@ -76,6 +76,18 @@ PAIR_BYTES = K_X * D * 2 + G * 2 + 4       # bf16 item components + bf16 gate_pr
 PAIR_BYTES_F32C = K_X * D * 4 + G * 4 + 4  # f32 cache: bf16 hi + lo components + f32 gate_pre + id = 2308 B
 PAIR_FLOPS = 2 * (G * D + G * H + H * G)   # component GEMM + cross-net 64->128->64 = 40960
 S1_OPS = 2 * D                             # int8 MACs x 2 per (query, row)
+PAIR_MUFU = 2 * H + 2 * G + G              # ex2 + rcp per hidden / combine SiLU, ex2 per softmax term = 448
+
+
+def mufu_peak():
+    """Measured MUFU throughput (tools/mufu_bench.cu on this pool's B200: ex2 / rcp, all SMs),
+    else the nominal 16 per clock per SM at 1.965 GHz."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_mufu_bench.json")) as f:
+            v = [json.loads(l)["ops_per_s"] for l in f if l.strip()]
+        return min(v), "measured (profiles/r02_mufu_bench.json)"
+    except Exception:
+        return 16 * 148 * 1.965e9, "nominal 16/clk/SM x 148 SMs x 1.965 GHz"
 
 
 def peaks():
@@ -898,19 +910,23 @@ def main():
         units = work / cnt
         if name in ("mol_score", "mol_score_tc") and exact:
             # exact path: the item side is L2-resident (27K items x 1.15 KB), so the kernel is bound by
-            # the SFU (SiLU / exp per logit) and the epilogue chain, not HBM; reported against the bf16
-            # tensor peak with the per-pair tensor FLOPs
-            achieved = units * PAIR_FLOPS / per_launch_s / 1e12
-            r = {"kernel": name, "bound": "tensor", "achieved": achieved, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
-                 "frac": achieved / pk["bf16_tflops"], "traffic": None, "units_per_launch": units,
-                 "per_unit": f"{PAIR_FLOPS} tensor FLOPs per (user, item) pair", "peak_src": pk["src"],
-                 "note": "SFU/latency-bound (320 MUFU ops per pair); see DESIGN.md"}
+            # the SFU (ex2 / rcp for every SiLU and softmax term) and the epilogue chain, not HBM or the
+            # tensor pipe (K1)
+            mp, msrc = mufu_peak()
+            achieved = units * PAIR_MUFU / per_launch_s
+            r = {"kernel": name, "bound": "sfu", "achieved": achieved / 1e12, "peak": mp / 1e12, "unit": "Tops/s (MUFU)",
+                 "frac": achieved / mp, "traffic": None, "units_per_launch": units,
+                 "per_unit": f"{PAIR_MUFU} MUFU ops per (user, item) pair", "peak_src": msrc,
+                 "tensor_frac": units * PAIR_FLOPS / per_launch_s / 1e12 / pk["bf16_tflops"]}
         elif name in ("mol_score", "mol_score_tc"):
             pb = PAIR_BYTES_F32C if f32_cache else PAIR_BYTES
             achieved = units * pb / per_launch_s / 1e9
+            mp, _ = mufu_peak()
             r = {"kernel": name, "bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                  "frac": achieved / pk["hbm_gbs"], "traffic": None, "units_per_launch": units,
-                 "per_unit": f"{pb} B per (query, candidate) pair", "peak_src": pk["src"]}
+                 "per_unit": f"{pb} B per (query, candidate) pair", "peak_src": pk["src"],
+                 # the same kernel against the SFU: 448 MUFU ops per pair (K1)
+                 "sfu_frac": units * PAIR_MUFU / per_launch_s / mp}
         elif name == "stage1_filter_f16":
             achieved = units * S1_OPS / per_launch_s / 1e12
             r = {"kernel": name, "bound": "tensor", "achieved": achieved, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
