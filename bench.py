@@ -79,6 +79,21 @@ S1_OPS = 2 * D                             # int8 MACs x 2 per (query, row)
 PAIR_MUFU = 2 * H + 2 * G + G              # ex2 + rcp per hidden / combine SiLU, ex2 per softmax term = 448
 
 
+def tc_microbench_peaks():
+    """tcgen05 dense MMA rates measured by tools/tc_peak_bench.cu on this pool's B200 (one CTA per
+    SM, back-to-back M128 x N256 MMAs, max clock): {"i8": Tops/s, "f16": TFLOP/s}, or {}."""
+    out = {}
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_tc_peak_bench.json")) as f:
+            for l in f:
+                if l.strip():
+                    d = json.loads(l)
+                    out["i8" if "i8" in d["mma"] else "f16"] = d["tops_per_s"]
+    except Exception:
+        pass
+    return out
+
+
 def mufu_peak():
     """Measured MUFU throughput (tools/mufu_bench.cu on this pool's B200: ex2 / rcp, all SMs),
     else the nominal 16 per clock per SM at 1.965 GHz."""
@@ -933,6 +948,9 @@ def main():
                  "frac": achieved / pk["bf16_tflops"], "traffic": None, "units_per_launch": units,
                  "per_unit": f"{S1_OPS} fp16 flops per (query, row)", "peak_src": f"{pk['src']} bf16 (= fp16 dense rate)",
                  "note": "fp16 pre-test + exact fp32 re-check of the undecided band (DESIGN.md K2f)"}
+            tcp = tc_microbench_peaks()
+            if "f16" in tcp:  # the same against the tcgen05 rate measured by tools/tc_peak_bench.cu
+                r["frac_vs_tcgen05_microbench"] = achieved / tcp["f16"]
         elif name.startswith("stage1_filter"):
             achieved = units * S1_OPS / per_launch_s / 1e12
             peak_i8 = 2 * pk["bf16_tflops"]
@@ -941,6 +959,9 @@ def main():
                  "per_unit": f"{S1_OPS} int8 ops per (query, row)",
                  "peak_src": f"2x {pk['src']} bf16 (int8 dense rate)",
                  "note": "bound by the SIMT threshold test of every accumulator (ALU pipe, ~3.2 instr each), not the MMA"}
+            tcp = tc_microbench_peaks()
+            if "i8" in tcp:  # the same against the tcgen05 kind::i8 rate measured by tools/tc_peak_bench.cu
+                r["frac_vs_tcgen05_microbench"] = achieved / tcp["i8"]
         else:
             return None
         if args.config == "100m" and world == 1:  # the committed capture is of the 100M N=1 step
