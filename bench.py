@@ -942,6 +942,13 @@ def main():
                  "per_unit": f"{pb} B per (query, candidate) pair", "peak_src": pk["src"],
                  # the same kernel against the SFU: 448 MUFU ops per pair (K1)
                  "sfu_frac": units * PAIR_MUFU / per_launch_s / mp}
+            if cfg.get("k_prime"):
+                # item-major minimum: every distinct candidate item fetched once per batch; expected
+                # distinct items of B K' uniform-ish picks over the shard, Xl (1 - exp(-units / Xl))
+                # (SURVEY.md §8(d)); an analytic expectation, not a count
+                distinct = Xl * (1.0 - math.exp(-units / Xl))
+                r["item_major_min_bytes"] = distinct * pb
+                r["item_major_min_frac"] = distinct * pb / per_launch_s / 1e9 / pk["hbm_gbs"]
         elif name == "stage1_filter_f16":
             achieved = units * S1_OPS / per_launch_s / 1e12
             r = {"kernel": name, "bound": "tensor", "achieved": achieved, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
